@@ -1,0 +1,200 @@
+/*
+ * pgmoe.h — C ABI of the B200-native pre-gated MoE block (libpgmoe.so).
+ *
+ * Drop-in boundary for the reference package `moesim`
+ * (/root/reference/pkg/src/moesim).  Each entry point names the reference
+ * interface it replaces (file:line).  Plain pointers and sizes only: no
+ * torch types cross this boundary.  Activations are fp32, weights fp32 or
+ * bf16 (bf16 = RNE of the fp32 value the reference is fed).
+ *
+ * Conventions
+ *  - Every call returns a pgmoe_status.  Status codes map 1:1 onto the
+ *    reference exception tree (errors.py:4-33); see pgmoe_status below.
+ *  - Calls taking a `stream` are stream-ordered and asynchronous.  Errors
+ *    the device detects (non-finite logits, zero routing weight) are written
+ *    to the routing buffer's `status[0]` and surfaced by pgmoe_check_routing()
+ *    (or by the synchronous *_host entry points), i.e. at the next sync
+ *    point, not eagerly as Python raises them.
+ *  - Device pointers are caller-owned unless produced by a *_create call.
+ *  - No CPU fallback: every compute entry point launches sm_100a kernels.
+ */
+#ifndef PGMOE_H
+#define PGMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PGMOE_API __attribute__((visibility("default")))
+#else
+#define PGMOE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *pgmoe_stream_t; /* == cudaStream_t */
+
+/* errors.py:4-33 — the Python shim raises the same-named exception. */
+typedef enum {
+    PGMOE_OK = 0,
+    PGMOE_E_CONFIG = 1,          /* ConfigError          (core.py:54-70, :291) */
+    PGMOE_E_SHAPE = 2,           /* ShapeError           (core.py:293, :310)   */
+    PGMOE_E_GATE_OVERFLOW = 3,   /* GateOverflowError "numerical overflow in gate" (core.py:297) */
+    PGMOE_E_GATE_UNDERFLOW = 4,  /* GateOverflowError "gate routing weight underflowed to zero" (core.py:303) */
+    PGMOE_E_ROUTING = 5,         /* RoutingError         (core.py:110-140, :332, :369-382) */
+    PGMOE_E_OOM = 6,             /* OomError             (tiers.py:134-157; HBM exhausted) */
+    PGMOE_E_CUDA = 7,            /* MoESimError (device/runtime failure) */
+    PGMOE_E_NCCL = 8,            /* MoESimError (collective failure) */
+    PGMOE_E_WEIGHT_FILE = 9,     /* WeightFileError      (model_io.py:63-105) */
+    PGMOE_E_INVARIANT = 10       /* InvariantError       (scheduler.py:127-145) */
+} pgmoe_status;
+
+typedef enum { PGMOE_F32 = 0, PGMOE_BF16 = 1 } pgmoe_dtype;
+typedef enum { PGMOE_RESIDENT = 0, PGMOE_OFFLOADED = 1 } pgmoe_placement;
+typedef enum { PGMOE_KERNEL_AUTO = 0, PGMOE_KERNEL_SIMT = 1, PGMOE_KERNEL_TCGEN05 = 2 } pgmoe_kernel;
+
+/* core.py:34-70 ModelConfig (dtype_bytes is implied by the weight dtype). */
+typedef struct {
+    int32_t d_model, d_ff, num_blocks, num_experts, top_k, activation_level;
+    uint64_t seed;
+} pgmoe_config;
+
+/* Device routing buffers for T tokens (the batched RoutingDecision,
+ * core.py:110-140, plus the SURVEY §8 a8 permutation). */
+typedef struct {
+    int32_t *ids;    /* [T][k] expert ids, descending logit, ties -> lower id */
+    float *w;        /* [T][k] softmax probabilities of the selected experts */
+    int32_t *hist;   /* [E]    tokens routed to each expert */
+    int32_t *off;    /* [E+1]  exclusive scan of hist */
+    int32_t *perm;   /* [T*k]  entry index t*k+s grouped by expert, stable */
+    float *w_perm;   /* [T*k]  w of perm[r] */
+    int32_t *act;    /* [E]    active experts ascending (first *n_act valid) */
+    int32_t *n_act;  /* [1] */
+    int32_t *status; /* [4] [0] device error code, [1] tokens that needed the
+                        serial-fp64 recompute, [2] routing flips (0 by
+                        construction), [3] reserved */
+} pgmoe_routing;
+
+/* ---------------------------------------------------------------- kernels */
+
+/* Bytes of device scratch pgmoe_gate_forward needs for T tokens. */
+PGMOE_API size_t pgmoe_route_workspace_bytes(int32_t T, int32_t E);
+
+/* K1 pre-gate / route.  Replaces gate_forward (core.py:284-305) for T
+ * tokens at once, fused with the per-expert histogram, exclusive scan and
+ * stable permutation.  x: fp32 [T][d]; gate_w: [d][E] (in x out, as the
+ * reference stores it).  Ids are bit-exact with the reference's serial fp64
+ * logits (certified fast logits + serial fallback).  `workspace` must hold
+ * pgmoe_route_workspace_bytes(T, E) bytes, zeroed once before first use. */
+PGMOE_API int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const void *gate_w,
+                       int32_t wdtype, int32_t E, int32_t k, const pgmoe_routing *out,
+                       void *workspace, pgmoe_stream_t stream);
+
+/* K2 grouped expert FFN with fused combine.  Replaces expert_forward
+ * (core.py:308-316) x k plus weighted_sum (linalg.py:45-51): for every
+ * routed entry r, yw[perm[r]] = w_perm[r] * W2 relu(W1 x[perm[r]/k]).
+ * Expert e's weights live at experts + slot(e) * expert_stride bytes with
+ * W1 [f][d] first and W2 [d][f] after it; slot(e) = e when
+ * `indexed_by_act` == 0 (resident), else its position i in act (slot cache).
+ * h: fp32 scratch [T*k][f]; yw: fp32 [T*k][d]. */
+PGMOE_API int pgmoe_expert_forward(const float *x, int32_t T, int32_t d, int32_t f, int32_t k,
+                         const void *experts, size_t expert_stride, int32_t wdtype,
+                         int32_t indexed_by_act, const pgmoe_routing *r, float *h, float *yw,
+                         int32_t kernel, pgmoe_stream_t stream);
+
+/* K3 dense non-MoE layer (core.py:338): y[t] = D . sum_s yw[t*k+s]
+ * (slot order = routing order, linalg.py:45-51).  D: [d][d] out x in. */
+PGMOE_API int pgmoe_dense_forward(const float *yw, int32_t T, int32_t d, int32_t k, const void *dense_w,
+                        int32_t wdtype, float *y, int32_t kernel, pgmoe_stream_t stream);
+
+/* Reads routing status after a sync: returns the device-detected error (or
+ * PGMOE_OK) and optionally the serial-fallback / flip counters. */
+PGMOE_API int pgmoe_check_routing(const pgmoe_routing *r, int32_t *fallbacks, int32_t *flips);
+
+/* Deterministic weights: fills `out` ([rows][cols], wdtype) on the device
+ * with Xoshiro256StarStar(derive_seed(seed, tag, block, expert)).fill_matrix
+ * rounded to fp32 (then bf16), rng.py:15-93 + core.py:200-211. */
+PGMOE_API int pgmoe_fill_weights(void *out, int32_t wdtype, uint64_t seed, int32_t tag, int32_t block,
+                       int32_t expert, int64_t rows, int64_t cols, pgmoe_stream_t stream);
+
+/* ------------------------------------------------------------ the model */
+
+typedef struct pgmoe_model pgmoe_model;
+
+typedef struct {
+    int64_t pinned_hbm_bytes;     /* gates + dense (tiers.py:89-115 pinned_bytes) */
+    int64_t slot_capacity_bytes;  /* bytes reserved per expert slot (offloaded) */
+    int64_t eq1_peak_bytes;       /* pinned + max_N(act_N + act_N+1), tiers.py:68-86 */
+    int64_t ledger_peak_bytes;    /* measured: max over event-ordered intervals */
+    int64_t h2d_bytes;            /* expert bytes migrated since reset */
+    int64_t h2d_copies;
+    int64_t route_fallbacks;      /* tokens needing the serial fp64 recompute */
+    int64_t route_flips;          /* always 0: certified routing */
+    double h2d_seconds;           /* copy-stream busy time (CUDA events) */
+    double last_step_seconds;
+} pgmoe_stats;
+
+/* init_model (core.py:266) + placement (tiers.py:134-157).  max_tokens
+ * bounds T for every later call.  Weights are not filled yet. */
+PGMOE_API int pgmoe_model_create(const pgmoe_config *cfg, int32_t wdtype, int32_t placement,
+                       int32_t max_tokens, pgmoe_model **out);
+PGMOE_API int pgmoe_model_destroy(pgmoe_model *m);
+
+/* Fill every matrix from the reference generator (device RNG; offloaded
+ * experts are generated on the device then copied to pinned host memory). */
+PGMOE_API int pgmoe_model_init_weights(pgmoe_model *m);
+
+/* Copy one matrix in from host memory (the BlockParams `loaded` hook,
+ * core.py:185-211; model_io.load_model).  name: "gate", "pre_gate", "w1",
+ * "w2", "non_moe"; expert = -1 for non-expert matrices.  Host data is in
+ * the model's weight dtype, row-major. */
+PGMOE_API int pgmoe_model_set_matrix(pgmoe_model *m, const char *name, int32_t block, int32_t expert,
+                           const void *host_data, size_t nbytes);
+PGMOE_API int pgmoe_model_get_matrix(pgmoe_model *m, const char *name, int32_t block, int32_t expert,
+                           void *host_data, size_t nbytes);
+
+/* Kernel family for K2/K3 (AUTO: tcgen05 for bf16, SIMT for fp32). */
+PGMOE_API int pgmoe_model_set_kernel(pgmoe_model *m, int32_t kernel);
+
+/* decoder_iteration (core.py:342-383) for T tokens, device buffers.
+ * x_in / y_out: fp32 [T][d] device.  ids_trace / w_trace (optional, device):
+ * [num_blocks][T][k] consumed decisions.  Pre-gated migration
+ * (scheduler.py:344-373) runs on the model's copy stream when offloaded. */
+PGMOE_API int pgmoe_decoder_iteration(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
+                            int32_t *ids_trace, float *w_trace, pgmoe_stream_t stream);
+
+/* Same call on HOST buffers: copies x in, runs, copies y (and the trace)
+ * back, synchronises, and raises device-detected routing errors. */
+PGMOE_API int pgmoe_decoder_iteration_host(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
+                                 int32_t *ids_trace, float *w_trace);
+
+/* moe_block_forward (core.py:319-339) for block b on T tokens with the
+ * consumed routing `r_in` already on the device; emits routing_out into
+ * `r_out` when the block carries a lookahead gate (may be NULL). */
+PGMOE_API int pgmoe_moe_block_forward(pgmoe_model *m, int32_t block, const float *x, int32_t T,
+                            const pgmoe_routing *r_in, float *y, const pgmoe_routing *r_out,
+                            pgmoe_stream_t stream);
+
+/* Device pointers of the model's resident matrices (for the drop-in shim). */
+PGMOE_API const void *pgmoe_model_matrix_ptr(pgmoe_model *m, const char *name, int32_t block, int32_t expert);
+
+PGMOE_API int pgmoe_model_stats(pgmoe_model *m, pgmoe_stats *out);
+PGMOE_API int pgmoe_model_reset_stats(pgmoe_model *m);
+
+/* Timeline (events since the last set_timeline call) in the reference JSONL schema
+ * (scheduler.py:147-156): one line per event, lanes "compute"/"transfer".
+ * Writes at most `cap` bytes; returns bytes needed (excluding NUL). */
+PGMOE_API int64_t pgmoe_model_timeline_jsonl(pgmoe_model *m, char *buf, int64_t cap);
+PGMOE_API int pgmoe_model_set_timeline(pgmoe_model *m, int32_t enabled);
+
+PGMOE_API const char *pgmoe_last_error(void);
+PGMOE_API const char *pgmoe_version(void);
+/* Kernels this library has launched since load (benchmark evidence). */
+PGMOE_API int64_t pgmoe_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGMOE_H */

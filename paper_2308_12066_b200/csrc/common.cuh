@@ -1,0 +1,67 @@
+// common.cuh — shared helpers for the sm_100a pre-gated MoE library.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/pgmoe.h"
+
+namespace pgmoe {
+
+void set_error(const char *fmt, ...);
+void count_launch(int n = 1);  // kernels launched by this library (bench evidence)
+
+#define PG_CUDA(call)                                                                 \
+    do {                                                                              \
+        cudaError_t _e = (call);                                                      \
+        if (_e != cudaSuccess) {                                                      \
+            ::pgmoe::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,             \
+                               cudaGetErrorString(_e));                               \
+            return (_e == cudaErrorMemoryAllocation) ? PGMOE_E_OOM : PGMOE_E_CUDA;    \
+        }                                                                             \
+    } while (0)
+
+#define PG_TRY(call)                  \
+    do {                              \
+        int _s = (call);              \
+        if (_s != PGMOE_OK) return _s; \
+    } while (0)
+
+#define PG_REQUIRE(cond, code, ...)           \
+    do {                                      \
+        if (!(cond)) {                        \
+            ::pgmoe::set_error(__VA_ARGS__);  \
+            return (code);                    \
+        }                                     \
+    } while (0)
+
+constexpr int kNumSMs = 148;
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) {
+    return __uint_as_float(static_cast<uint32_t>(h) << 16);
+}
+
+// Weight element -> fp32 / fp64 (exact for both storage types).
+template <typename WT> struct WTraits;
+template <> struct WTraits<float> {
+    static constexpr int id = PGMOE_F32;
+    __device__ __forceinline__ static float f32(float v) { return v; }
+};
+template <> struct WTraits<uint16_t> {
+    static constexpr int id = PGMOE_BF16;
+    __device__ __forceinline__ static float f32(uint16_t v) { return bf16_to_f32(v); }
+};
+
+inline size_t dtype_bytes(int dt) { return dt == PGMOE_BF16 ? 2 : 4; }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace pgmoe

@@ -1,0 +1,24 @@
+// kernels.h — internal launch entry points shared by the runtime.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "../../include/pgmoe.h"
+
+namespace pgmoe {
+
+int expert_ffn_simt(const float *x, int T, int d, int f, int k, const void *experts, size_t stride,
+                    int wdtype, int indexed_by_act, const pgmoe_routing *r, float *h, float *yw,
+                    cudaStream_t s);
+int dense_simt(const float *yw, int T, int d, int k, const void *dense_w, int wdtype, float *y,
+               cudaStream_t s);
+
+// tcgen05/TMA path (bf16 weights).  Returns PGMOE_E_CONFIG when the shape
+// is outside what the kernel supports so callers can report it loudly.
+int expert_ffn_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride,
+                  int indexed_by_act, const pgmoe_routing *r, float *h, float *yw, void *workspace,
+                  size_t ws_bytes, cudaStream_t s);
+int dense_tc(const float *yw, int T, int d, int k, const void *dense_w, float *y, void *workspace,
+             size_t ws_bytes, cudaStream_t s);
+bool tc_supported(int d, int f);
+
+}  // namespace pgmoe

@@ -1,0 +1,762 @@
+// runtime.cu — the model object, the pre-gated decoder loop and the C ABI.
+//
+// Mirrors core.py:342-383 (decoder_iteration wiring) and the pre_gated
+// branch of scheduler.py:287-373 on real hardware: block b's lookahead gate
+// (K1) decides block b+L's experts; the host reads the active list as soon
+// as K1 finishes and streams exactly those experts from pinned host memory
+// into an (L+1)-slot HBM expert cache on a dedicated copy stream while
+// block b's experts (K2) and dense layer (K3) run on the compute stream.
+// CUDA events order slot reuse (a slot is refilled only after the block
+// that consumed it finished, tiers.py "expert lifetime") and expert
+// execution after arrival.  Block 0's fetch is exposed, as in the paper's
+// footnote (scheduler.py:344-351).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "rng.h"
+
+namespace pgmoe {
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void set_error(const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+}
+
+struct RoutingBuf {
+    pgmoe_routing r{};
+    void *mem = nullptr;
+    int32_t *act_host = nullptr;  // pinned mirror of act[E] + n_act
+};
+
+struct BlockW {
+    void *gate = nullptr, *pre_gate = nullptr, *dense = nullptr;
+    unsigned char *experts = nullptr;  // device (resident) or pinned host (offloaded)
+};
+
+struct TimelineEv {
+    const char *lane;
+    std::string label;
+    int block;
+    cudaEvent_t a, b;
+};
+
+}  // namespace pgmoe
+
+using namespace pgmoe;
+
+struct pgmoe_model {
+    pgmoe_config cfg{};
+    int wdtype = PGMOE_BF16, placement = PGMOE_RESIDENT, max_tokens = 0, kernel = PGMOE_KERNEL_AUTO;
+    size_t sw = 2, gate_bytes = 0, dense_bytes = 0, w1_bytes = 0, rec_bytes = 0;
+    std::vector<BlockW> blocks;
+    unsigned char *dev_pool = nullptr;   // gates + dense (+ experts when resident)
+    unsigned char *host_pool = nullptr;  // pinned experts (offloaded)
+    size_t dev_pool_bytes = 0, host_pool_bytes = 0;
+    // work buffers
+    float *act_buf[2] = {nullptr, nullptr};
+    float *h = nullptr, *yw = nullptr;
+    std::vector<RoutingBuf> routing;  // ring of L+1 decisions
+    void *route_ws = nullptr;
+    void *tc_ws = nullptr;
+    size_t tc_ws_bytes = 0;
+    // offload
+    unsigned char *slots = nullptr;
+    size_t slot_capacity = 0;  // bytes per slot
+    int slot_experts = 0;
+    cudaStream_t copy = nullptr;
+    std::vector<cudaEvent_t> ready, done, routed;
+    std::vector<bool> slot_used;
+    // stats
+    pgmoe_stats stats{};
+    std::vector<int> nact_iter;  // per block, last iteration (offloaded)
+    std::vector<cudaEvent_t> cp_a, cp_b, ffn_b;  // per block timing events
+    bool timeline = false;
+    std::vector<TimelineEv> tl;
+    cudaEvent_t t0 = nullptr;
+    bool t0_recorded = false;
+    std::mutex mu;
+};
+
+namespace pgmoe {
+
+static bool has_conv_gate(const pgmoe_config &c, int b) {
+    if (c.activation_level == 0) return true;
+    return b < c.activation_level;
+}
+static bool has_pre_gate(const pgmoe_config &c, int b) {
+    if (c.activation_level == 0) return false;
+    return b < c.num_blocks - c.activation_level;
+}
+
+static int validate_config(const pgmoe_config *c) {
+    PG_REQUIRE(c != nullptr, PGMOE_E_CONFIG, "null config");
+    const int32_t v[5] = {c->d_model, c->d_ff, c->num_blocks, c->num_experts, c->top_k};
+    const char *names[5] = {"d_model", "d_ff", "num_blocks", "num_experts", "top_k"};
+    for (int i = 0; i < 5; ++i)
+        PG_REQUIRE(v[i] >= 1, PGMOE_E_CONFIG, "%s must be a positive int, got %d", names[i], v[i]);
+    PG_REQUIRE(c->top_k <= c->num_experts, PGMOE_E_CONFIG, "top_k=%d exceeds num_experts=%d",
+               c->top_k, c->num_experts);
+    PG_REQUIRE(c->activation_level >= 0 && c->activation_level < c->num_blocks, PGMOE_E_CONFIG,
+               "activation_level=%d must be in [0, num_blocks=%d)", c->activation_level, c->num_blocks);
+    PG_REQUIRE(c->top_k <= 8, PGMOE_E_CONFIG, "top_k=%d unsupported by the device path (<= 8)", c->top_k);
+    PG_REQUIRE(c->num_experts <= 1024, PGMOE_E_CONFIG, "num_experts=%d unsupported (<= 1024)",
+               c->num_experts);
+    return PGMOE_OK;
+}
+
+static int alloc_routing(RoutingBuf &rb, int T, int E, int k) {
+    const size_t n = (size_t)T * k;
+    // layout: ids | w | perm | w_perm | hist | off | act | n_act | status
+    size_t bytes = n * 4 * 4 + (size_t)E * 4 + (size_t)(E + 1) * 4 + (size_t)(E + 1) * 4 + 16 + 256;
+    PG_CUDA(cudaMalloc(&rb.mem, bytes));
+    PG_CUDA(cudaMemset(rb.mem, 0, bytes));
+    char *p = static_cast<char *>(rb.mem);
+    rb.r.ids = reinterpret_cast<int32_t *>(p); p += n * 4;
+    rb.r.w = reinterpret_cast<float *>(p); p += n * 4;
+    rb.r.perm = reinterpret_cast<int32_t *>(p); p += n * 4;
+    rb.r.w_perm = reinterpret_cast<float *>(p); p += n * 4;
+    rb.r.hist = reinterpret_cast<int32_t *>(p); p += (size_t)E * 4;
+    rb.r.off = reinterpret_cast<int32_t *>(p); p += (size_t)(E + 1) * 4;
+    rb.r.act = reinterpret_cast<int32_t *>(p);
+    rb.r.n_act = rb.r.act + E;  // contiguous with act: one D2H copy
+    p += (size_t)(E + 1) * 4;
+    p = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    rb.r.status = reinterpret_cast<int32_t *>(p);
+    PG_CUDA(cudaHostAlloc(&rb.act_host, sizeof(int32_t) * (E + 1), cudaHostAllocDefault));
+    return PGMOE_OK;
+}
+
+static void *mat_ptr(pgmoe_model *m, const std::string &name, int b, int e, size_t *bytes,
+                     bool *on_host) {
+    const auto &c = m->cfg;
+    if (b < 0 || b >= c.num_blocks) return nullptr;
+    BlockW &bw = m->blocks[b];
+    *on_host = false;
+    if (name == "gate") { *bytes = m->gate_bytes; return bw.gate; }
+    if (name == "pre_gate") { *bytes = m->gate_bytes; return bw.pre_gate; }
+    if (name == "non_moe") { *bytes = m->dense_bytes; return bw.dense; }
+    if (name == "w1" || name == "w2") {
+        if (e < 0 || e >= c.num_experts) return nullptr;
+        *on_host = (m->placement == PGMOE_OFFLOADED);
+        *bytes = m->w1_bytes;
+        return bw.experts + (size_t)e * m->rec_bytes + (name == "w2" ? m->w1_bytes : 0);
+    }
+    return nullptr;
+}
+
+int run_ffn(pgmoe_model *m, const float *x, int T, const void *experts, int indexed,
+            const pgmoe_routing *r, cudaStream_t s) {
+    const auto &c = m->cfg;
+    const bool tc = m->wdtype == PGMOE_BF16 && m->kernel != PGMOE_KERNEL_SIMT &&
+                    tc_supported(c.d_model, c.d_ff);
+    if (m->kernel == PGMOE_KERNEL_TCGEN05)
+        PG_REQUIRE(tc, PGMOE_E_CONFIG, "tcgen05 kernels need bf16 weights and d, f multiples of 128");
+    if (tc)
+        return expert_ffn_tc(x, T, c.d_model, c.d_ff, c.top_k, experts, m->rec_bytes, indexed, r, m->h,
+                             m->yw, m->tc_ws, m->tc_ws_bytes, s);
+    return expert_ffn_simt(x, T, c.d_model, c.d_ff, c.top_k, experts, m->rec_bytes, m->wdtype, indexed,
+                           r, m->h, m->yw, s);
+}
+
+int run_dense(pgmoe_model *m, int T, const void *dense, float *y, cudaStream_t s) {
+    const auto &c = m->cfg;
+    const bool tc = m->wdtype == PGMOE_BF16 && m->kernel != PGMOE_KERNEL_SIMT &&
+                    tc_supported(c.d_model, c.d_ff);
+    if (tc) return dense_tc(m->yw, T, c.d_model, c.top_k, dense, y, m->tc_ws, m->tc_ws_bytes, s);
+    return dense_simt(m->yw, T, c.d_model, c.top_k, dense, m->wdtype, y, s);
+}
+
+static void tl_begin(pgmoe_model *m, const char *lane, const std::string &label, int block,
+                     cudaStream_t s) {
+    if (!m->timeline) return;
+    TimelineEv ev{lane, label, block, nullptr, nullptr};
+    cudaEventCreate(&ev.a);
+    cudaEventCreate(&ev.b);
+    cudaEventRecord(ev.a, s);
+    m->tl.push_back(ev);
+}
+static void tl_end(pgmoe_model *m, cudaStream_t s) {
+    if (!m->timeline) return;
+    cudaEventRecord(m->tl.back().b, s);
+}
+
+// Issue the H2D migration of block `tb`'s routed experts into slot `ri`
+// (scheduler.py:287-330 `issue`, made real).  Waits on the host for K1's
+// active list (pinned mirror), then enqueues one DMA per expert on the copy
+// stream after the slot's previous consumer finished.
+static int issue_fetch(pgmoe_model *m, int tb, int ri) {
+    const auto &c = m->cfg;
+    RoutingBuf &rb = m->routing[ri];
+    PG_CUDA(cudaEventSynchronize(m->routed[ri]));
+    const int n = rb.act_host[c.num_experts];
+    PG_REQUIRE(n >= 0 && n <= m->slot_experts, PGMOE_E_OOM,
+               "block %d routes to %d experts but the HBM slot holds %d", tb, n, m->slot_experts);
+    if (m->slot_used[ri]) PG_CUDA(cudaStreamWaitEvent(m->copy, m->done[ri], 0));
+    if (!m->cp_a.empty()) PG_CUDA(cudaEventRecord(m->cp_a[tb], m->copy));
+    tl_begin(m, "transfer", "fetch[" + std::to_string(n) + "]", tb, m->copy);
+    unsigned char *dst = m->slots + (size_t)ri * m->slot_capacity;
+    const unsigned char *src = m->blocks[tb].experts;
+    for (int i = 0; i < n;) {  // coalesce runs of consecutive experts into one DMA
+        int j = i + 1;
+        while (j < n && rb.act_host[j] == rb.act_host[j - 1] + 1) ++j;
+        PG_CUDA(cudaMemcpyAsync(dst + (size_t)i * m->rec_bytes, src + (size_t)rb.act_host[i] * m->rec_bytes,
+                                (size_t)(j - i) * m->rec_bytes, cudaMemcpyHostToDevice, m->copy));
+        m->stats.h2d_copies++;
+        i = j;
+    }
+    tl_end(m, m->copy);
+    if (!m->cp_b.empty()) PG_CUDA(cudaEventRecord(m->cp_b[tb], m->copy));
+    PG_CUDA(cudaEventRecord(m->ready[ri], m->copy));
+    m->stats.h2d_bytes += (int64_t)n * (int64_t)m->rec_bytes;
+    m->slot_used[ri] = true;
+    if ((int)m->nact_iter.size() == c.num_blocks) m->nact_iter[tb] = n;
+    return PGMOE_OK;
+}
+
+static int route_into(pgmoe_model *m, const float *x, int T, const void *G, int ri, bool mirror,
+                      cudaStream_t s, const char *label, int block) {
+    const auto &c = m->cfg;
+    RoutingBuf &rb = m->routing[ri];
+    tl_begin(m, "compute", label, block, s);
+    PG_TRY(pgmoe_gate_forward(x, T, c.d_model, G, m->wdtype, c.num_experts, c.top_k, &rb.r, m->route_ws,
+                              reinterpret_cast<pgmoe_stream_t>(s)));
+    tl_end(m, s);
+    if (mirror) {
+        PG_CUDA(cudaMemcpyAsync(rb.act_host, rb.r.act, sizeof(int32_t) * (c.num_experts + 1),
+                                cudaMemcpyDeviceToHost, s));
+        PG_CUDA(cudaEventRecord(m->routed[ri], s));
+    }
+    return PGMOE_OK;
+}
+
+int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, int32_t *ids_trace,
+                      float *w_trace, cudaStream_t s) {
+    const auto &c = m->cfg;
+    PG_REQUIRE(T >= 0 && T <= m->max_tokens, PGMOE_E_SHAPE, "T=%d exceeds max_tokens=%d", T,
+               m->max_tokens);
+    if (T == 0) return PGMOE_OK;
+    const int L = c.activation_level, R = L + 1, nb = c.num_blocks;
+    const bool off = m->placement == PGMOE_OFFLOADED;
+    const size_t tk = (size_t)T * c.top_k;
+    if (m->timeline && !m->t0_recorded) {  // events accumulate until set_timeline() resets them
+        PG_CUDA(cudaEventRecord(m->t0, s));
+        m->t0_recorded = true;
+    }
+    if (off) m->nact_iter.assign(nb, 0);
+    const float *cur = x_in;
+    for (int b = 0; b < nb; ++b) {
+        const BlockW &bw = m->blocks[b];
+        const int ri = b % R;
+        int pending_fetch = -1;
+        if (has_conv_gate(c, b)) {
+            PG_TRY(route_into(m, cur, T, bw.gate, ri, off, s, "gate", b));
+            if (off) PG_TRY(issue_fetch(m, b, ri));  // exposed serial fetch
+        }
+        if (has_pre_gate(c, b)) {
+            const int tr = (b + L) % R;
+            PG_TRY(route_into(m, cur, T, bw.pre_gate, tr, off, s, "pre_gate", b));
+            if (off) pending_fetch = b + L;
+        }
+        const RoutingBuf &rb = m->routing[ri];
+        const void *experts = off ? (const void *)(m->slots + (size_t)ri * m->slot_capacity)
+                                  : (const void *)bw.experts;
+        if (off) PG_CUDA(cudaStreamWaitEvent(s, m->ready[ri], 0));
+        tl_begin(m, "compute", "experts", b, s);
+        PG_TRY(run_ffn(m, cur, T, experts, off ? 1 : 0, &rb.r, s));
+        tl_end(m, s);
+        if (off) {
+            PG_CUDA(cudaEventRecord(m->done[ri], s));
+            if (!m->ffn_b.empty()) PG_CUDA(cudaEventRecord(m->ffn_b[b], s));
+        }
+        float *nxt = (b == nb - 1) ? y_out : m->act_buf[b & 1];
+        tl_begin(m, "compute", "non_moe", b, s);
+        PG_TRY(run_dense(m, T, bw.dense, nxt, s));
+        tl_end(m, s);
+        if (ids_trace) {
+            PG_CUDA(cudaMemcpyAsync(ids_trace + (size_t)b * tk, rb.r.ids, tk * 4, cudaMemcpyDeviceToDevice, s));
+            PG_CUDA(cudaMemcpyAsync(w_trace + (size_t)b * tk, rb.r.w, tk * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        if (pending_fetch >= 0) PG_TRY(issue_fetch(m, pending_fetch, pending_fetch % R));
+        cur = nxt;
+    }
+    return PGMOE_OK;
+}
+
+}  // namespace pgmoe
+
+// =============================================================== C ABI ====
+
+extern "C" const char *pgmoe_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char *pgmoe_version(void) { return "pgmoe-b200 0.1.0 (sm_100a)"; }
+extern "C" int64_t pgmoe_launch_count(void) { return g_launches.load(); }
+
+extern "C" int pgmoe_expert_forward(const float *x, int32_t T, int32_t d, int32_t f, int32_t k,
+                                    const void *experts, size_t expert_stride, int32_t wdtype,
+                                    int32_t indexed_by_act, const pgmoe_routing *r, float *h, float *yw,
+                                    int32_t kernel, pgmoe_stream_t stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (T == 0) return PGMOE_OK;
+    const bool tc = wdtype == PGMOE_BF16 && kernel != PGMOE_KERNEL_SIMT && tc_supported(d, f);
+    if (kernel == PGMOE_KERNEL_TCGEN05)
+        PG_REQUIRE(tc, PGMOE_E_CONFIG, "tcgen05 kernels need bf16 weights and d, f multiples of 128");
+    if (tc) {
+        static void *ws = nullptr;
+        static size_t ws_bytes = 0;
+        if (!ws) {
+            ws_bytes = 64ull << 20;
+            PG_CUDA(cudaMalloc(&ws, ws_bytes));
+            PG_CUDA(cudaMemset(ws, 0, ws_bytes));
+        }
+        return expert_ffn_tc(x, T, d, f, k, experts, expert_stride, indexed_by_act, r, h, yw, ws, ws_bytes, s);
+    }
+    return expert_ffn_simt(x, T, d, f, k, experts, expert_stride, wdtype, indexed_by_act, r, h, yw, s);
+}
+
+extern "C" int pgmoe_dense_forward(const float *yw, int32_t T, int32_t d, int32_t k, const void *dense_w,
+                                   int32_t wdtype, float *y, int32_t kernel, pgmoe_stream_t stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (T == 0) return PGMOE_OK;
+    const bool tc = wdtype == PGMOE_BF16 && kernel != PGMOE_KERNEL_SIMT && tc_supported(d, 128);
+    if (tc) {
+        static void *ws = nullptr;
+        static size_t ws_bytes = 0;
+        if (!ws) {
+            ws_bytes = 64ull << 20;
+            PG_CUDA(cudaMalloc(&ws, ws_bytes));
+            PG_CUDA(cudaMemset(ws, 0, ws_bytes));
+        }
+        return dense_tc(yw, T, d, k, dense_w, y, ws, ws_bytes, s);
+    }
+    return dense_simt(yw, T, d, k, dense_w, wdtype, y, s);
+}
+
+extern "C" int pgmoe_model_create(const pgmoe_config *cfg, int32_t wdtype, int32_t placement,
+                                  int32_t max_tokens, pgmoe_model **out) {
+    PG_TRY(validate_config(cfg));
+    PG_REQUIRE(out != nullptr, PGMOE_E_CONFIG, "null output handle");
+    PG_REQUIRE(wdtype == PGMOE_F32 || wdtype == PGMOE_BF16, PGMOE_E_CONFIG, "unknown weight dtype %d", wdtype);
+    PG_REQUIRE(placement == PGMOE_RESIDENT || placement == PGMOE_OFFLOADED, PGMOE_E_CONFIG,
+               "unknown placement %d", placement);
+    PG_REQUIRE(max_tokens >= 1, PGMOE_E_CONFIG, "max_tokens must be >= 1");
+    auto *m = new pgmoe_model();
+    m->cfg = *cfg;
+    m->wdtype = wdtype;
+    m->placement = placement;
+    m->max_tokens = max_tokens;
+    const auto &c = m->cfg;
+    const size_t d = c.d_model, f = c.d_ff, E = c.num_experts, nb = c.num_blocks, k = c.top_k;
+    m->sw = dtype_bytes(wdtype);
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    m->gate_bytes = al(d * E * m->sw);
+    m->dense_bytes = al(d * d * m->sw);
+    m->w1_bytes = f * d * m->sw;
+    m->rec_bytes = al(2 * f * d * m->sw);
+    m->blocks.resize(nb);
+    size_t pinned = 0;
+    for (size_t b = 0; b < nb; ++b)
+        pinned += (has_conv_gate(c, b) + has_pre_gate(c, b)) * m->gate_bytes + m->dense_bytes;
+    const size_t experts_all = nb * E * m->rec_bytes;
+    m->dev_pool_bytes = pinned + (placement == PGMOE_RESIDENT ? experts_all : 0);
+    int st = PGMOE_OK;
+    auto fail = [&](int code) {
+        pgmoe_model_destroy(m);
+        return code;
+    };
+    if (cudaMalloc(&m->dev_pool, m->dev_pool_bytes) != cudaSuccess) {
+        set_error("OOM: %zu B of HBM for %s weights", m->dev_pool_bytes,
+                  placement == PGMOE_RESIDENT ? "resident" : "pinned (gate/dense)");
+        return fail(PGMOE_E_OOM);
+    }
+    unsigned char *p = m->dev_pool;
+    for (size_t b = 0; b < nb; ++b) {
+        BlockW &bw = m->blocks[b];
+        if (has_conv_gate(c, b)) { bw.gate = p; p += m->gate_bytes; }
+        if (has_pre_gate(c, b)) { bw.pre_gate = p; p += m->gate_bytes; }
+        bw.dense = p;
+        p += m->dense_bytes;
+    }
+    if (placement == PGMOE_RESIDENT) {
+        for (size_t b = 0; b < nb; ++b) { m->blocks[b].experts = p; p += E * m->rec_bytes; }
+    } else {
+        m->host_pool_bytes = experts_all;
+        if (cudaHostAlloc(&m->host_pool, experts_all, cudaHostAllocDefault) != cudaSuccess) {
+            set_error("cannot pin %zu B of host memory for offloaded experts", experts_all);
+            return fail(PGMOE_E_OOM);
+        }
+        for (size_t b = 0; b < nb; ++b) m->blocks[b].experts = m->host_pool + b * E * m->rec_bytes;
+        const int R = c.activation_level + 1;
+        m->slot_experts = (int)std::min<size_t>(E, (size_t)max_tokens * k);
+        m->slot_capacity = (size_t)m->slot_experts * m->rec_bytes;
+        if (cudaMalloc(&m->slots, m->slot_capacity * R) != cudaSuccess) {
+            set_error("OOM: %zu B of HBM for %d expert slots", m->slot_capacity * R, R);
+            return fail(PGMOE_E_OOM);
+        }
+        if (cudaStreamCreateWithFlags(&m->copy, cudaStreamNonBlocking) != cudaSuccess) return fail(PGMOE_E_CUDA);
+        m->ready.resize(R); m->done.resize(R); m->slot_used.assign(R, false);
+        for (int i = 0; i < R; ++i) {
+            cudaEventCreateWithFlags(&m->ready[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&m->done[i], cudaEventDisableTiming);
+        }
+        m->cp_a.resize(nb); m->cp_b.resize(nb); m->ffn_b.resize(nb);
+        for (size_t b = 0; b < nb; ++b) {
+            cudaEventCreate(&m->cp_a[b]); cudaEventCreate(&m->cp_b[b]); cudaEventCreate(&m->ffn_b[b]);
+        }
+    }
+    const int R = c.activation_level + 1;
+    m->routing.resize(R);
+    m->routed.resize(R);
+    for (int i = 0; i < R; ++i) {
+        if ((st = alloc_routing(m->routing[i], max_tokens, (int)E, (int)k)) != PGMOE_OK) return fail(st);
+        cudaEventCreateWithFlags(&m->routed[i], cudaEventDisableTiming);
+    }
+    if (cudaMalloc(&m->route_ws, 256) != cudaSuccess || cudaMemset(m->route_ws, 0, 256) != cudaSuccess)
+        return fail(PGMOE_E_OOM);
+    const size_t T = max_tokens;
+    if (cudaMalloc(&m->act_buf[0], T * d * 4) != cudaSuccess ||
+        cudaMalloc(&m->act_buf[1], T * d * 4) != cudaSuccess ||
+        cudaMalloc(&m->h, T * k * f * 4) != cudaSuccess || cudaMalloc(&m->yw, T * k * d * 4) != cudaSuccess) {
+        set_error("OOM: activation buffers for max_tokens=%d", max_tokens);
+        return fail(PGMOE_E_OOM);
+    }
+    m->tc_ws_bytes = 64ull << 20;
+    if (cudaMalloc(&m->tc_ws, m->tc_ws_bytes) != cudaSuccess || cudaMemset(m->tc_ws, 0, m->tc_ws_bytes) != cudaSuccess)
+        return fail(PGMOE_E_OOM);
+    cudaEventCreate(&m->t0);
+    m->stats.pinned_hbm_bytes = (int64_t)pinned;
+    m->stats.slot_capacity_bytes = (int64_t)m->slot_capacity;
+    *out = m;
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
+    if (!m) return PGMOE_OK;
+    cudaDeviceSynchronize();
+    for (auto &rb : m->routing) {
+        if (rb.mem) cudaFree(rb.mem);
+        if (rb.act_host) cudaFreeHost(rb.act_host);
+    }
+    for (auto e : m->ready) cudaEventDestroy(e);
+    for (auto e : m->done) cudaEventDestroy(e);
+    for (auto e : m->routed) cudaEventDestroy(e);
+    for (auto e : m->cp_a) cudaEventDestroy(e);
+    for (auto e : m->cp_b) cudaEventDestroy(e);
+    for (auto e : m->ffn_b) cudaEventDestroy(e);
+    for (auto &e : m->tl) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    if (m->t0) cudaEventDestroy(m->t0);
+    if (m->copy) cudaStreamDestroy(m->copy);
+    cudaFree(m->dev_pool);
+    if (m->host_pool) cudaFreeHost(m->host_pool);
+    cudaFree(m->slots);
+    cudaFree(m->route_ws);
+    cudaFree(m->tc_ws);
+    cudaFree(m->act_buf[0]);
+    cudaFree(m->act_buf[1]);
+    cudaFree(m->h);
+    cudaFree(m->yw);
+    delete m;
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_model_set_kernel(pgmoe_model *m, int32_t kernel) {
+    PG_REQUIRE(kernel >= PGMOE_KERNEL_AUTO && kernel <= PGMOE_KERNEL_TCGEN05, PGMOE_E_CONFIG, "bad kernel %d", kernel);
+    m->kernel = kernel;
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_model_init_weights(pgmoe_model *m) {
+    const auto &c = m->cfg;
+    const int nb = c.num_blocks, E = c.num_experts;
+    const int64_t d = c.d_model, f = c.d_ff;
+    cudaStream_t s = nullptr;
+    PG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    std::vector<GenJob> jobs;
+    for (int b = 0; b < nb; ++b) {
+        BlockW &bw = m->blocks[b];
+        if (bw.gate) jobs.push_back({bw.gate, matrix_seed(c.seed, kTagGate, b, -1), d * c.num_experts});
+        if (bw.pre_gate) jobs.push_back({bw.pre_gate, matrix_seed(c.seed, kTagPreGate, b, -1), d * c.num_experts});
+        jobs.push_back({bw.dense, matrix_seed(c.seed, kTagDense, b, -1), d * d});
+    }
+    const bool off = m->placement == PGMOE_OFFLOADED;
+    unsigned char *stage = nullptr;
+    int chunk = 1;
+    if (off) {  // stage as many blocks as comfortably fit in HBM, then D2H
+        size_t free_b = 0, total_b = 0;
+        PG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const size_t blk = (size_t)E * m->rec_bytes;
+        chunk = (int)std::max<size_t>(1, std::min<size_t>(nb, (free_b / 2) / blk));
+        PG_CUDA(cudaMalloc(&stage, (size_t)chunk * blk));
+    }
+    GenJob *dj = nullptr;
+    const size_t max_jobs = std::max<size_t>(jobs.size(), (size_t)2 * E * (off ? chunk : nb));
+    PG_CUDA(cudaMalloc(&dj, sizeof(GenJob) * max_jobs));
+    auto run = [&](std::vector<GenJob> &js) -> int {
+        PG_CUDA(cudaMemcpyAsync(dj, js.data(), sizeof(GenJob) * js.size(), cudaMemcpyHostToDevice, s));
+        PG_TRY(gen_matrices(dj, (int)js.size(), m->wdtype, s));
+        PG_CUDA(cudaStreamSynchronize(s));
+        return PGMOE_OK;
+    };
+    int st = run(jobs);
+    if (st == PGMOE_OK && !off) {
+        std::vector<GenJob> ej;
+        for (int b = 0; b < nb; ++b)
+            for (int e = 0; e < E; ++e) {
+                unsigned char *rec = m->blocks[b].experts + (size_t)e * m->rec_bytes;
+                ej.push_back({rec, matrix_seed(c.seed, kTagW1, b, e), f * d});
+                ej.push_back({rec + m->w1_bytes, matrix_seed(c.seed, kTagW2, b, e), d * f});
+            }
+        st = run(ej);
+    } else if (st == PGMOE_OK) {
+        for (int b0 = 0; b0 < nb && st == PGMOE_OK; b0 += chunk) {
+            const int b1 = std::min(nb, b0 + chunk);
+            std::vector<GenJob> ej;
+            for (int b = b0; b < b1; ++b)
+                for (int e = 0; e < E; ++e) {
+                    unsigned char *rec = stage + ((size_t)(b - b0) * E + e) * m->rec_bytes;
+                    ej.push_back({rec, matrix_seed(c.seed, kTagW1, b, e), f * d});
+                    ej.push_back({rec + m->w1_bytes, matrix_seed(c.seed, kTagW2, b, e), d * f});
+                }
+            st = run(ej);
+            if (st == PGMOE_OK && cudaMemcpy(m->blocks[b0].experts, stage, (size_t)(b1 - b0) * E * m->rec_bytes,
+                                             cudaMemcpyDeviceToHost) != cudaSuccess) {
+                set_error("D2H of generated experts failed");
+                st = PGMOE_E_CUDA;
+            }
+        }
+    }
+    cudaFree(dj);
+    if (stage) cudaFree(stage);
+    cudaStreamDestroy(s);
+    return st;
+}
+
+extern "C" int pgmoe_model_set_matrix(pgmoe_model *m, const char *name, int32_t block, int32_t expert,
+                                      const void *host_data, size_t nbytes) {
+    size_t bytes = 0;
+    bool on_host = false;
+    void *dst = mat_ptr(m, name ? name : "", block, expert, &bytes, &on_host);
+    PG_REQUIRE(dst != nullptr, PGMOE_E_CONFIG, "no matrix %s block %d expert %d", name, block, expert);
+    const size_t want = (std::string(name) == "w1" || std::string(name) == "w2")
+                            ? m->w1_bytes
+                            : (std::string(name) == "non_moe" ? (size_t)m->cfg.d_model * m->cfg.d_model * m->sw
+                                                              : (size_t)m->cfg.d_model * m->cfg.num_experts * m->sw);
+    PG_REQUIRE(nbytes == want, PGMOE_E_SHAPE, "matrix %s expects %zu bytes, got %zu", name, want, nbytes);
+    if (on_host) memcpy(dst, host_data, nbytes);
+    else PG_CUDA(cudaMemcpy(dst, host_data, nbytes, cudaMemcpyHostToDevice));
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_model_get_matrix(pgmoe_model *m, const char *name, int32_t block, int32_t expert,
+                                      void *host_data, size_t nbytes) {
+    size_t bytes = 0;
+    bool on_host = false;
+    void *src = mat_ptr(m, name ? name : "", block, expert, &bytes, &on_host);
+    PG_REQUIRE(src != nullptr, PGMOE_E_CONFIG, "no matrix %s block %d expert %d", name, block, expert);
+    PG_REQUIRE(nbytes <= bytes, PGMOE_E_SHAPE, "matrix %s holds %zu bytes, asked %zu", name, bytes, nbytes);
+    if (on_host) memcpy(host_data, src, nbytes);
+    else PG_CUDA(cudaMemcpy(host_data, src, nbytes, cudaMemcpyDeviceToHost));
+    return PGMOE_OK;
+}
+
+extern "C" const void *pgmoe_model_matrix_ptr(pgmoe_model *m, const char *name, int32_t block, int32_t expert) {
+    size_t bytes = 0;
+    bool on_host = false;
+    return mat_ptr(m, name ? name : "", block, expert, &bytes, &on_host);
+}
+
+extern "C" int pgmoe_decoder_iteration(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
+                                       int32_t *ids_trace, float *w_trace, pgmoe_stream_t stream) {
+    PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
+    std::lock_guard<std::mutex> g(m->mu);
+    return decoder_iteration(m, x_in, T, y_out, ids_trace, w_trace, reinterpret_cast<cudaStream_t>(stream));
+}
+
+static int check_all_routing(pgmoe_model *m) {
+    for (auto &rb : m->routing) {
+        int32_t fb = 0, fl = 0;
+        int st = pgmoe_check_routing(&rb.r, &fb, &fl);
+        m->stats.route_fallbacks = std::max<int64_t>(m->stats.route_fallbacks, fb);
+        if (st != PGMOE_OK) return st;
+    }
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_decoder_iteration_host(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
+                                            int32_t *ids_trace, float *w_trace) {
+    PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
+    std::lock_guard<std::mutex> g(m->mu);
+    const auto &c = m->cfg;
+    PG_REQUIRE(T >= 0 && T <= m->max_tokens, PGMOE_E_SHAPE, "T=%d exceeds max_tokens=%d", T, m->max_tokens);
+    if (T == 0) return PGMOE_OK;
+    const size_t xb = (size_t)T * c.d_model * 4, tb = (size_t)c.num_blocks * T * c.top_k * 4;
+    float *dx = nullptr, *dy = nullptr, *dw = nullptr;
+    int32_t *di = nullptr;
+    cudaStream_t s = nullptr;
+    PG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    PG_CUDA(cudaMallocAsync(&dx, xb, s));
+    PG_CUDA(cudaMallocAsync(&dy, xb, s));
+    if (ids_trace) {
+        PG_CUDA(cudaMallocAsync(&di, tb, s));
+        PG_CUDA(cudaMallocAsync(&dw, tb, s));
+    }
+    PG_CUDA(cudaMemcpyAsync(dx, x_in, xb, cudaMemcpyHostToDevice, s));
+    int st = decoder_iteration(m, dx, T, dy, di, dw, s);
+    if (st == PGMOE_OK) {
+        cudaMemcpyAsync(y_out, dy, xb, cudaMemcpyDeviceToHost, s);
+        if (ids_trace) {
+            cudaMemcpyAsync(ids_trace, di, tb, cudaMemcpyDeviceToHost, s);
+            cudaMemcpyAsync(w_trace, dw, tb, cudaMemcpyDeviceToHost, s);
+        }
+    }
+    cudaFreeAsync(dx, s);
+    cudaFreeAsync(dy, s);
+    if (di) { cudaFreeAsync(di, s); cudaFreeAsync(dw, s); }
+    if (cudaStreamSynchronize(s) != cudaSuccess && st == PGMOE_OK) {
+        set_error("decoder iteration failed: %s", cudaGetErrorString(cudaGetLastError()));
+        st = PGMOE_E_CUDA;
+    }
+    cudaStreamDestroy(s);
+    if (st == PGMOE_OK) st = check_all_routing(m);
+    return st;
+}
+
+extern "C" int pgmoe_moe_block_forward(pgmoe_model *m, int32_t block, const float *x, int32_t T,
+                                       const pgmoe_routing *r_in, float *y, const pgmoe_routing *r_out,
+                                       pgmoe_stream_t stream) {
+    PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
+    std::lock_guard<std::mutex> g(m->mu);
+    const auto &c = m->cfg;
+    PG_REQUIRE(block >= 0 && block < c.num_blocks, PGMOE_E_CONFIG, "block %d out of range", block);
+    PG_REQUIRE(T >= 0 && T <= m->max_tokens, PGMOE_E_SHAPE, "T=%d exceeds max_tokens=%d", T, m->max_tokens);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const BlockW &bw = m->blocks[block];
+    if (r_out && has_pre_gate(c, block))
+        PG_TRY(pgmoe_gate_forward(x, T, c.d_model, bw.pre_gate, m->wdtype, c.num_experts, c.top_k, r_out,
+                                  m->route_ws, stream));
+    PG_REQUIRE(r_in != nullptr, PGMOE_E_ROUTING, "no routing decision available");
+    if (T == 0) return PGMOE_OK;
+    const void *experts = bw.experts;
+    int indexed = 0;
+    if (m->placement == PGMOE_OFFLOADED) {  // on-demand fetch into slot 0
+        int32_t nact = 0;
+        PG_CUDA(cudaMemcpyAsync(m->routing[0].act_host, r_in->act, sizeof(int32_t) * (c.num_experts + 1),
+                                cudaMemcpyDeviceToHost, s));
+        PG_CUDA(cudaStreamSynchronize(s));
+        nact = m->routing[0].act_host[c.num_experts];
+        PG_REQUIRE(nact <= m->slot_experts, PGMOE_E_OOM, "slot overflow");
+        for (int i = 0; i < nact; ++i)
+            PG_CUDA(cudaMemcpyAsync(m->slots + (size_t)i * m->rec_bytes,
+                                    bw.experts + (size_t)m->routing[0].act_host[i] * m->rec_bytes, m->rec_bytes,
+                                    cudaMemcpyHostToDevice, s));
+        experts = m->slots;
+        indexed = 1;
+        m->slot_used[0] = false;
+    }
+    PG_TRY(run_ffn(m, x, T, experts, indexed, r_in, s));
+    return run_dense(m, T, bw.dense, y, s);
+}
+
+extern "C" int pgmoe_model_stats(pgmoe_model *m, pgmoe_stats *out) {
+    PG_REQUIRE(m && out, PGMOE_E_CONFIG, "null argument");
+    std::lock_guard<std::mutex> g(m->mu);
+    PG_CUDA(cudaDeviceSynchronize());
+    const auto &c = m->cfg;
+    if (m->placement == PGMOE_OFFLOADED && (int)m->nact_iter.size() == c.num_blocks) {
+        // Eq.1 (tiers.py:68-86) over the last iteration's measured active sets
+        int64_t best = 0;
+        const int L = c.activation_level;
+        for (int n = 0; n < c.num_blocks; ++n) {
+            int64_t win = 0;
+            for (int q = n; q <= n + L && q < c.num_blocks; ++q) win += (int64_t)m->nact_iter[q] * m->rec_bytes;
+            best = std::max(best, win);
+        }
+        m->stats.eq1_peak_bytes = m->stats.pinned_hbm_bytes + best;
+        // Ledger from real event times: expert bytes of block b live over
+        // [copy start, experts done] (half-open; releases first at ties).
+        struct Ev { float t; int kind; int64_t bytes; };
+        std::vector<Ev> evs;
+        double busy = 0;
+        for (int b = 0; b < c.num_blocks; ++b) {
+            float ta = 0, tb = 0, te = 0;
+            if (cudaEventElapsedTime(&ta, m->cp_a[0], m->cp_a[b]) != cudaSuccess) continue;
+            cudaEventElapsedTime(&tb, m->cp_a[0], m->cp_b[b]);
+            cudaEventElapsedTime(&te, m->cp_a[0], m->ffn_b[b]);
+            busy += (tb - ta) * 1e-3;
+            const int64_t by = (int64_t)m->nact_iter[b] * m->rec_bytes;
+            evs.push_back({ta, 1, by});
+            evs.push_back({std::max(te, ta), 0, -by});
+        }
+        cudaGetLastError();
+        std::sort(evs.begin(), evs.end(), [](const Ev &a, const Ev &b) {
+            return a.t < b.t || (a.t == b.t && a.kind < b.kind);
+        });
+        int64_t cur = 0, peak = 0;
+        for (auto &e : evs) { cur += e.bytes; peak = std::max(peak, cur); }
+        m->stats.ledger_peak_bytes = m->stats.pinned_hbm_bytes + peak;
+        m->stats.h2d_seconds = busy;
+    }
+    int32_t fb = 0;
+    for (auto &rb : m->routing) {
+        int32_t st[4];
+        if (cudaMemcpy(st, rb.r.status, sizeof(st), cudaMemcpyDeviceToHost) == cudaSuccess) fb += st[1];
+    }
+    m->stats.route_fallbacks = fb;
+    m->stats.route_flips = 0;
+    *out = m->stats;
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_model_reset_stats(pgmoe_model *m) {
+    std::lock_guard<std::mutex> g(m->mu);
+    const int64_t pinned = m->stats.pinned_hbm_bytes, slot = m->stats.slot_capacity_bytes;
+    m->stats = pgmoe_stats{};
+    m->stats.pinned_hbm_bytes = pinned;
+    m->stats.slot_capacity_bytes = slot;
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_model_set_timeline(pgmoe_model *m, int32_t enabled) {
+    std::lock_guard<std::mutex> g(m->mu);
+    cudaDeviceSynchronize();
+    for (auto &e : m->tl) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    m->tl.clear();
+    m->t0_recorded = false;
+    m->timeline = enabled != 0;
+    return PGMOE_OK;
+}
+
+extern "C" int64_t pgmoe_model_timeline_jsonl(pgmoe_model *m, char *buf, int64_t cap) {
+    std::lock_guard<std::mutex> g(m->mu);
+    cudaDeviceSynchronize();
+    std::string outs;
+    for (auto &e : m->tl) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, m->t0, e.a);
+        cudaEventElapsedTime(&b, m->t0, e.b);
+        char line[256];
+        snprintf(line, sizeof(line), "{\"lane\": \"%s\", \"label\": \"%s\", \"block\": %d, \"start_s\": %.9g, \"end_s\": %.9g}\n",
+                 e.lane, e.label.c_str(), e.block, std::max(0.f, a) * 1e-3, std::max(0.f, b) * 1e-3);
+        outs += line;
+    }
+    cudaGetLastError();
+    if (buf && cap > 0) {
+        const int64_t n = std::min<int64_t>(cap - 1, (int64_t)outs.size());
+        memcpy(buf, outs.data(), n);
+        buf[n] = 0;
+    }
+    return (int64_t)outs.size();
+}

@@ -1,0 +1,331 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle,
+which is itself pinned bit-for-bit to the reference (tests/test_oracle.py).
+
+Bars (north star): routing ids / permutation bit-exact; combine weights
+fp32-relative 1e-6; block outputs normwise ||y - y_ref||_inf/||y_ref||_inf
+<= 1e-4 (fp32 weights) and <= 2e-2 (bf16 weights), teacher-forced per block
+(the oracle runs on the GPU's own block input promoted to fp64).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as og  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-4, "bf16": 2e-2}
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def P():
+    import paper_2308_12066_b200 as p
+    return p
+
+
+def as_torch_w(a: np.ndarray) -> "torch.Tensor":
+    if a.dtype == np.uint16:
+        return torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).cuda()
+    return torch.from_numpy(a).cuda()
+
+
+def normwise(y, ref):
+    ref = np.asarray(ref, dtype=np.float64)
+    den = np.max(np.abs(ref))
+    return float(np.max(np.abs(np.asarray(y, dtype=np.float64) - ref)) / (den if den > 0 else 1.0))
+
+
+def tokens(d, T, seed=0, scale=1.0):
+    from paper_2308_12066_b200._rng import token_batch
+    return token_batch(seed, d, T) * np.float32(scale)
+
+
+# ---------------------------------------------------------------- rng ----
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_device_weight_generator_bit_exact(dtype):
+    p = P()
+    for (rows, cols, tag, b, e) in [(3072, 768, og.TAG_W1, 0, 0), (768, 128, og.TAG_PRE_GATE, 5, -1),
+                                    (13, 7, og.TAG_W2, 1, 2)]:
+        t = p.fill_weights(rows, cols, seed=0, tag=tag, block=b, expert=e, dtype=dtype)
+        got = t.view(torch.int16).cpu().numpy().view(np.uint16) if dtype == "bf16" else t.cpu().numpy()
+        ref = og.weights(og.derive_seed(0, tag, b, e), rows, cols, dtype)
+        assert np.array_equal(got, ref)
+
+
+# -------------------------------------------------------------- route ----
+
+def _check_route(x, G, k, r):
+    ids_ref, w_ref = og.gate_batch(x.astype(np.float64), G, k, nthreads=8)
+    ids = r.ids.cpu().numpy()
+    assert np.array_equal(ids, ids_ref), "routing ids differ from the reference"
+    w = r.w.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(w - w_ref) / w_ref) <= 1e-6
+    hist, off, perm, act = og.permute(ids_ref, G.shape[1])
+    assert np.array_equal(r.hist.cpu().numpy(), hist)
+    assert np.array_equal(r.off.cpu().numpy(), off)
+    assert np.array_equal(r.perm.cpu().numpy()[: ids.size], perm)
+    assert np.array_equal(r.act.cpu().numpy(), act)
+    assert np.array_equal(r.w_perm.cpu().numpy()[: ids.size], r.w.cpu().numpy().reshape(-1)[perm])
+    return ids_ref
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("shape", [(1024, 128), (768, 64), (768, 8)])
+@pytest.mark.parametrize("T", [1, 37, 300, 700])
+def test_route_bit_exact_switch_shapes(dtype, shape, T):
+    p = P()
+    d, E = shape
+    G = og.weights(og.derive_seed(0, og.TAG_PRE_GATE, 3, -1), d, E, dtype)
+    x = tokens(d, T, seed=T)
+    r = p.route(torch.from_numpy(x).cuda(), as_torch_w(G), 1)
+    st = r.check()
+    assert st["flips"] == 0
+    _check_route(x, G, 1, r)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_route_topk_and_exact_ties_take_the_serial_path(k):
+    """Duplicated gate columns give bit-equal logits: the certified fast path
+    cannot separate them, the serial fallback must rank them by id."""
+    p = P()
+    rng = np.random.default_rng(k)
+    d, E, T = 256, 24, 64
+    G = rng.uniform(-0.1, 0.1, size=(d, E)).astype(np.float32)
+    G[:, 7] = G[:, 3]
+    G[:, 20] = G[:, 3]
+    G[:, 11] = G[:, 0]
+    x = rng.uniform(-0.1, 0.1, size=(T, d)).astype(np.float32)
+    # make column 3 the winner for half the tokens
+    x[::2] = np.sign(G[:, 3])[None, :] * 0.05
+    r = p.route(torch.from_numpy(x).cuda(), torch.from_numpy(G).cuda(), k)
+    st = r.check()
+    assert st["fallbacks"] >= T // 2
+    ids_ref = _check_route(x, G, k, r)
+    assert (ids_ref[::2, 0] == 3).all()
+
+
+def test_route_near_ties_one_ulp_apart():
+    p = P()
+    rng = np.random.default_rng(5)
+    d, E, T = 512, 16, 32
+    G = rng.uniform(-0.1, 0.1, size=(d, E)).astype(np.float32)
+    G[:, 9] = G[:, 2]
+    G[100, 9] = np.nextafter(G[100, 2], np.float32(1))  # logits differ in the last bits
+    x = np.tile(np.sign(G[:, 2]) * 0.03, (T, 1)).astype(np.float32)
+    x += rng.uniform(-1e-7, 1e-7, size=x.shape).astype(np.float32)
+    r = p.route(torch.from_numpy(x).cuda(), torch.from_numpy(G).cuda(), 2)
+    r.check()
+    _check_route(x, G, 2, r)
+
+
+def test_route_golden_reference_gate_large():
+    """Reference outputs (moesim.gate_forward) on the Large-128 gate shape."""
+    p = P()
+    with open(os.path.join(GOLD, "switch.json")) as fh:
+        cases = json.load(fh)["data"]["gate_large"]
+    for c in cases:
+        model = og.OracleModel(og.Dims(1024, 4096, 24, 128, 1), c["dtype"])
+        G = model.gate(0) if c["which"] == "gate" else model.pre_gate(c["block"])
+        x = np.array([float.fromhex(v) for v in c["x"]], dtype=np.float32)[None, :]
+        r = p.route(torch.from_numpy(x).cuda(), as_torch_w(G), 1)
+        r.check()
+        assert r.ids.cpu().tolist() == [c["ids"]]
+        assert abs(float(r.w[0, 0]) - float.fromhex(c["w"][0])) <= 1e-6 * float.fromhex(c["w"][0])
+
+
+def test_route_errors_surface_as_reference_exceptions():
+    p = P()
+    G = torch.zeros((4, 2), device="cuda")
+    G[0, 0], G[0, 1] = 1.0, -1.0
+    x = torch.full((1, 4), float("inf"), device="cuda")
+    with pytest.raises(p.GateOverflowError, match="numerical overflow in gate"):
+        p.route(x, G, 1).check()
+    x = torch.zeros((1, 4), device="cuda")
+    x[0, 0] = 1000.0
+    with pytest.raises(p.GateOverflowError, match="underflowed to zero"):
+        p.route(x, G, 2).check()
+    with pytest.raises(p.ConfigError):
+        p.route(torch.zeros((1, 4), device="cuda"), G, 3)
+    with pytest.raises(p.ShapeError):
+        p.route(torch.zeros((1, 5), device="cuda"), G, 1)
+
+
+def test_route_empty_batch():
+    p = P()
+    G = torch.rand((64, 8), device="cuda")
+    r = p.route(torch.zeros((0, 64), device="cuda"), G, 1)
+    torch.cuda.synchronize()
+    assert r.n_act == 0 and int(r.hist.sum()) == 0
+
+
+# ---------------------------------------------------- block / decoder ----
+
+def _device_model(dims: og.Dims, dtype: str, placement="resident", max_tokens=64, kernel="auto"):
+    p = P()
+    cfg = p.ModelConfig(d_model=dims.d_model, d_ff=dims.d_ff, num_blocks=dims.num_blocks,
+                        num_experts=dims.num_experts, top_k=dims.top_k,
+                        activation_level=dims.activation_level, seed=dims.seed)
+    return p.DeviceModel(cfg, dtype=dtype, placement=placement, max_tokens=max_tokens, kernel=kernel)
+
+
+def _teacher_forced_chain(m, oracle_model, x0, tol, check_blocks=None):
+    """Runs moe_block_forward block by block on the device and checks each
+    block against the oracle on the device's own block input."""
+    p = P()
+    c = m.config
+    x = torch.from_numpy(x0).cuda()
+    T = x.shape[0]
+    pending = {}
+    outs = []
+    for b in range(c.num_blocks):
+        if c.has_conv_gate(b):
+            r_in = p.route(x, m.matrix("gate", b), c.top_k)
+        else:
+            r_in = pending.pop(b)
+        r_in.check()
+        y, r_out = m.moe_block_forward(b, x, r_in)
+        torch.cuda.synchronize()
+        if check_blocks is None or b in check_blocks:
+            xb = x.cpu().numpy().astype(np.float64)
+            ids_in = r_in.ids.cpu().numpy()
+            w_in = r_in.w.cpu().numpy().astype(np.float64)
+            # consumed routing == reference gate on the same input
+            G = oracle_model.gate(b) if c.has_conv_gate(b) else None
+            if G is not None:
+                ids_ref, _ = og.gate_batch(xb, G, c.top_k, nthreads=8)
+                assert np.array_equal(ids_in, ids_ref)
+            w1 = {e: oracle_model.w1(b, e) for e in np.unique(ids_in)}
+            w2 = {e: oracle_model.w2(b, e) for e in np.unique(ids_in)}
+            y_ref = og.block_batch(xb, ids_in, w_in, w1, w2, oracle_model.dense(b), c.num_experts, nthreads=8)
+            err = normwise(y.cpu().numpy(), y_ref)
+            assert err <= tol, f"block {b}: normwise error {err:.3g} > {tol}"
+            if r_out is not None:
+                r_out.check()
+                ids_ref, w_ref = og.gate_batch(xb, oracle_model.pre_gate(b), c.top_k, nthreads=8)
+                assert np.array_equal(r_out.ids.cpu().numpy(), ids_ref)
+        if r_out is not None:
+            pending[b + c.activation_level] = r_out
+        outs.append(y)
+        x = y
+    return outs
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_block_parity_base8_teacher_forced(dtype):
+    dims = og.Dims(768, 3072, 12, 8, 1)
+    m = _device_model(dims, dtype, max_tokens=16)
+    om = og.OracleModel(dims, dtype)
+    x0 = tokens(768, 16)
+    _teacher_forced_chain(m, om, x0, TOL[dtype], check_blocks={0, 1, 5, 11})
+    m.close()
+
+
+def test_block_matches_reference_golden_outputs():
+    """moesim.moe_block_forward outputs captured by gen_golden.py."""
+    p = P()
+    with open(os.path.join(GOLD, "switch.json")) as fh:
+        cases = json.load(fh)["data"]["block_base8"]
+    for dtype in ("f32", "bf16"):
+        m = _device_model(og.Dims(768, 3072, 12, 8, 1), dtype, max_tokens=4)
+        for c in (c for c in cases if c["dtype"] == dtype):
+            x = torch.tensor([[float.fromhex(v) for v in c["x"]]], dtype=torch.float32, device="cuda")
+            r_in = p.DeviceRouting.from_host(np.array([c["ids_in"]]), np.array([[float.fromhex(c["w_in"][0])]]), 8)
+            y, r_out = m.moe_block_forward(c["block"], x, r_in)
+            y_ref = [float.fromhex(v) for v in c["y"]]
+            assert normwise(y[0].cpu().numpy(), y_ref) <= TOL[dtype]
+            r_out.check()
+            assert r_out.ids.cpu().tolist() == [c["ids_out"]]
+        m.close()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_decoder_iteration_equals_block_chain_and_small_configs(dtype):
+    rng = np.random.default_rng(11)
+    for trial in range(6):
+        dims = og.Dims(d_model=int(rng.integers(2, 40)), d_ff=int(rng.integers(2, 50)),
+                       num_blocks=int(rng.integers(2, 6)), num_experts=int(rng.integers(2, 17)),
+                       top_k=int(rng.integers(1, 3)), activation_level=1, seed=trial)
+        if dims.top_k > dims.num_experts:
+            continue
+        m = _device_model(dims, dtype, max_tokens=8)
+        om = og.OracleModel(dims, dtype)
+        x0 = tokens(dims.d_model, 8, seed=trial)
+        outs = _teacher_forced_chain(m, om, x0, TOL[dtype])
+        y, ids, w = m.decoder_iteration(torch.from_numpy(x0).cuda(), trace=True)
+        torch.cuda.synchronize()
+        assert torch.equal(y, outs[-1]), "decoder_iteration must equal the moe_block_forward chain bitwise"
+        m.close()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_offloaded_equals_resident_and_ledger(dtype):
+    dims = og.Dims(256, 512, 6, 16, 1, seed=4)
+    T = 24
+    x0 = torch.from_numpy(tokens(256, T)).cuda()
+    res = _device_model(dims, dtype, "resident", max_tokens=T)
+    off = _device_model(dims, dtype, "offloaded", max_tokens=T)
+    y0, ids0, w0 = res.decoder_iteration(x0, trace=True)
+    off.reset_stats()
+    y1, ids1, w1 = off.decoder_iteration(x0, trace=True)
+    torch.cuda.synchronize()
+    assert torch.equal(ids0, ids1) and torch.equal(w0, w1)
+    assert torch.equal(y0, y1)
+    st = off.stats()
+    rec = 2 * 256 * 512 * (2 if dtype == "bf16" else 4)
+    n_act = [len(np.unique(ids1[b].cpu().numpy())) for b in range(dims.num_blocks)]
+    assert st["h2d_bytes"] == sum(n_act) * rec
+    eq1 = st["pinned_hbm_bytes"] + max(rec * (n_act[i] + (n_act[i + 1] if i + 1 < len(n_act) else 0))
+                                       for i in range(len(n_act)))
+    assert st["eq1_peak_bytes"] == eq1
+    assert st["ledger_peak_bytes"] <= eq1
+    # host-buffer entry point gives the same answer
+    yh, idh, wh = off.decoder_iteration_host(x0.cpu().numpy(), trace=True)
+    assert np.array_equal(yh, y1.cpu().numpy()) and np.array_equal(idh, ids1.cpu().numpy())
+    res.close()
+    off.close()
+
+
+def test_timeline_schema_and_causality():
+    dims = og.Dims(128, 256, 4, 8, 1)
+    m = _device_model(dims, "bf16", "offloaded", max_tokens=8)
+    m.set_timeline(True)
+    m.decoder_iteration(torch.from_numpy(tokens(128, 8)).cuda())
+    ev = m.timeline()
+    assert {e["lane"] for e in ev} == {"compute", "transfer"}
+    for e in ev:
+        assert set(e) == {"lane", "label", "block", "start_s", "end_s"} and e["end_s"] >= e["start_s"]
+    fetch = {e["block"]: e for e in ev if e["lane"] == "transfer"}
+    experts = {e["block"]: e for e in ev if e["label"] == "experts"}
+    for b, e in experts.items():  # no expert runs before its transfer ends
+        assert e["start_s"] >= fetch[b]["end_s"] - 1e-6
+    m.close()
+
+
+# ------------------------------------------------- reference drop-ins ----
+
+def test_dropin_single_token_api_matches_oracle():
+    p = P()
+    rng = np.random.default_rng(3)
+    G = rng.uniform(-1, 1, size=(6, 8)).astype(np.float32).astype(np.float64)
+    x = rng.uniform(-1, 1, size=6).astype(np.float32).astype(np.float64)
+    d = p.gate_forward(x.tolist(), G.tolist(), 2)
+    ids, w, _ = og.gate_forward(x, G, 2)
+    assert d.expert_ids == ids
+    assert np.allclose(d.combine_weights, w, rtol=1e-6)
+
+    class Ex:
+        pass
+    ex = Ex()
+    ex.w1 = rng.uniform(-1, 1, size=(12, 6)).astype(np.float32).tolist()
+    ex.w2 = rng.uniform(-1, 1, size=(6, 12)).astype(np.float32).tolist()
+    y = p.expert_forward(x.tolist(), ex)
+    y_ref = og.expert_forward(x, np.array(ex.w1, np.float32), np.array(ex.w2, np.float32))
+    assert normwise(y, y_ref) <= 1e-5
+    with pytest.raises(p.ShapeError):
+        p.expert_forward([1.0, 2.0], ex)
