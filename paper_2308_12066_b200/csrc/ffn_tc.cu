@@ -1,16 +1,533 @@
-// ffn_tc.cu — placeholder until the tcgen05 kernels land.
+// ffn_tc.cu — K2/K3 on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// One persistent, warp-specialised grouped GEMM serves the three dense
+// contractions of a block (core.py:308-316, :338):
+//   up   : H[r][m]  = relu(W1_e[m] . x[tok(r)])              (M = f, K = d)
+//   down : yw[perm[r]][m] = w_perm[r] * (W2_e[m] . H[r])     (M = d, K = f)
+//   dense: y[t][m]  = D[m] . sum_s yw[t*k+s]                 (M = d, K = d)
+// "Swap-AB": the weight rows fill the 128-row UMMA M dimension, the (few)
+// routed tokens of an expert are the N dimension (padded to 16), so the
+// tensor core streams each weight tile exactly once — the kernel is HBM
+// bound on weight bytes, which is the roofline at these shapes.
+//
+// Warp roles (256 threads, one CTA per SM):
+//   warp 0      : TMA producer — weight tiles [128 x 64] bf16, SWIZZLE_128B,
+//                 3-D tensor map over the expert records (K, rows, record)
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-3   : B producers — gather routed token rows (fp32), convert to
+//                 bf16 and store them in the UMMA K-major SWIZZLE_128B layout
+//   warps 4-7   : epilogue — tcgen05.ld the fp32 accumulator, apply ReLU /
+//                 combine weight / scatter (or split-K fix-up) and store
+// Small-T launches (few tiles) split K across CTAs; the last CTA to finish
+// a tile sums the partials in split order (deterministic) and applies the
+// epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace pgmoe {
-bool tc_supported(int, int) { return false; }
-int expert_ffn_tc(const float *, int, int, int, int, const void *, size_t, int, const pgmoe_routing *,
-                  float *, float *, void *, size_t, cudaStream_t) {
-    set_error("tcgen05 path not built");
-    return PGMOE_E_CONFIG;
+
+namespace tc {
+
+constexpr int kThreads = 256;
+constexpr int BM = 128;     // UMMA M (weight rows per tile)
+constexpr int BK = 64;      // bf16 elements per 128-byte swizzle row
+constexpr int kABytes = BM * BK * 2;  // 16 KB
+constexpr int kMaxGroups = 1024;
+constexpr int kCounterInts = 8192;    // split-K tile counters at the head of the workspace
+
+enum Mode { kUp = 0, kDown = 1, kDense = 2 };
+
+struct Params {
+    int mode, M, K, T, k;
+    const int *act, *n_act, *off, *hist, *perm;
+    const float *w_perm;
+    int indexed_by_act;
+    const float *src;
+    float *dst;
+    int *counters;
+    float *partial;
+    long long partial_cap;  // floats
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-int dense_tc(const float *, int, int, int, const void *, float *, void *, size_t, cudaStream_t) {
-    set_error("tcgen05 path not built");
-    return PGMOE_E_CONFIG;
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
+    d |= (uint64_t)1 << 16;                        // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;              // SBO: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
+    return d;
+}
+// Instruction descriptor: bf16 x bf16 -> fp32, both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t idesc_bf16(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    const uint32_t lo = __bfloat16_as_ushort(__float2bfloat16_rn(a));
+    const uint32_t hi = __bfloat16_as_ushort(__float2bfloat16_rn(b));
+    return lo | (hi << 16);
+}
+
+struct Sched {
+    int groups, m_tiles, kb_total, kbs, S;
+    long long tiles, units;
+    int *prefix;  // [groups + 1] tile prefix (smem)
+};
+
+struct Unit {
+    int g, m_tile, n0, n_valid, n_pad, kb0, kb1, tile, s, tok0, rec;
+};
+
+template <int BN>
+__device__ __forceinline__ Unit decode_unit(const Params &p, const Sched &sc, long long u) {
+    Unit x;
+    x.tile = (int)(u / sc.S);
+    x.s = (int)(u - (long long)x.tile * sc.S);
+    int lo = 0, hi = sc.groups - 1;  // last g with prefix[g] <= tile
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sc.prefix[mid] <= x.tile) lo = mid;
+        else hi = mid - 1;
+    }
+    x.g = lo;
+    const int local = x.tile - sc.prefix[lo];
+    const int n_tile = local / sc.m_tiles;
+    x.m_tile = local - n_tile * sc.m_tiles;
+    int ng, e = 0;
+    if (p.mode == kDense) {
+        ng = p.T;
+        x.tok0 = 0;
+        x.rec = 0;
+    } else {
+        e = p.act[x.g];
+        ng = p.hist[e];
+        x.tok0 = p.off[e];
+        x.rec = p.indexed_by_act ? x.g : e;
+    }
+    x.n0 = n_tile * BN;
+    x.n_valid = min(BN, ng - x.n0);
+    x.n_pad = max(16, (x.n_valid + 15) & ~15);
+    x.kb0 = x.s * sc.kbs;
+    x.kb1 = min(sc.kb_total, x.kb0 + sc.kbs);
+    return x;
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap wmap, Params p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                            ~uintptr_t(1023));
+    constexpr int kBBytes = BN * 128;
+    unsigned char *sA = smem;
+    unsigned char *sB = smem + STAGES * kABytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * kBBytes);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    int *s_flag = reinterpret_cast<int *>(tmem_slot + 1);
+    int *prefix = s_flag + 4;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // ---- schedule (identical in every CTA) --------------------------------
+    Sched sc;
+    sc.groups = (p.mode == kDense) ? 1 : *p.n_act;
+    sc.m_tiles = p.M / BM;
+    sc.kb_total = p.K / BK;
+    sc.prefix = prefix;
+    if (warp == 0) {
+        int run = 0;
+        for (int g0 = 0; g0 < sc.groups; g0 += 32) {
+            const int g = g0 + lane;
+            int nt = 0;
+            if (g < sc.groups) {
+                const int ng = (p.mode == kDense) ? p.T : p.hist[p.act[g]];
+                nt = ((ng + BN - 1) / BN) * sc.m_tiles;
+            }
+            int incl = nt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (g < sc.groups) prefix[g] = run + incl - nt;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) prefix[sc.groups] = run;
+    }
+    if (warp == 1) {  // TMEM: two accumulator stages of BN fp32 columns
+        constexpr uint32_t cols = (2 * BN < 32) ? 32 : 2 * BN;
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1 + 64);  // TMA arrive.expect_tx + 64 B-producer threads
+            mbar_init(&empty[i], 1);      // tcgen05.commit
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    sc.tiles = prefix[sc.groups];
+    {
+        // split-K so that small launches still cover every SM
+        int S = 1;
+        const long long want = 2LL * gridDim.x;
+        if (sc.tiles > 0 && sc.tiles < want) { const long long q = (want + sc.tiles - 1) / sc.tiles; S = (int)(q < sc.kb_total ? q : sc.kb_total); }
+        while (S > 1 && ((long long)sc.tiles * S * BN * BM > p.partial_cap || sc.tiles > kCounterInts)) --S;
+        sc.kbs = (sc.kb_total + S - 1) / S;
+        sc.S = (sc.kb_total + sc.kbs - 1) / sc.kbs;
+    }
+    sc.units = sc.tiles * sc.S;
+
+    if (warp == 0) {
+        // ================= TMA producer: weight tiles =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (long long u = blockIdx.x; u < sc.units; u += gridDim.x) {
+                const Unit x = decode_unit<BN>(p, sc, u);
+                for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], kABytes);
+                    tma_load_3d(sA + stage * kABytes, &wmap, &full[stage], kb * BK, x.m_tile * BM, x.rec);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer (single thread) ======================
+        int stage = 0, cnt = 0;
+        uint32_t phase = 0;
+        for (long long u = blockIdx.x; u < sc.units; u += gridDim.x, ++cnt) {
+            const Unit x = decode_unit<BN>(p, sc, u);
+            const int acc = cnt & 1;
+            mbar_wait(&tempty[acc], ((cnt >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t tmem_d = tmem_base + acc * BN;
+            const uint32_t idesc = idesc_bf16(x.n_pad);
+            for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a0 = smem_u32(sA + stage * kABytes);
+                    const uint32_t b0 = smem_u32(sB + stage * kBBytes);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        umma_bf16(tmem_d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc,
+                                  (kb > x.kb0 || kk > 0) ? 1u : 0u);
+                    umma_commit(&empty[stage]);
+                }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            if (lane == 0) umma_commit(&tfull[acc]);
+            __syncwarp();
+        }
+    } else if (warp < 4) {
+        // ================= B producers: routed token rows -> bf16 ===========
+        const int bt = tid - 64;  // 0..63
+        int stage = 0;
+        uint32_t phase = 0;
+        for (long long u = blockIdx.x; u < sc.units; u += gridDim.x) {
+            const Unit x = decode_unit<BN>(p, sc, u);
+            for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                unsigned char *dst = sB + stage * kBBytes;
+                const int kcol = kb * BK;
+                for (int it = bt; it < x.n_pad * 8; it += 64) {
+                    const int n = it >> 3, c = it & 7;
+                    uint4 out = make_uint4(0, 0, 0, 0);
+                    if (n < x.n_valid) {
+                        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                        const int col = x.n0 + n;
+                        if (p.mode == kDense) {
+                            for (int s = 0; s < p.k; ++s) {
+                                const float4 *q = reinterpret_cast<const float4 *>(
+                                    p.src + ((size_t)col * p.k + s) * p.K + kcol + c * 8);
+                                const float4 a = __ldg(q), b = __ldg(q + 1);
+                                v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+                                v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+                            }
+                        } else {
+                            const int row = (p.mode == kUp) ? __ldg(p.perm + x.tok0 + col) / p.k : x.tok0 + col;
+                            const float4 *q = reinterpret_cast<const float4 *>(p.src + (size_t)row * p.K + kcol + c * 8);
+                            const float4 a = __ldg(q), b = __ldg(q + 1);
+                            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+                            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+                        }
+                        out = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                                         pack_bf16(v[6], v[7]));
+                    }
+                    // K-major SWIZZLE_128B: row n at 128 B, 16-B chunk c XOR (n % 8)
+                    *reinterpret_cast<uint4 *>(dst + (n >> 3) * 1024 + (n & 7) * 128 + ((c ^ (n & 7)) << 4)) = out;
+                }
+                fence_async_smem();
+                mbar_arrive(&full[stage]);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else {
+        // ================= epilogue: TMEM -> registers -> global ===========
+        const int ew = warp - 4;          // TMEM lanes 32*ew .. 32*ew+31
+        const int et = tid - 128;         // 0..127
+        int cnt = 0;
+        for (long long u = blockIdx.x; u < sc.units; u += gridDim.x, ++cnt) {
+            const Unit x = decode_unit<BN>(p, sc, u);
+            const int acc = cnt & 1;
+            mbar_wait(&tfull[acc], (cnt >> 1) & 1);
+            tc_fence_after();
+            const int m = x.m_tile * BM + et;
+            const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+            if (sc.S == 1) {
+                for (int c0 = 0; c0 < x.n_pad; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(taddr + c0, v);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int n = c0 + j;
+                        if (n >= x.n_valid) break;
+                        const int col = x.n0 + n;
+                        if (p.mode == kUp) {
+                            p.dst[(size_t)(x.tok0 + col) * p.M + m] = fmaxf(v[j], 0.f);
+                        } else if (p.mode == kDown) {
+                            const int r = x.tok0 + col;
+                            p.dst[(size_t)__ldg(p.perm + r) * p.M + m] = __ldg(p.w_perm + r) * v[j];
+                        } else {
+                            p.dst[(size_t)col * p.M + m] = v[j];
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&tempty[acc]);
+            } else {
+                float *part = p.partial + ((size_t)x.tile * sc.S + x.s) * (BN * BM);
+                for (int c0 = 0; c0 < x.n_pad; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(taddr + c0, v);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (c0 + j < x.n_valid) part[(size_t)(c0 + j) * BM + et] = v[j];
+                }
+                tc_fence_before();
+                mbar_arrive(&tempty[acc]);  // accumulator free: the rest works from global
+                __threadfence();
+                named_sync(1, 128);
+                if (et == 0) s_flag[0] = (atomicAdd(p.counters + x.tile, 1) == sc.S - 1);
+                named_sync(1, 128);
+                if (s_flag[0]) {
+                    __threadfence();
+                    const float *base = p.partial + (size_t)x.tile * sc.S * (BN * BM);
+                    for (int n = 0; n < x.n_valid; ++n) {
+                        float acc_v = 0.f;
+                        for (int s = 0; s < sc.S; ++s) acc_v += __ldcg(base + ((size_t)s * BN + n) * BM + et);
+                        const int col = x.n0 + n;
+                        if (p.mode == kUp) {
+                            p.dst[(size_t)(x.tok0 + col) * p.M + m] = fmaxf(acc_v, 0.f);
+                        } else if (p.mode == kDown) {
+                            const int r = x.tok0 + col;
+                            p.dst[(size_t)__ldg(p.perm + r) * p.M + m] = __ldg(p.w_perm + r) * acc_v;
+                        } else {
+                            p.dst[(size_t)col * p.M + m] = acc_v;
+                        }
+                    }
+                    if (et == 0) p.counters[x.tile] = 0;
+                }
+                named_sync(1, 128);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        constexpr uint32_t cols = (2 * BN < 32) ? 32 : 2 * BN;
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
+    }
+}
+
+template <int BN, int STAGES>
+constexpr size_t smem_bytes() {
+    return 1024 + (size_t)STAGES * (kABytes + BN * 128) + (2 * STAGES + 4) * 8 + 32 + (kMaxGroups + 1) * 4;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// Weight view: nrec records of [rows][K] bf16, `rec_bytes` apart.
+static int make_map(CUtensorMap *map, const void *base, int K, int rows, int nrec, size_t rec_bytes) {
+    auto fn = encode_fn();
+    PG_REQUIRE(fn != nullptr, PGMOE_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)nrec};
+    const cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)rec_bytes};
+    const cuuint32_t box[3] = {BK, BM, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    PG_REQUIRE(r == CUDA_SUCCESS, PGMOE_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PGMOE_OK;
+}
+
+template <int BN, int STAGES>
+static int launch(const CUtensorMap &map, const Params &p, cudaStream_t s) {
+    constexpr size_t smem = smem_bytes<BN, STAGES>();
+    static bool attr = false;
+    if (!attr) {
+        PG_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        attr = true;
+    }
+    grouped_gemm_kernel<BN, STAGES><<<kNumSMs, kThreads, smem, s>>>(map, p);
+    PG_CUDA(cudaGetLastError());
+    count_launch();
+    return PGMOE_OK;
+}
+
+static int run(const CUtensorMap &map, Params p, int max_cols, void *ws, size_t ws_bytes, cudaStream_t s) {
+    PG_REQUIRE(ws_bytes > kCounterInts * 4 + 4096, PGMOE_E_CONFIG, "tcgen05 workspace too small");
+    p.counters = static_cast<int *>(ws);
+    p.partial = reinterpret_cast<float *>(static_cast<char *>(ws) + kCounterInts * 4);
+    p.partial_cap = (long long)((ws_bytes - kCounterInts * 4) / 4);
+    if (max_cols <= 64) return launch<64, 6>(map, p, s);
+    return launch<256, 4>(map, p, s);
+}
+
+}  // namespace tc
+
+bool tc_supported(int d, int f) { return d % 128 == 0 && f % 128 == 0 && d >= 128 && f >= 128; }
+
+int expert_ffn_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride,
+                  int indexed_by_act, const pgmoe_routing *r, float *h, float *yw, void *ws, size_t ws_bytes,
+                  cudaStream_t s) {
+    PG_REQUIRE(tc_supported(d, f), PGMOE_E_CONFIG, "tcgen05 path needs d, f multiples of 128");
+    PG_REQUIRE((reinterpret_cast<uintptr_t>(experts) & 15) == 0 && stride % 16 == 0, PGMOE_E_CONFIG,
+               "expert records must be 16-byte aligned");
+    // Records addressed through the map are < E (resident) or < n_act (slot
+    // cache), both <= 1024; the extent only bounds TMA address generation.
+    const int rec_extent = 1024;
+    tc::Params p{};
+    p.T = T;
+    p.k = k;
+    p.act = r->act; p.n_act = r->n_act; p.off = r->off; p.hist = r->hist; p.perm = r->perm; p.w_perm = r->w_perm;
+    p.indexed_by_act = indexed_by_act;
+    const int max_cols = T * k;
+    CUtensorMap up_map, dn_map;
+    PG_TRY(tc::make_map(&up_map, experts, d, f, rec_extent, stride));
+    PG_TRY(tc::make_map(&dn_map, static_cast<const char *>(experts) + (size_t)f * d * 2, f, d, rec_extent, stride));
+    p.mode = tc::kUp;
+    p.M = f;
+    p.K = d;
+    p.src = x;
+    p.dst = h;
+    PG_TRY(tc::run(up_map, p, max_cols, ws, ws_bytes, s));
+    p.mode = tc::kDown;
+    p.M = d;
+    p.K = f;
+    p.src = h;
+    p.dst = yw;
+    return tc::run(dn_map, p, max_cols, ws, ws_bytes, s);
+}
+
+int dense_tc(const float *yw, int T, int d, int k, const void *dense_w, float *y, void *ws, size_t ws_bytes,
+             cudaStream_t s) {
+    PG_REQUIRE(d % 128 == 0, PGMOE_E_CONFIG, "tcgen05 dense needs d multiple of 128");
+    tc::Params p{};
+    p.mode = tc::kDense;
+    p.M = d;
+    p.K = d;
+    p.T = T;
+    p.k = k;
+    p.src = yw;
+    p.dst = y;
+    CUtensorMap map;
+    PG_TRY(tc::make_map(&map, dense_w, d, d, 1, (size_t)d * d * 2));
+    return tc::run(map, p, T, ws, ws_bytes, s);
+}
+
 }  // namespace pgmoe

@@ -329,3 +329,65 @@ def test_dropin_single_token_api_matches_oracle():
     assert normwise(y, y_ref) <= 1e-5
     with pytest.raises(p.ShapeError):
         p.expert_forward([1.0, 2.0], ex)
+
+
+# ------------------------------------------------- tcgen05 vs SIMT / oracle
+
+@pytest.mark.parametrize("T,E,k", [(1, 128, 1), (5, 8, 1), (37, 64, 1), (256, 128, 1), (600, 2, 1), (64, 16, 2),
+                                   (300, 8, 2)])
+def test_tcgen05_grouped_ffn_matches_oracle(T, E, k):
+    """K2 on tcgen05 (split-K at small T, multi N-tiles for hot experts) vs
+    the oracle's fp64 experts+combine, and vs the SIMT kernel."""
+    p = P()
+    d, f = 256, 512
+    rng = np.random.default_rng(T * 7 + E)
+    G = og.weights(og.derive_seed(1, og.TAG_GATE, 0, -1), d, E, "bf16")
+    x = tokens(d, T, seed=E)
+    xt = torch.from_numpy(x).cuda()
+    r = p.route(xt, as_torch_w(G), k)
+    r.check()
+    recs = np.stack([np.concatenate([og.weights(og.derive_seed(1, og.TAG_W1, 0, e), f, d, "bf16").reshape(-1),
+                                     og.weights(og.derive_seed(1, og.TAG_W2, 0, e), d, f, "bf16").reshape(-1)])
+                     for e in range(E)])
+    recs_t = as_torch_w(recs)
+    yw_tc = p.expert_ffn(xt, r, recs_t, f, kernel="tcgen05")
+    yw_simt = p.expert_ffn(xt, r, recs_t, f, kernel="simt")
+    torch.cuda.synchronize()
+    ids = r.ids.cpu().numpy()
+    w = r.w.cpu().numpy().astype(np.float64)
+    ref = np.zeros((T * k, d))
+    for t in range(T):
+        for s in range(k):
+            e = ids[t, s]
+            ref[t * k + s] = w[t, s] * og.expert_forward(x[t].astype(np.float64), recs[e, : f * d].reshape(f, d),
+                                                         recs[e, f * d:].reshape(d, f))
+    assert normwise(yw_simt.cpu().numpy(), ref) <= 1e-4
+    assert normwise(yw_tc.cpu().numpy(), ref) <= TOL["bf16"]
+    # dense on tcgen05 (split-K, k-slot sum) vs oracle
+    D = og.weights(og.derive_seed(1, og.TAG_DENSE, 0, -1), d, d, "bf16")
+    y_tc = p.dense(yw_tc, T, k, as_torch_w(D), kernel="tcgen05")
+    mix = yw_tc.cpu().numpy().astype(np.float64).reshape(T, k, d).sum(1)
+    y_ref = np.stack([og.matvec(D, mix[t]) for t in range(T)])
+    assert normwise(y_tc.cpu().numpy(), y_ref) <= TOL["bf16"]
+
+
+def test_tcgen05_deterministic_across_runs():
+    p = P()
+    d, f, E, T = 256, 512, 4, 3
+    x = torch.from_numpy(tokens(d, T)).cuda()
+    G = as_torch_w(og.weights(og.derive_seed(2, og.TAG_GATE, 0, -1), d, E, "bf16"))
+    r = p.route(x, G, 1)
+    recs = torch.randn((E, 2 * f * d), device="cuda").to(torch.bfloat16) * 0.05
+    a = p.expert_ffn(x, r, recs, f, kernel="tcgen05")
+    b = p.expert_ffn(x, r, recs, f, kernel="tcgen05")
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("placement", ["resident", "offloaded"])
+def test_model_tcgen05_equals_teacher_forced_oracle_large_dims(placement):
+    dims = og.Dims(1024, 4096, 3, 128, 1)
+    m = _device_model(dims, "bf16", placement, max_tokens=64, kernel="tcgen05")
+    om = og.OracleModel(dims, "bf16")
+    _teacher_forced_chain(m, om, tokens(1024, 64), TOL["bf16"], check_blocks={0, 2})
+    m.close()
