@@ -340,6 +340,82 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def run_ep(args, rank: int, world: int):
+    """configs[4]: Switch-Large-128 expert-parallel over `world` GPUs (experts
+    sharded, resident in HBM), NCCL all-to-all dispatch/combine, T tokens
+    per rank (weak scaling)."""
+    import torch
+    import paper_2308_12066_b200 as P
+    from paper_2308_12066_b200 import _lib
+    from paper_2308_12066_b200._rng import token_batch
+    from paper_2308_12066_b200.ep import EPDecoder
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    pr = PRESETS[args.preset]
+    cfg = P.ModelConfig(top_k=1, activation_level=1, seed=0, **pr)
+    T = args.tokens
+    t_setup = time.perf_counter()
+    dec = EPDecoder(cfg, dtype="bf16", max_tokens=T, kernel=args.kernel)
+    setup_s = time.perf_counter() - t_setup
+    x_host = torch.from_numpy(token_batch(0, cfg.d_model, T, offset=rank * T)).pin_memory()
+    x = x_host.cuda()
+    L = _lib.load()
+    for _ in range(args.warmup):
+        dec.decoder_iteration(x)
+    torch.cuda.synchronize()
+    launches0 = L.pgmoe_launch_count()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        y, _ = dec.decoder_iteration(x)
+    ev1.record()
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    clk = clocks.stop()
+    launches = L.pgmoe_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    # end to end: pinned host tokens in, result out, every step
+    y_host = torch.empty_like(x_host).pin_memory()
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        xd = x_host.cuda(non_blocking=True)
+        y, _ = dec.decoder_iteration(xd)
+        y_host.copy_(y, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    t = torch.tensor([e2e_s], device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    nb = cfg.num_blocks
+    out = {
+        "metric": METRIC, "value": round(T * world / (ms * 1e-3), 3), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (reference RNG weights/tokens, SURVEY §8(d))",
+        "config": {"workload": f"Switch-{args.preset} expert-parallel x{world} (BASELINE configs[4])",
+                   "preset": args.preset, "placement": "resident-sharded", "tokens_per_rank": T,
+                   "global_batch": T * world, "num_blocks": nb, "parallelism": f"ep{world}",
+                   "exchange": "NCCL all_to_all_single dispatch + combine per block",
+                   "l2": "per-step expert bytes >> 126 MB L2", "kernel": args.kernel},
+        "per_block_latency_ms": round(ms / nb, 4),
+        "e2e": {"value": round(T * world / e2e_s, 3), "unit": "tokens/s",
+                "h2d_bytes_per_step": T * cfg.d_model * 4, "d2h_bytes_per_step": T * cfg.d_model * 4},
+        "gpu_launches": int(launches), "clocks": clk, "setup_s": round(setup_s, 2),
+    }
+    dec.close()
+    return out
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return None
@@ -375,6 +451,8 @@ def main():
     ap.add_argument("--kernel", choices=["auto", "simt", "tcgen05"], default="auto")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", choices=["auto", "single", "ep"], default="auto",
+                    help="auto: offloaded single-GPU at N=1, expert-parallel at N>1")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -383,14 +461,17 @@ def main():
         if out is not None:
             print(json.dumps(out), flush=True)
         return
-    if world > 1:
+    mode = args.mode if args.mode != "auto" else ("ep" if world > 1 else "single")
+    if world > 1 or mode == "ep":
         import torch
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        torch.distributed.init_process_group("nccl")
-    out = run_ours(args, rank, world)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        torch.distributed.init_process_group("nccl", rank=rank, world_size=world)
+    out = run_ep(args, rank, world) if mode == "ep" else run_ours(args, rank, world)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if world > 1 or mode == "ep":
         import torch
         torch.distributed.destroy_process_group()
 

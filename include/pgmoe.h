@@ -109,6 +109,22 @@ PGMOE_API int pgmoe_expert_forward(const float *x, int32_t T, int32_t d, int32_t
 PGMOE_API int pgmoe_dense_forward(const float *yw, int32_t T, int32_t d, int32_t k, const void *dense_w,
                         int32_t wdtype, float *y, int32_t kernel, pgmoe_stream_t stream);
 
+/* ---------------------------------------------- expert parallelism (EP) */
+
+/* Dispatch packing: out[r] = src[perm[r] / k] for r < n (rows of d floats). */
+PGMOE_API int pgmoe_gather_rows(const float *src, const int32_t *perm, int32_t n, int32_t d, int32_t k,
+                                float *out, pgmoe_stream_t stream);
+
+/* Combine un-permute: yw[perm[r]] = w_perm[r] * back[r] (linalg.py:45-51 weights). */
+PGMOE_API int pgmoe_unpermute_combine(const float *back, const int32_t *perm, const float *w_perm, int32_t n,
+                                      int32_t d, float *yw, pgmoe_stream_t stream);
+
+/* Receiver routing over rows received from P ranks: recv_cnt [P][El] holds
+ * how many rows each source sent for each local expert (rows arrive grouped
+ * by source, then by expert).  Fills hist/off/perm/act/n_act (w_perm = 1). */
+PGMOE_API int pgmoe_ep_local_routing(const int32_t *recv_cnt, int32_t P, int32_t El, const pgmoe_routing *out,
+                                     pgmoe_stream_t stream);
+
 /* Reads routing status after a sync: returns the device-detected error (or
  * PGMOE_OK) and optionally the serial-fallback / flip counters. */
 PGMOE_API int pgmoe_check_routing(const pgmoe_routing *r, int32_t *fallbacks, int32_t *flips);
@@ -141,6 +157,17 @@ typedef struct {
 PGMOE_API int pgmoe_model_create(const pgmoe_config *cfg, int32_t wdtype, int32_t placement,
                        int32_t max_tokens, pgmoe_model **out);
 PGMOE_API int pgmoe_model_destroy(pgmoe_model *m);
+
+/* Expert-parallel shard: same model, but only experts [expert_begin,
+ * expert_end) are stored (gates and dense layers are replicated).  Weight
+ * seeds use the global expert id, so shards reproduce the single-GPU model. */
+PGMOE_API int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, int32_t placement,
+                                    int32_t max_tokens, int32_t expert_begin, int32_t expert_end,
+                                    pgmoe_model **out);
+
+/* Device base of block `block`'s expert records (W1 then W2 per record). */
+PGMOE_API int pgmoe_model_expert_records(pgmoe_model *m, int32_t block, const void **base, size_t *stride,
+                                         int32_t *expert_begin, int32_t *n_local);
 
 /* Fill every matrix from the reference generator (device RNG; offloaded
  * experts are generated on the device then copied to pinned host memory). */

@@ -61,7 +61,8 @@ EXPORTS = (
     "pgmoe_model_set_kernel", "pgmoe_decoder_iteration", "pgmoe_decoder_iteration_host",
     "pgmoe_moe_block_forward", "pgmoe_model_matrix_ptr", "pgmoe_model_stats", "pgmoe_model_reset_stats",
     "pgmoe_model_timeline_jsonl", "pgmoe_model_set_timeline", "pgmoe_last_error", "pgmoe_version",
-    "pgmoe_launch_count",
+    "pgmoe_launch_count", "pgmoe_model_create_ex", "pgmoe_model_expert_records", "pgmoe_gather_rows",
+    "pgmoe_unpermute_combine", "pgmoe_ep_local_routing",
 )
 
 _lib = None
@@ -103,6 +104,11 @@ def load():
         "pgmoe_last_error": (ctypes.c_char_p, []),
         "pgmoe_version": (ctypes.c_char_p, []),
         "pgmoe_launch_count": (i64, []),
+        "pgmoe_model_create_ex": (i32, [P(Config), i32, i32, i32, i32, i32, P(vp)]),
+        "pgmoe_model_expert_records": (i32, [vp, i32, P(vp), P(sz), P(i32), P(i32)]),
+        "pgmoe_gather_rows": (i32, [vp, vp, i32, i32, i32, vp, vp]),
+        "pgmoe_unpermute_combine": (i32, [vp, vp, vp, i32, i32, vp, vp]),
+        "pgmoe_ep_local_routing": (i32, [vp, i32, i32, P(Routing), vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -280,7 +280,7 @@ class DeviceModel:
     """A pre-gated MoE decoder on one B200 (pgmoe_model)."""
 
     def __init__(self, config: ModelConfig, dtype: str = "bf16", placement: str = "resident",
-                 max_tokens: int = 256, kernel: str = "auto", init: str = "rng"):
+                 max_tokens: int = 256, kernel: str = "auto", init: str = "rng", expert_range=None):
         _require_cuda()
         self.config = config
         self.dtype = dtype
@@ -291,7 +291,10 @@ class DeviceModel:
         self._L = _lib.load()
         c = config.c_struct()
         pl = {"resident": _lib.RESIDENT, "offloaded": _lib.OFFLOADED}[placement]
-        _lib.check(self._L.pgmoe_model_create(ctypes.byref(c), self.wdt, pl, max_tokens, ctypes.byref(self._h)))
+        e0, e1 = expert_range if expert_range is not None else (0, config.num_experts)
+        self.expert_range = (e0, e1)
+        _lib.check(self._L.pgmoe_model_create_ex(ctypes.byref(c), self.wdt, pl, max_tokens, e0, e1,
+                                                 ctypes.byref(self._h)))
         self.set_kernel(kernel)
         if init == "rng":
             _lib.check(self._L.pgmoe_model_init_weights(self._h))

@@ -2,27 +2,32 @@
 //
 // One persistent, warp-specialised grouped GEMM serves the three dense
 // contractions of a block (core.py:308-316, :338):
-//   up   : H[r][m]  = relu(W1_e[m] . x[tok(r)])              (M = f, K = d)
-//   down : yw[perm[r]][m] = w_perm[r] * (W2_e[m] . H[r])     (M = d, K = f)
-//   dense: y[t][m]  = D[m] . sum_s yw[t*k+s]                 (M = d, K = d)
-// "Swap-AB": the weight rows fill the 128-row UMMA M dimension, the (few)
-// routed tokens of an expert are the N dimension (padded to 16), so the
-// tensor core streams each weight tile exactly once — the kernel is HBM
-// bound on weight bytes, which is the roofline at these shapes.
+//   up   : hb[r][m]  = bf16(relu(W1_e[m] . xb[r]))              (M = f, K = d)
+//   down : yw[perm[r]][m] = w_perm[r] * (W2_e[m] . hb[r])       (M = d, K = f)
+//          (+ mixb[perm[r]][m] = bf16(that) when top_k == 1)
+//   dense: y[t][m]  = D[m] . mixb[t]                            (M = d, K = d)
+// "Swap-AB": weight rows fill the 128-row UMMA M dimension and the few
+// routed tokens of an expert are the N dimension (padded to 16), so every
+// weight tile is streamed from HBM exactly once; the kernel is bound by
+// weight bytes, which is the roofline at these shapes.
 //
-// Warp roles (256 threads, one CTA per SM):
-//   warp 0      : TMA producer — weight tiles [128 x 64] bf16, SWIZZLE_128B,
-//                 3-D tensor map over the expert records (K, rows, record)
+// Both operands arrive by TMA into 128-byte-swizzled K-major tiles: the
+// weights through a 3-D map over the expert records (K, rows, record) and
+// the activations (bf16 rows packed once per GEMM in routing order, so an
+// expert's tokens are contiguous) through a 2-D map in 16-row boxes.
+//
+// Warp roles (192 threads, one CTA per SM):
+//   warp 0      : TMA producer (one elected lane)
 //   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-3   : B producers — gather routed token rows (fp32), convert to
-//                 bf16 and store them in the UMMA K-major SWIZZLE_128B layout
-//   warps 4-7   : epilogue — tcgen05.ld the fp32 accumulator, apply ReLU /
-//                 combine weight / scatter (or split-K fix-up) and store
-// Small-T launches (few tiles) split K across CTAs; the last CTA to finish
-// a tile sums the partials in split order (deterministic) and applies the
-// epilogue.
+//   warps 2-5   : epilogue — tcgen05.ld the fp32 accumulator, ReLU / combine
+//                 weight / scatter, or the split-K fix-up
+// Launches with few tiles split K across CTAs; the last CTA to finish a tile
+// (atomic ticket) sums the partials in split order — deterministic — and
+// runs the epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -31,12 +36,13 @@ namespace pgmoe {
 
 namespace tc {
 
-constexpr int kThreads = 256;
-constexpr int BM = 128;     // UMMA M (weight rows per tile)
-constexpr int BK = 64;      // bf16 elements per 128-byte swizzle row
+constexpr int kThreads = 192;
+constexpr int BM = 128;               // UMMA M (weight rows per tile)
+constexpr int BK = 64;                // bf16 elements per 128-byte swizzle row
 constexpr int kABytes = BM * BK * 2;  // 16 KB
+constexpr int kBRowsPerBox = 16;      // activation rows per TMA box (2 KB)
 constexpr int kMaxGroups = 1024;
-constexpr int kCounterInts = 8192;    // split-K tile counters at the head of the workspace
+constexpr int kCounterInts = 8192;    // split-K tile tickets at the head of the workspace
 
 enum Mode { kUp = 0, kDown = 1, kDense = 2 };
 
@@ -45,8 +51,8 @@ struct Params {
     const int *act, *n_act, *off, *hist, *perm;
     const float *w_perm;
     int indexed_by_act;
-    const float *src;
-    float *dst;
+    float *out_f32;       // kDown: yw [T*k][M] ; kDense: y [T][M]
+    uint16_t *out_bf16;   // kUp: hb [T*k][M] ; kDown (k == 1): mixb [T][M]
     int *counters;
     float *partial;
     long long partial_cap;  // floats
@@ -76,15 +82,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Weights are streamed once: evict-first in L2.
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
-                                            int c2) {
+                                            int c2, uint64_t policy) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
@@ -92,11 +105,11 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
-    d |= (uint64_t)1 << 16;                        // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;              // SBO: 8 rows x 128 B
-    d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);  // start address
+    d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;        // SBO: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                  // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
     return d;
 }
 // Instruction descriptor: bf16 x bf16 -> fp32, both K-major, M = 128, N = n.
@@ -127,20 +140,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-    const uint32_t lo = __bfloat16_as_ushort(__float2bfloat16_rn(a));
-    const uint32_t hi = __bfloat16_as_ushort(__float2bfloat16_rn(b));
-    return lo | (hi << 16);
-}
+__device__ __forceinline__ uint16_t bf16_bits(float a) { return __bfloat16_as_ushort(__float2bfloat16_rn(a)); }
 
 struct Sched {
     int groups, m_tiles, kb_total, kbs, S;
     long long tiles, units;
-    int *prefix;  // [groups + 1] tile prefix (smem)
+    const int *prefix;  // [groups + 1] tile prefix (smem)
 };
 
 struct Unit {
-    int g, m_tile, n0, n_valid, n_pad, kb0, kb1, tile, s, tok0, rec;
+    int g, m_tile, n0, n_valid, n_pad, kb0, kb1, tile, s, row0, rec;
 };
 
 template <int BN>
@@ -158,15 +167,15 @@ __device__ __forceinline__ Unit decode_unit(const Params &p, const Sched &sc, lo
     const int local = x.tile - sc.prefix[lo];
     const int n_tile = local / sc.m_tiles;
     x.m_tile = local - n_tile * sc.m_tiles;
-    int ng, e = 0;
+    int ng;
     if (p.mode == kDense) {
         ng = p.T;
-        x.tok0 = 0;
+        x.row0 = 0;
         x.rec = 0;
     } else {
-        e = p.act[x.g];
+        const int e = p.act[x.g];
         ng = p.hist[e];
-        x.tok0 = p.off[e];
+        x.row0 = p.off[e];
         x.rec = p.indexed_by_act ? x.g : e;
     }
     x.n0 = n_tile * BN;
@@ -177,9 +186,25 @@ __device__ __forceinline__ Unit decode_unit(const Params &p, const Sched &sc, lo
     return x;
 }
 
+template <int BN>
+__device__ __forceinline__ void store_out(const Params &p, const Unit &x, int n, int m, float v) {
+    const int col = x.n0 + n;
+    if (p.mode == kUp) {
+        p.out_bf16[(size_t)(x.row0 + col) * p.M + m] = bf16_bits(fmaxf(v, 0.f));  // relu, linalg.py:41-42
+    } else if (p.mode == kDown) {
+        const int r = x.row0 + col;
+        const int dst = __ldg(p.perm + r);
+        const float y = __ldg(p.w_perm + r) * v;  // combine weight (linalg.py:45-51)
+        p.out_f32[(size_t)dst * p.M + m] = y;
+        if (p.out_bf16) p.out_bf16[(size_t)dst * p.M + m] = bf16_bits(y);  // top-1: mix == w*y
+    } else {
+        p.out_f32[(size_t)col * p.M + m] = v;
+    }
+}
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-grouped_gemm_kernel(const __grid_constant__ CUtensorMap wmap, Params p) {
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, Params p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                             ~uintptr_t(1023));
@@ -228,17 +253,20 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap wmap, Params p) {
                      "r"(cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (tid == 0) {
+    if (tid == 64) {
         for (int i = 0; i < STAGES; ++i) {
-            mbar_init(&full[i], 1 + 64);  // TMA arrive.expect_tx + 64 B-producer threads
-            mbar_init(&empty[i], 1);      // tcgen05.commit
+            mbar_init(&full[i], 1);   // producer arrive.expect_tx (A + B bytes)
+            mbar_init(&empty[i], 1);  // tcgen05.commit
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 128);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
+    }
+    if (tid == 96) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&amap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&bmap) : "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -246,10 +274,13 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap wmap, Params p) {
     const uint32_t tmem_base = *tmem_slot;
     sc.tiles = prefix[sc.groups];
     {
-        // split-K so that small launches still cover every SM
+        // split K only when there are too few tiles to cover the SMs
         int S = 1;
         const long long want = 2LL * gridDim.x;
-        if (sc.tiles > 0 && sc.tiles < want) { const long long q = (want + sc.tiles - 1) / sc.tiles; S = (int)(q < sc.kb_total ? q : sc.kb_total); }
+        if (sc.tiles > 0 && sc.tiles < want) {
+            const long long q = (want + sc.tiles - 1) / sc.tiles;
+            S = (int)(q < sc.kb_total ? q : sc.kb_total);
+        }
         while (S > 1 && ((long long)sc.tiles * S * BN * BM > p.partial_cap || sc.tiles > kCounterInts)) --S;
         sc.kbs = (sc.kb_total + S - 1) / S;
         sc.S = (sc.kb_total + sc.kbs - 1) / sc.kbs;
@@ -257,16 +288,21 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap wmap, Params p) {
     sc.units = sc.tiles * sc.S;
 
     if (warp == 0) {
-        // ================= TMA producer: weight tiles =====================
+        // ================= TMA producer: weight tile + activation rows =====
         if (lane == 0) {
+            uint64_t policy;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
             int stage = 0;
             uint32_t phase = 0;
             for (long long u = blockIdx.x; u < sc.units; u += gridDim.x) {
                 const Unit x = decode_unit<BN>(p, sc, u);
+                const int brow = x.row0 + x.n0;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], kABytes);
-                    tma_load_3d(sA + stage * kABytes, &wmap, &full[stage], kb * BK, x.m_tile * BM, x.rec);
+                    mbar_expect_tx(&full[stage], kABytes + x.n_pad * 128);
+                    tma_load_3d(sA + stage * kABytes, &amap, &full[stage], kb * BK, x.m_tile * BM, x.rec, policy);
+                    for (int j = 0; j < x.n_pad; j += kBRowsPerBox)
+                        tma_load_2d(sB + stage * kBBytes + j * 128, &bmap, &full[stage], kb * BK, brow + j);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -300,53 +336,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap wmap, Params p) {
             if (lane == 0) umma_commit(&tfull[acc]);
             __syncwarp();
         }
-    } else if (warp < 4) {
-        // ================= B producers: routed token rows -> bf16 ===========
-        const int bt = tid - 64;  // 0..63
-        int stage = 0;
-        uint32_t phase = 0;
-        for (long long u = blockIdx.x; u < sc.units; u += gridDim.x) {
-            const Unit x = decode_unit<BN>(p, sc, u);
-            for (int kb = x.kb0; kb < x.kb1; ++kb) {
-                mbar_wait(&empty[stage], phase ^ 1);
-                unsigned char *dst = sB + stage * kBBytes;
-                const int kcol = kb * BK;
-                for (int it = bt; it < x.n_pad * 8; it += 64) {
-                    const int n = it >> 3, c = it & 7;
-                    uint4 out = make_uint4(0, 0, 0, 0);
-                    if (n < x.n_valid) {
-                        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                        const int col = x.n0 + n;
-                        if (p.mode == kDense) {
-                            for (int s = 0; s < p.k; ++s) {
-                                const float4 *q = reinterpret_cast<const float4 *>(
-                                    p.src + ((size_t)col * p.k + s) * p.K + kcol + c * 8);
-                                const float4 a = __ldg(q), b = __ldg(q + 1);
-                                v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
-                                v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
-                            }
-                        } else {
-                            const int row = (p.mode == kUp) ? __ldg(p.perm + x.tok0 + col) / p.k : x.tok0 + col;
-                            const float4 *q = reinterpret_cast<const float4 *>(p.src + (size_t)row * p.K + kcol + c * 8);
-                            const float4 a = __ldg(q), b = __ldg(q + 1);
-                            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-                            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-                        }
-                        out = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                                         pack_bf16(v[6], v[7]));
-                    }
-                    // K-major SWIZZLE_128B: row n at 128 B, 16-B chunk c XOR (n % 8)
-                    *reinterpret_cast<uint4 *>(dst + (n >> 3) * 1024 + (n & 7) * 128 + ((c ^ (n & 7)) << 4)) = out;
-                }
-                fence_async_smem();
-                mbar_arrive(&full[stage]);
-                if (++stage == STAGES) { stage = 0; phase ^= 1; }
-            }
-        }
     } else {
         // ================= epilogue: TMEM -> registers -> global ===========
-        const int ew = warp - 4;          // TMEM lanes 32*ew .. 32*ew+31
-        const int et = tid - 128;         // 0..127
+        const int q = warp & 3;        // TMEM lane quarter this warp may access
+        const int et = q * 32 + lane;  // accumulator row 0..127
         int cnt = 0;
         for (long long u = blockIdx.x; u < sc.units; u += gridDim.x, ++cnt) {
             const Unit x = decode_unit<BN>(p, sc, u);
@@ -354,36 +347,25 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap wmap, Params p) {
             mbar_wait(&tfull[acc], (cnt >> 1) & 1);
             tc_fence_after();
             const int m = x.m_tile * BM + et;
-            const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
             if (sc.S == 1) {
-                for (int c0 = 0; c0 < x.n_pad; c0 += 16) {
+                for (int c0 = 0; c0 < x.n_valid; c0 += 16) {
                     float v[16];
                     tmem_ld16(taddr + c0, v);
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int n = c0 + j;
-                        if (n >= x.n_valid) break;
-                        const int col = x.n0 + n;
-                        if (p.mode == kUp) {
-                            p.dst[(size_t)(x.tok0 + col) * p.M + m] = fmaxf(v[j], 0.f);
-                        } else if (p.mode == kDown) {
-                            const int r = x.tok0 + col;
-                            p.dst[(size_t)__ldg(p.perm + r) * p.M + m] = __ldg(p.w_perm + r) * v[j];
-                        } else {
-                            p.dst[(size_t)col * p.M + m] = v[j];
-                        }
-                    }
+                    for (int j = 0; j < 16; ++j)
+                        if (c0 + j < x.n_valid) store_out<BN>(p, x, c0 + j, m, v[j]);
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[acc]);
             } else {
                 float *part = p.partial + ((size_t)x.tile * sc.S + x.s) * (BN * BM);
-                for (int c0 = 0; c0 < x.n_pad; c0 += 16) {
+                for (int c0 = 0; c0 < x.n_valid; c0 += 16) {
                     float v[16];
                     tmem_ld16(taddr + c0, v);
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        if (c0 + j < x.n_valid) part[(size_t)(c0 + j) * BM + et] = v[j];
+                        if (c0 + j < x.n_valid) __stcg(part + (size_t)(c0 + j) * BM + et, v[j]);
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[acc]);  // accumulator free: the rest works from global
@@ -393,19 +375,20 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap wmap, Params p) {
                 named_sync(1, 128);
                 if (s_flag[0]) {
                     __threadfence();
-                    const float *base = p.partial + (size_t)x.tile * sc.S * (BN * BM);
-                    for (int n = 0; n < x.n_valid; ++n) {
-                        float acc_v = 0.f;
-                        for (int s = 0; s < sc.S; ++s) acc_v += __ldcg(base + ((size_t)s * BN + n) * BM + et);
-                        const int col = x.n0 + n;
-                        if (p.mode == kUp) {
-                            p.dst[(size_t)(x.tok0 + col) * p.M + m] = fmaxf(acc_v, 0.f);
-                        } else if (p.mode == kDown) {
-                            const int r = x.tok0 + col;
-                            p.dst[(size_t)__ldg(p.perm + r) * p.M + m] = __ldg(p.w_perm + r) * acc_v;
-                        } else {
-                            p.dst[(size_t)col * p.M + m] = acc_v;
+                    const float *base = p.partial + (size_t)x.tile * sc.S * (BN * BM) + et;
+                    for (int n0 = 0; n0 < x.n_valid; n0 += 4) {
+                        float a4[4] = {0.f, 0.f, 0.f, 0.f};
+                        for (int s = 0; s < sc.S; ++s) {  // split order: deterministic
+                            float v4[4];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                v4[j] = (n0 + j < x.n_valid) ? __ldcg(base + ((size_t)s * BN + n0 + j) * BM) : 0.f;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) a4[j] += v4[j];
                         }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (n0 + j < x.n_valid) store_out<BN>(p, x, n0 + j, m, a4[j]);
                     }
                     if (et == 0) p.counters[x.tile] = 0;
                 }
@@ -419,6 +402,43 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap wmap, Params p) {
         tc_fence_after();
         constexpr uint32_t cols = (2 * BN < 32) ? 32 : 2 * BN;
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
+    }
+}
+
+// xb[r] = bf16(x[perm[r] / k])  (activation rows in routing order)
+__global__ void pack_rows_bf16_kernel(const float *__restrict__ x, const int *__restrict__ perm, int n, int d, int k,
+                                      uint16_t *__restrict__ xb) {
+    const int vec = d / 8;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * vec;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / vec), c = (int)(i - (long long)r * vec);
+        const int row = perm ? __ldg(perm + r) / k : r;
+        const float4 *s = reinterpret_cast<const float4 *>(x + (size_t)row * d) + 2 * c;
+        const float4 a = __ldg(s), b = __ldg(s + 1);
+        uint4 o;
+        o.x = bf16_bits(a.x) | ((uint32_t)bf16_bits(a.y) << 16);
+        o.y = bf16_bits(a.z) | ((uint32_t)bf16_bits(a.w) << 16);
+        o.z = bf16_bits(b.x) | ((uint32_t)bf16_bits(b.y) << 16);
+        o.w = bf16_bits(b.z) | ((uint32_t)bf16_bits(b.w) << 16);
+        reinterpret_cast<uint4 *>(xb)[(size_t)r * vec + c] = o;
+    }
+}
+
+// mixb[t] = bf16(sum_s yw[t*k+s]) in slot (routing) order, linalg.py:45-51
+__global__ void sum_slots_bf16_kernel(const float *__restrict__ yw, int T, int d, int k, uint16_t *__restrict__ mixb) {
+    const int vec = d / 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)T * vec;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int t = (int)(i / vec), c = (int)(i - (long long)t * vec);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s = 0; s < k; ++s) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(yw + ((size_t)t * k + s) * d) + c);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        uint2 o;
+        o.x = bf16_bits(acc.x) | ((uint32_t)bf16_bits(acc.y) << 16);
+        o.y = bf16_bits(acc.z) | ((uint32_t)bf16_bits(acc.w) << 16);
+        reinterpret_cast<uint2 *>(mixb)[(size_t)t * vec + c] = o;
     }
 }
 
@@ -439,8 +459,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// Weight view: nrec records of [rows][K] bf16, `rec_bytes` apart.
-static int make_map(CUtensorMap *map, const void *base, int K, int rows, int nrec, size_t rec_bytes) {
+// Weight view: nrec records of [rows][K] bf16, `rec_bytes` apart; box 128 x 64.
+static int make_wmap(CUtensorMap *map, const void *base, int K, int rows, int nrec, size_t rec_bytes) {
     auto fn = encode_fn();
     PG_REQUIRE(fn != nullptr, PGMOE_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)nrec};
@@ -450,84 +470,148 @@ static int make_map(CUtensorMap *map, const void *base, int K, int rows, int nre
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    PG_REQUIRE(r == CUDA_SUCCESS, PGMOE_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    PG_REQUIRE(r == CUDA_SUCCESS, PGMOE_E_CUDA, "cuTensorMapEncodeTiled(weights) failed (%d)", (int)r);
+    return PGMOE_OK;
+}
+
+// Activation view: [rows][K] bf16, box 16 x 64 (rows past the end read as 0).
+static int make_bmap(CUtensorMap *map, const void *base, int K, int rows) {
+    auto fn = encode_fn();
+    PG_REQUIRE(fn != nullptr, PGMOE_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)std::max(rows, 1)};
+    const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    const cuuint32_t box[2] = {BK, kBRowsPerBox};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    PG_REQUIRE(r == CUDA_SUCCESS, PGMOE_E_CUDA, "cuTensorMapEncodeTiled(activations) failed (%d)", (int)r);
     return PGMOE_OK;
 }
 
 template <int BN, int STAGES>
-static int launch(const CUtensorMap &map, const Params &p, cudaStream_t s) {
+static int launch(const CUtensorMap &amap, const CUtensorMap &bmap, const Params &p, cudaStream_t s) {
     constexpr size_t smem = smem_bytes<BN, STAGES>();
+    static_assert(smem <= 227 * 1024, "shared memory budget");
     static bool attr = false;
     if (!attr) {
         PG_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         attr = true;
     }
-    grouped_gemm_kernel<BN, STAGES><<<kNumSMs, kThreads, smem, s>>>(map, p);
+    grouped_gemm_kernel<BN, STAGES><<<kNumSMs, kThreads, smem, s>>>(amap, bmap, p);
     PG_CUDA(cudaGetLastError());
     count_launch();
     return PGMOE_OK;
 }
 
-static int run(const CUtensorMap &map, Params p, int max_cols, void *ws, size_t ws_bytes, cudaStream_t s) {
+// BN: widest N tile.  Token groups wider than BN are split into N tiles
+// (each re-reads its weight tile), so BN follows the expected tokens per
+// expert: 64 covers decode batches, 256 the compute-bound stress shapes.
+static int run(const CUtensorMap &amap, const CUtensorMap &bmap, Params p, int bn, void *ws, size_t ws_bytes,
+               cudaStream_t s) {
     PG_REQUIRE(ws_bytes > kCounterInts * 4 + 4096, PGMOE_E_CONFIG, "tcgen05 workspace too small");
     p.counters = static_cast<int *>(ws);
     p.partial = reinterpret_cast<float *>(static_cast<char *>(ws) + kCounterInts * 4);
     p.partial_cap = (long long)((ws_bytes - kCounterInts * 4) / 4);
-    if (max_cols <= 64) return launch<64, 6>(map, p, s);
-    return launch<256, 4>(map, p, s);
+    if (bn <= 64) return launch<64, 8>(amap, bmap, p, s);
+    return launch<256, 4>(amap, bmap, p, s);
+}
+
+static int launch_grid(long long work) {
+    return (int)std::min<long long>(kNumSMs * 8, std::max(1LL, (work + 255) / 256));
 }
 
 }  // namespace tc
 
-bool tc_supported(int d, int f) { return d % 128 == 0 && f % 128 == 0 && d >= 128 && f >= 128; }
+bool tc_supported(int d, int f) { return d % 128 == 0 && f % 128 == 0 && d >= 128 && f >= d; }
 
-int expert_ffn_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride,
-                  int indexed_by_act, const pgmoe_routing *r, float *h, float *yw, void *ws, size_t ws_bytes,
-                  cudaStream_t s) {
-    PG_REQUIRE(tc_supported(d, f), PGMOE_E_CONFIG, "tcgen05 path needs d, f multiples of 128");
+int tc_pack_rows(const float *x, const int *perm, int n, int d, int k, uint16_t *xb, cudaStream_t s) {
+    if (n == 0) return PGMOE_OK;
+    tc::pack_rows_bf16_kernel<<<tc::launch_grid((long long)n * d / 8), 256, 0, s>>>(x, perm, n, d, k, xb);
+    PG_CUDA(cudaGetLastError());
+    count_launch();
+    return PGMOE_OK;
+}
+
+int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
+                   const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, void *ws,
+                   size_t ws_bytes, cudaStream_t s) {
+    PG_REQUIRE(tc_supported(d, f), PGMOE_E_CONFIG, "tcgen05 path needs d, f multiples of 128 and f >= d");
     PG_REQUIRE((reinterpret_cast<uintptr_t>(experts) & 15) == 0 && stride % 16 == 0, PGMOE_E_CONFIG,
                "expert records must be 16-byte aligned");
+    const int n = T * k;
     // Records addressed through the map are < E (resident) or < n_act (slot
     // cache), both <= 1024; the extent only bounds TMA address generation.
     const int rec_extent = 1024;
+    const int bn = (n >= 2048) ? 256 : 64;
+    PG_TRY(tc_pack_rows(x, r->perm, n, d, k, xb, s));
     tc::Params p{};
     p.T = T;
     p.k = k;
     p.act = r->act; p.n_act = r->n_act; p.off = r->off; p.hist = r->hist; p.perm = r->perm; p.w_perm = r->w_perm;
     p.indexed_by_act = indexed_by_act;
-    const int max_cols = T * k;
-    CUtensorMap up_map, dn_map;
-    PG_TRY(tc::make_map(&up_map, experts, d, f, rec_extent, stride));
-    PG_TRY(tc::make_map(&dn_map, static_cast<const char *>(experts) + (size_t)f * d * 2, f, d, rec_extent, stride));
+    CUtensorMap wmap, bmap;
+    PG_TRY(tc::make_wmap(&wmap, experts, d, f, rec_extent, stride));
+    PG_TRY(tc::make_bmap(&bmap, xb, d, n));
     p.mode = tc::kUp;
     p.M = f;
     p.K = d;
-    p.src = x;
-    p.dst = h;
-    PG_TRY(tc::run(up_map, p, max_cols, ws, ws_bytes, s));
+    p.out_bf16 = hb;
+    PG_TRY(tc::run(wmap, bmap, p, bn, ws, ws_bytes, s));
+    PG_TRY(tc::make_wmap(&wmap, static_cast<const char *>(experts) + (size_t)f * d * 2, f, d, rec_extent, stride));
+    PG_TRY(tc::make_bmap(&bmap, hb, f, n));
     p.mode = tc::kDown;
     p.M = d;
     p.K = f;
-    p.src = h;
-    p.dst = yw;
-    return tc::run(dn_map, p, max_cols, ws, ws_bytes, s);
+    p.out_f32 = yw;
+    p.out_bf16 = (k == 1) ? mixb : nullptr;
+    return tc::run(wmap, bmap, p, bn, ws, ws_bytes, s);
 }
 
-int dense_tc(const float *yw, int T, int d, int k, const void *dense_w, float *y, void *ws, size_t ws_bytes,
-             cudaStream_t s) {
+int dense_tc2(const float *yw, const uint16_t *mixb_ready, int T, int d, int k, const void *dense_w, float *y,
+              uint16_t *mixb_scratch, void *ws, size_t ws_bytes, cudaStream_t s) {
     PG_REQUIRE(d % 128 == 0, PGMOE_E_CONFIG, "tcgen05 dense needs d multiple of 128");
+    const uint16_t *mixb = mixb_ready;
+    if (!mixb) {
+        if (T > 0) {
+            tc::sum_slots_bf16_kernel<<<tc::launch_grid((long long)T * d / 4), 256, 0, s>>>(yw, T, d, k, mixb_scratch);
+            PG_CUDA(cudaGetLastError());
+            count_launch();
+        }
+        mixb = mixb_scratch;
+    }
     tc::Params p{};
     p.mode = tc::kDense;
     p.M = d;
     p.K = d;
     p.T = T;
     p.k = k;
-    p.src = yw;
-    p.dst = y;
-    CUtensorMap map;
-    PG_TRY(tc::make_map(&map, dense_w, d, d, 1, (size_t)d * d * 2));
-    return tc::run(map, p, T, ws, ws_bytes, s);
+    p.out_f32 = y;
+    CUtensorMap wmap, bmap;
+    PG_TRY(tc::make_wmap(&wmap, dense_w, d, d, 1, (size_t)d * d * 2));
+    PG_TRY(tc::make_bmap(&bmap, mixb, d, T));
+    return tc::run(wmap, bmap, p, T >= 2048 ? 256 : 64, ws, ws_bytes, s);
+}
+
+// Entry points with the fp32-scratch signatures: the bf16 operands live in
+// the caller's fp32 h scratch ([T*k][f] floats hold hb [T*k][f] plus
+// xb [T*k][d] bf16 since f >= d) and the mix in a temporary.
+int expert_ffn_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride,
+                  int indexed_by_act, const pgmoe_routing *r, float *h, float *yw, void *ws, size_t ws_bytes,
+                  cudaStream_t s) {
+    uint16_t *hb = reinterpret_cast<uint16_t *>(h);
+    uint16_t *xb = hb + (size_t)T * k * f;
+    return expert_ffn_tc2(x, T, d, f, k, experts, stride, indexed_by_act, r, xb, hb, yw, nullptr, ws, ws_bytes, s);
+}
+
+int dense_tc(const float *yw, int T, int d, int k, const void *dense_w, float *y, void *ws, size_t ws_bytes,
+             cudaStream_t s) {
+    uint16_t *mixb = nullptr;
+    PG_CUDA(cudaMallocAsync(&mixb, (size_t)std::max(T, 1) * d * 2, s));
+    int st = dense_tc2(yw, nullptr, T, d, k, dense_w, y, mixb, ws, ws_bytes, s);
+    cudaFreeAsync(mixb, s);
+    return st;
 }
 
 }  // namespace pgmoe

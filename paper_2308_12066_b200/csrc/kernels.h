@@ -20,5 +20,13 @@ int expert_ffn_tc(const float *x, int T, int d, int f, int k, const void *expert
 int dense_tc(const float *yw, int T, int d, int k, const void *dense_w, float *y, void *workspace,
              size_t ws_bytes, cudaStream_t s);
 bool tc_supported(int d, int f);
+// Fused-operand variants used by the runtime: bf16 activations packed once
+// (xb), bf16 hidden (hb), and for top-1 the bf16 mix written by the down
+// projection's epilogue so the dense layer reads it directly.
+int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
+                   const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, void *ws,
+                   size_t ws_bytes, cudaStream_t s);
+int dense_tc2(const float *yw, const uint16_t *mixb_ready, int T, int d, int k, const void *dense_w, float *y,
+              uint16_t *mixb_scratch, void *ws, size_t ws_bytes, cudaStream_t s);
 
 }  // namespace pgmoe

@@ -62,6 +62,7 @@ using namespace pgmoe;
 struct pgmoe_model {
     pgmoe_config cfg{};
     int wdtype = PGMOE_BF16, placement = PGMOE_RESIDENT, max_tokens = 0, kernel = PGMOE_KERNEL_AUTO;
+    int e_begin = 0, e_local = 0;  // expert range held by this model (expert parallelism)
     size_t sw = 2, gate_bytes = 0, dense_bytes = 0, w1_bytes = 0, rec_bytes = 0;
     std::vector<BlockW> blocks;
     unsigned char *dev_pool = nullptr;   // gates + dense (+ experts when resident)
@@ -70,6 +71,7 @@ struct pgmoe_model {
     // work buffers
     float *act_buf[2] = {nullptr, nullptr};
     float *h = nullptr, *yw = nullptr;
+    uint16_t *xb = nullptr, *hb = nullptr, *mixb = nullptr;  // bf16 tcgen05 operands
     std::vector<RoutingBuf> routing;  // ring of L+1 decisions
     void *route_ws = nullptr;
     void *tc_ws = nullptr;
@@ -151,10 +153,11 @@ static void *mat_ptr(pgmoe_model *m, const std::string &name, int b, int e, size
     if (name == "pre_gate") { *bytes = m->gate_bytes; return bw.pre_gate; }
     if (name == "non_moe") { *bytes = m->dense_bytes; return bw.dense; }
     if (name == "w1" || name == "w2") {
-        if (e < 0 || e >= c.num_experts) return nullptr;
+        const int le = e - m->e_begin;
+        if (le < 0 || le >= m->e_local) return nullptr;
         *on_host = (m->placement == PGMOE_OFFLOADED);
         *bytes = m->w1_bytes;
-        return bw.experts + (size_t)e * m->rec_bytes + (name == "w2" ? m->w1_bytes : 0);
+        return bw.experts + (size_t)le * m->rec_bytes + (name == "w2" ? m->w1_bytes : 0);
     }
     return nullptr;
 }
@@ -167,8 +170,8 @@ int run_ffn(pgmoe_model *m, const float *x, int T, const void *experts, int inde
     if (m->kernel == PGMOE_KERNEL_TCGEN05)
         PG_REQUIRE(tc, PGMOE_E_CONFIG, "tcgen05 kernels need bf16 weights and d, f multiples of 128");
     if (tc)
-        return expert_ffn_tc(x, T, c.d_model, c.d_ff, c.top_k, experts, m->rec_bytes, indexed, r, m->h,
-                             m->yw, m->tc_ws, m->tc_ws_bytes, s);
+        return expert_ffn_tc2(x, T, c.d_model, c.d_ff, c.top_k, experts, m->rec_bytes, indexed, r, m->xb, m->hb,
+                              m->yw, c.top_k == 1 ? m->mixb : nullptr, m->tc_ws, m->tc_ws_bytes, s);
     return expert_ffn_simt(x, T, c.d_model, c.d_ff, c.top_k, experts, m->rec_bytes, m->wdtype, indexed,
                            r, m->h, m->yw, s);
 }
@@ -177,7 +180,9 @@ int run_dense(pgmoe_model *m, int T, const void *dense, float *y, cudaStream_t s
     const auto &c = m->cfg;
     const bool tc = m->wdtype == PGMOE_BF16 && m->kernel != PGMOE_KERNEL_SIMT &&
                     tc_supported(c.d_model, c.d_ff);
-    if (tc) return dense_tc(m->yw, T, c.d_model, c.top_k, dense, y, m->tc_ws, m->tc_ws_bytes, s);
+    if (tc)
+        return dense_tc2(m->yw, c.top_k == 1 ? m->mixb : nullptr, T, c.d_model, c.top_k, dense, y, m->mixb,
+                         m->tc_ws, m->tc_ws_bytes, s);
     return dense_simt(m->yw, T, c.d_model, c.top_k, dense, m->wdtype, y, s);
 }
 
@@ -249,6 +254,9 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
     const auto &c = m->cfg;
     PG_REQUIRE(T >= 0 && T <= m->max_tokens, PGMOE_E_SHAPE, "T=%d exceeds max_tokens=%d", T,
                m->max_tokens);
+    PG_REQUIRE(m->e_local == c.num_experts, PGMOE_E_CONFIG,
+               "model holds experts [%d, %d) only: expert-parallel decoding runs through ep.py", m->e_begin,
+               m->e_begin + m->e_local);
     if (T == 0) return PGMOE_OK;
     const int L = c.activation_level, R = L + 1, nb = c.num_blocks;
     const bool off = m->placement == PGMOE_OFFLOADED;
@@ -331,7 +339,9 @@ extern "C" int pgmoe_dense_forward(const float *yw, int32_t T, int32_t d, int32_
                                    int32_t wdtype, float *y, int32_t kernel, pgmoe_stream_t stream) {
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (T == 0) return PGMOE_OK;
-    const bool tc = wdtype == PGMOE_BF16 && kernel != PGMOE_KERNEL_SIMT && tc_supported(d, 128);
+    const bool tc = wdtype == PGMOE_BF16 && kernel != PGMOE_KERNEL_SIMT && d % 128 == 0;
+    if (kernel == PGMOE_KERNEL_TCGEN05)
+        PG_REQUIRE(tc, PGMOE_E_CONFIG, "tcgen05 dense needs bf16 weights and d multiple of 128");
     if (tc) {
         static void *ws = nullptr;
         static size_t ws_bytes = 0;
@@ -348,6 +358,15 @@ extern "C" int pgmoe_dense_forward(const float *yw, int32_t T, int32_t d, int32_
 extern "C" int pgmoe_model_create(const pgmoe_config *cfg, int32_t wdtype, int32_t placement,
                                   int32_t max_tokens, pgmoe_model **out) {
     PG_TRY(validate_config(cfg));
+    return pgmoe_model_create_ex(cfg, wdtype, placement, max_tokens, 0, cfg->num_experts, out);
+}
+
+extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, int32_t placement,
+                                     int32_t max_tokens, int32_t expert_begin, int32_t expert_end,
+                                     pgmoe_model **out) {
+    PG_TRY(validate_config(cfg));
+    PG_REQUIRE(0 <= expert_begin && expert_begin < expert_end && expert_end <= cfg->num_experts, PGMOE_E_CONFIG,
+               "expert range [%d, %d) outside [0, %d)", expert_begin, expert_end, cfg->num_experts);
     PG_REQUIRE(out != nullptr, PGMOE_E_CONFIG, "null output handle");
     PG_REQUIRE(wdtype == PGMOE_F32 || wdtype == PGMOE_BF16, PGMOE_E_CONFIG, "unknown weight dtype %d", wdtype);
     PG_REQUIRE(placement == PGMOE_RESIDENT || placement == PGMOE_OFFLOADED, PGMOE_E_CONFIG,
@@ -358,8 +377,10 @@ extern "C" int pgmoe_model_create(const pgmoe_config *cfg, int32_t wdtype, int32
     m->wdtype = wdtype;
     m->placement = placement;
     m->max_tokens = max_tokens;
+    m->e_begin = expert_begin;
+    m->e_local = expert_end - expert_begin;
     const auto &c = m->cfg;
-    const size_t d = c.d_model, f = c.d_ff, E = c.num_experts, nb = c.num_blocks, k = c.top_k;
+    const size_t d = c.d_model, f = c.d_ff, E = m->e_local, nb = c.num_blocks, k = c.top_k;
     m->sw = dtype_bytes(wdtype);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     m->gate_bytes = al(d * E * m->sw);
@@ -421,7 +442,7 @@ extern "C" int pgmoe_model_create(const pgmoe_config *cfg, int32_t wdtype, int32
     m->routing.resize(R);
     m->routed.resize(R);
     for (int i = 0; i < R; ++i) {
-        if ((st = alloc_routing(m->routing[i], max_tokens, (int)E, (int)k)) != PGMOE_OK) return fail(st);
+        if ((st = alloc_routing(m->routing[i], max_tokens, c.num_experts, (int)k)) != PGMOE_OK) return fail(st);
         cudaEventCreateWithFlags(&m->routed[i], cudaEventDisableTiming);
     }
     if (cudaMalloc(&m->route_ws, 256) != cudaSuccess || cudaMemset(m->route_ws, 0, 256) != cudaSuccess)
@@ -429,7 +450,9 @@ extern "C" int pgmoe_model_create(const pgmoe_config *cfg, int32_t wdtype, int32
     const size_t T = max_tokens;
     if (cudaMalloc(&m->act_buf[0], T * d * 4) != cudaSuccess ||
         cudaMalloc(&m->act_buf[1], T * d * 4) != cudaSuccess ||
-        cudaMalloc(&m->h, T * k * f * 4) != cudaSuccess || cudaMalloc(&m->yw, T * k * d * 4) != cudaSuccess) {
+        cudaMalloc(&m->h, T * k * f * 4) != cudaSuccess || cudaMalloc(&m->yw, T * k * d * 4) != cudaSuccess ||
+        cudaMalloc(&m->xb, T * k * d * 2) != cudaSuccess || cudaMalloc(&m->hb, T * k * f * 2) != cudaSuccess ||
+        cudaMalloc(&m->mixb, T * d * 2) != cudaSuccess) {
         set_error("OOM: activation buffers for max_tokens=%d", max_tokens);
         return fail(PGMOE_E_OOM);
     }
@@ -468,6 +491,9 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     cudaFree(m->act_buf[1]);
     cudaFree(m->h);
     cudaFree(m->yw);
+    cudaFree(m->xb);
+    cudaFree(m->hb);
+    cudaFree(m->mixb);
     delete m;
     return PGMOE_OK;
 }
@@ -480,7 +506,7 @@ extern "C" int pgmoe_model_set_kernel(pgmoe_model *m, int32_t kernel) {
 
 extern "C" int pgmoe_model_init_weights(pgmoe_model *m) {
     const auto &c = m->cfg;
-    const int nb = c.num_blocks, E = c.num_experts;
+    const int nb = c.num_blocks, E = m->e_local, e0 = m->e_begin;
     const int64_t d = c.d_model, f = c.d_ff;
     cudaStream_t s = nullptr;
     PG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -516,8 +542,8 @@ extern "C" int pgmoe_model_init_weights(pgmoe_model *m) {
         for (int b = 0; b < nb; ++b)
             for (int e = 0; e < E; ++e) {
                 unsigned char *rec = m->blocks[b].experts + (size_t)e * m->rec_bytes;
-                ej.push_back({rec, matrix_seed(c.seed, kTagW1, b, e), f * d});
-                ej.push_back({rec + m->w1_bytes, matrix_seed(c.seed, kTagW2, b, e), d * f});
+                ej.push_back({rec, matrix_seed(c.seed, kTagW1, b, e0 + e), f * d});
+                ej.push_back({rec + m->w1_bytes, matrix_seed(c.seed, kTagW2, b, e0 + e), d * f});
             }
         st = run(ej);
     } else if (st == PGMOE_OK) {
@@ -527,8 +553,8 @@ extern "C" int pgmoe_model_init_weights(pgmoe_model *m) {
             for (int b = b0; b < b1; ++b)
                 for (int e = 0; e < E; ++e) {
                     unsigned char *rec = stage + ((size_t)(b - b0) * E + e) * m->rec_bytes;
-                    ej.push_back({rec, matrix_seed(c.seed, kTagW1, b, e), f * d});
-                    ej.push_back({rec + m->w1_bytes, matrix_seed(c.seed, kTagW2, b, e), d * f});
+                    ej.push_back({rec, matrix_seed(c.seed, kTagW1, b, e0 + e), f * d});
+                    ej.push_back({rec + m->w1_bytes, matrix_seed(c.seed, kTagW2, b, e0 + e), d * f});
                 }
             st = run(ej);
             if (st == PGMOE_OK && cudaMemcpy(m->blocks[b0].experts, stage, (size_t)(b1 - b0) * E * m->rec_bytes,
@@ -668,6 +694,16 @@ extern "C" int pgmoe_moe_block_forward(pgmoe_model *m, int32_t block, const floa
     }
     PG_TRY(run_ffn(m, x, T, experts, indexed, r_in, s));
     return run_dense(m, T, bw.dense, y, s);
+}
+
+extern "C" int pgmoe_model_expert_records(pgmoe_model *m, int32_t block, const void **base, size_t *stride,
+                                          int32_t *expert_begin, int32_t *n_local) {
+    PG_REQUIRE(m && block >= 0 && block < m->cfg.num_blocks, PGMOE_E_CONFIG, "bad block %d", block);
+    *base = m->blocks[block].experts;
+    *stride = m->rec_bytes;
+    *expert_begin = m->e_begin;
+    *n_local = m->e_local;
+    return PGMOE_OK;
 }
 
 extern "C" int pgmoe_model_stats(pgmoe_model *m, pgmoe_stats *out) {

@@ -1,0 +1,167 @@
+"""Expert parallelism (BASELINE configs[4]).
+
+Experts of every block are partitioned contiguously over P ranks (one
+process per GPU, ``torch.distributed``); gates and dense layers are
+replicated; every rank owns its own T sequences.  Per block there is
+exactly one exchange step each way:
+
+  K1 route (local tokens) -> counts [P][E/P] all-to-all -> dispatch rows
+  (all_to_all_single, NCCL over NVLink) -> receiver routing + K2 on the
+  local experts -> combine rows back -> weighted un-permute -> K3 dense.
+
+Because K1's permutation is grouped by expert and experts are contiguous
+per rank, the packed send buffer is already grouped by destination; the
+receiver regroups its rows by local expert with the same stable order a
+single GPU would use, so EP outputs equal the single-GPU outputs.
+
+The exchange plan (``dispatch_plan``/``local_routing_plan``) and the
+collectives (``Exchange``) are backend-neutral and are exercised on CPU
+with gloo in tests/test_ep_gloo.py; ``EPDecoder`` drives them with the
+sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .core import DeviceRouting, ModelConfig, _ptr, _stream
+from .errors import ConfigError, ShapeError
+
+
+def expert_range(E: int, P: int, rank: int) -> tuple[int, int]:
+    if E % P:
+        raise ConfigError(f"num_experts={E} is not divisible by world size {P}")
+    el = E // P
+    return rank * el, (rank + 1) * el
+
+
+def dispatch_plan(hist: np.ndarray, P: int) -> tuple[np.ndarray, np.ndarray]:
+    """hist [E] (tokens per global expert, this rank) -> (per-expert counts
+    [P][E/P] sent to each rank, rows sent to each rank [P])."""
+    h = np.asarray(hist).reshape(P, -1)
+    return h, h.sum(axis=1)
+
+
+def local_routing_plan(recv_cnt: np.ndarray):
+    """Host restatement of pgmoe_ep_local_routing: recv_cnt [P][El] ->
+    (hist [El], off [El+1], perm [n]) over the received rows."""
+    P, El = recv_cnt.shape
+    src_base = np.concatenate([[0], np.cumsum(recv_cnt.sum(axis=1))[:-1]])
+    src_off = np.concatenate([np.zeros((P, 1), np.int64), np.cumsum(recv_cnt, axis=1)[:, :-1]], axis=1)
+    hist = recv_cnt.sum(axis=0)
+    off = np.concatenate([[0], np.cumsum(hist)])
+    perm = []
+    for e in range(El):
+        for p in range(P):
+            b = src_base[p] + src_off[p, e]
+            perm.extend(range(b, b + recv_cnt[p, e]))
+    return hist.astype(np.int32), off.astype(np.int32), np.array(perm, dtype=np.int32)
+
+
+class Exchange:
+    """The two all-to-all steps of a block, over a torch.distributed group
+    (NCCL for device tensors; gloo works for CPU tensors)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def counts(self, send_cnt: torch.Tensor) -> torch.Tensor:
+        """send_cnt [P][El] int32 -> recv_cnt [P][El] (row p = from rank p)."""
+        recv = torch.empty_like(send_cnt)
+        dist.all_to_all_single(recv, send_cnt.contiguous(), group=self.group)
+        return recv
+
+    def rows(self, send: torch.Tensor, send_splits: list, recv_splits: list) -> torch.Tensor:
+        out = send.new_empty((int(sum(recv_splits)),) + tuple(send.shape[1:]))
+        dist.all_to_all_single(out, send, output_split_sizes=[int(v) for v in recv_splits],
+                               input_split_sizes=[int(v) for v in send_splits], group=self.group)
+        return out
+
+
+class EPDecoder:
+    """decoder_iteration (core.py:342-383) with experts sharded over ranks."""
+
+    def __init__(self, config: ModelConfig, dtype: str = "bf16", max_tokens: int = 256, group=None,
+                 kernel: str = "auto"):
+        from .core import DeviceModel
+        self.config = config
+        self.ex = Exchange(group)
+        self.P, self.rank = self.ex.P, self.ex.rank
+        self.e0, self.e1 = expert_range(config.num_experts, self.P, self.rank)
+        self.El = self.e1 - self.e0
+        self.model = DeviceModel(config, dtype=dtype, placement="resident", max_tokens=max_tokens,
+                                 kernel=kernel, init="rng", expert_range=(self.e0, self.e1))
+        self.kernel = kernel
+        self.max_tokens = max_tokens
+        k = config.top_k
+        self.max_recv = self.P * max_tokens * k
+        self.lr = DeviceRouting(self.max_recv, self.El, 1)
+        self.routing = DeviceRouting(max_tokens, config.num_experts, k)
+        self._L = _lib.load()
+        self.timing = {"exchange_s": 0.0, "blocks": 0}
+
+    def block(self, b: int, x: torch.Tensor, r_in: DeviceRouting, stream=None):
+        c = self.config
+        L = self._L
+        T, d, f, k = x.shape[0], c.d_model, c.d_ff, c.top_k
+        n = T * k
+        hist2 = r_in.hist.view(self.P, self.El)
+        recv_cnt = self.ex.counts(hist2)                      # [P][El] exchange (one block early in principle)
+        splits = torch.stack([hist2.sum(1), recv_cnt.sum(1)]).cpu()
+        send_splits, recv_splits = splits[0].tolist(), splits[1].tolist()
+        x_send = torch.empty((max(n, 1), d), dtype=torch.float32, device=x.device)
+        _lib.check(L.pgmoe_gather_rows(_ptr(x), _ptr(r_in.perm), n, d, k, _ptr(x_send), _stream(stream)))
+        x_recv = self.ex.rows(x_send[:n], send_splits, recv_splits)
+        n_recv = x_recv.shape[0]
+        if n_recv > self.max_recv:
+            raise ShapeError("received more rows than the EP buffers hold")
+        _lib.check(L.pgmoe_ep_local_routing(_ptr(recv_cnt), self.P, self.El, ctypes.byref(self.lr.c),
+                                            _stream(stream)))
+        base, stride = ctypes.c_void_p(), ctypes.c_size_t()
+        eb, nl = ctypes.c_int32(), ctypes.c_int32()
+        _lib.check(L.pgmoe_model_expert_records(self.model._h, b, ctypes.byref(base), ctypes.byref(stride),
+                                                ctypes.byref(eb), ctypes.byref(nl)))
+        h = torch.empty((max(n_recv, 1), f), dtype=torch.float32, device=x.device)
+        y_recv = torch.empty((max(n_recv, 1), d), dtype=torch.float32, device=x.device)
+        if n_recv:
+            from .core import _KERNEL
+            _lib.check(L.pgmoe_expert_forward(_ptr(x_recv), n_recv, d, f, 1, base, stride.value,
+                                              self.model.wdt, 0, ctypes.byref(self.lr.c), _ptr(h), _ptr(y_recv),
+                                              _KERNEL[self.kernel], _stream(stream)))
+        back = self.ex.rows(y_recv[:n_recv], recv_splits, send_splits)
+        yw = torch.empty((max(n, 1), d), dtype=torch.float32, device=x.device)
+        _lib.check(L.pgmoe_unpermute_combine(_ptr(back), _ptr(r_in.perm), _ptr(r_in.w_perm), n, d, _ptr(yw),
+                                             _stream(stream)))
+        y = torch.empty_like(x)
+        from .core import _KERNEL
+        _lib.check(L.pgmoe_dense_forward(_ptr(yw), T, d, k, _ptr(self.model.matrix("non_moe", b)),
+                                         self.model.wdt, _ptr(y), _KERNEL[self.kernel], _stream(stream)))
+        return y
+
+    def decoder_iteration(self, x: torch.Tensor, trace: bool = False):
+        """Local tokens x [T][d] (cuda fp32) -> (y, consumed ids per block)."""
+        from .core import route
+        c = self.config
+        pending: dict = {}
+        ids = []
+        for b in range(c.num_blocks):
+            if c.has_conv_gate(b):
+                r_in = route(x, self.model.matrix("gate", b), c.top_k)
+            else:
+                r_in = pending.pop(b)
+            if c.has_pre_gate(b):
+                pending[b + c.activation_level] = route(x, self.model.matrix("pre_gate", b), c.top_k)
+            if trace:
+                ids.append(r_in.ids.clone())
+            x = self.block(b, x, r_in)
+        return x, (torch.stack(ids) if trace else None)
+
+    def close(self):
+        self.model.close()

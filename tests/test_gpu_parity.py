@@ -391,3 +391,34 @@ def test_model_tcgen05_equals_teacher_forced_oracle_large_dims(placement):
     om = og.OracleModel(dims, "bf16")
     _teacher_forced_chain(m, om, tokens(1024, 64), TOL["bf16"], check_blocks={0, 2})
     m.close()
+
+
+# ------------------------------------------------------ expert parallel ----
+
+def test_ep_decoder_single_rank_nccl_equals_single_gpu():
+    """EP plumbing on one rank (NCCL world of 1): dispatch/combine over NCCL,
+    receiver routing and un-permute must reproduce the single-GPU decoder
+    bit-for-bit."""
+    import socket
+    import torch.distributed as dist
+    p = P()
+    from paper_2308_12066_b200.ep import EPDecoder
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        cfg = p.ModelConfig(d_model=256, d_ff=512, num_blocks=4, num_experts=16, top_k=2, activation_level=1)
+        x = p.token_inputs(cfg, 24)
+        ep = EPDecoder(cfg, dtype="bf16", max_tokens=24)
+        y_ep, ids_ep = ep.decoder_iteration(x, trace=True)
+        ref = p.DeviceModel(cfg, dtype="bf16", max_tokens=24)
+        y, ids, _ = ref.decoder_iteration(x, trace=True)
+        torch.cuda.synchronize()
+        assert torch.equal(ids_ep, ids)
+        assert torch.equal(y_ep, y)
+        ep.close()
+        ref.close()
+    finally:
+        dist.destroy_process_group()
