@@ -211,8 +211,7 @@ def run_ours(args, rank: int, world: int):
         model.decoder_iteration(x)
     torch.cuda.synchronize()
 
-    # ---- timed region: device-resident inputs --------------------------
-    model.set_timeline(True)
+    # ---- timed region: device-resident inputs (resident: CUDA-graph replay) --
     model.reset_stats()
     launches0 = L.pgmoe_launch_count()
     clocks = ClockSampler(dev)
@@ -235,8 +234,15 @@ def run_ours(args, rank: int, world: int):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     st = model.stats()
+    # ---- profile pass: per-kernel CUDA events on the compute / copy streams
+    prof_steps = max(1, min(args.steps, 3))
+    model.set_timeline(True)
+    for _ in range(prof_steps):
+        model.decoder_iteration(x)
+    torch.cuda.synchronize()
     tl = model.timeline()
     model.set_timeline(False)
+    gpu_launches_per_step = launches / args.steps
 
     # ---- per-kernel roofline from the CUDA events on the compute stream ---
     hbm_peak, tc_peak, peak_kind = peaks()
@@ -252,21 +258,26 @@ def run_ours(args, rank: int, world: int):
     else:  # resident: recompute from one traced iteration
         _, ids, _ = model.decoder_iteration(x, trace=True)
         torch.cuda.synchronize()
-        nact_total = sum(len(torch.unique(ids[b])) for b in range(nb)) * args.steps
+        nact_total = sum(len(torch.unique(ids[b])) for b in range(nb)) * prof_steps
     act_bytes_per_token = 2 * d * 4 + 2 * f * 4   # x read, yw write, h write+read (fp32)
-    ffn_bytes = nact_total * rec + args.steps * nb * T * act_bytes_per_token
+    ffn_bytes = nact_total * rec + prof_steps * nb * T * act_bytes_per_token
     ffn_gbs = ffn_bytes / ffn_s / 1e9 if ffn_s > 0 else None
     h2d_s = sum(e["end_s"] - e["start_s"] for e in fetch)
     pcie_gbs = measure_pcie_gbs(torch)
-    h2d_gbs = (st["h2d_bytes"] / h2d_s / 1e9) if h2d_s > 0 else None
+    h2d_gbs = (nact_total * rec / h2d_s / 1e9) if (h2d_s > 0 and fetch) else None
     # per-block roofline time: max(HBM, tensor, PCIe)
-    nact_avg = nact_total / (args.steps * nb)
+    nact_avg = nact_total / (prof_steps * nb)
     n_gates_avg = cfg.gate_count / nb
     hbm_b = n_gates_avg * d * E * sw + nact_avg * rec + d * d * sw + T * d * 4 * 5 + T * 8 + (2 * E + 1) * 4
     flops = n_gates_avg * 2 * T * d * E + 4 * T * d * f + 2 * T * d * d
     pcie_b = nact_avg * rec if args.placement == "offloaded" else 0
     t_roof = max(hbm_b / (hbm_peak * 1e9), flops / (tc_peak * 1e12), pcie_b / (pcie_gbs * 1e9))
     block_ms = ms / nb
+    phases = {}
+    for e in tl:
+        key = e["lane"] + ":" + e["label"].split("[")[0]
+        phases[key] = phases.get(key, 0.0) + (e["end_s"] - e["start_s"])
+    phases = {k: round(v * 1e3 / (prof_steps * nb), 4) for k, v in phases.items()}
 
     # ---- end-to-end through the C ABI with host buffers -----------------
     y_host = torch.empty_like(x_host).pin_memory()
@@ -300,6 +311,7 @@ def run_ours(args, rank: int, world: int):
                    "top_k": 1, "activation_level": 1, "parallelism": f"sequences x{world} (replicas)",
                    "l2": "per-step expert bytes >> 126 MB L2 (no reuse across steps)", "kernel": args.kernel},
         "per_block_latency_ms": round(block_ms, 4),
+        "per_block_phase_ms": phases,
         "block_roofline": {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / block_ms, 4),
                            "bound": "pcie" if pcie_b and pcie_b / (pcie_gbs * 1e9) >= hbm_b / (hbm_peak * 1e9) else "hbm",
                            "n_act_avg": round(nact_avg, 2)},
@@ -312,15 +324,18 @@ def run_ours(args, rank: int, world: int):
         "migration": {"h2d_gbs": round(h2d_gbs, 2) if h2d_gbs else None, "pcie_measured_gbs": round(pcie_gbs, 2),
                       "frac": round(h2d_gbs / pcie_gbs, 4) if h2d_gbs else None,
                       "h2d_bytes_per_step": st["h2d_bytes"] // max(1, args.steps),
-                      "copy_busy_frac": round(h2d_s / (ms * 1e-3 * args.steps), 4) if h2d_s else None,
+                      "copy_busy_frac": round(h2d_s / (ms * 1e-3 * prof_steps), 4) if h2d_s else None,
                       "peak_hbm_eq1_bytes": st["eq1_peak_bytes"], "peak_hbm_ledger_bytes": st["ledger_peak_bytes"],
                       "pinned_hbm_bytes": st["pinned_hbm_bytes"]},
         "routing": {"serial_fallbacks": st["route_fallbacks"], "flips": st["route_flips"]},
         "e2e": {"value": round(T * world / e2e_s, 3), "unit": "tokens/s",
                 "h2d_bytes_per_step": T * d * 4, "d2h_bytes_per_step": T * d * 4},
         "gpu_launches": int(launches),
+        "gpu_launches_per_step": gpu_launches_per_step,
         "clocks": clk,
         "setup_s": round(setup_s, 2),
+        "timing_note": "value/ms_per_step: CUDA events around the K timed steps (resident: CUDA-graph replay); "
+                       "roofline/phases: a following pass with per-kernel CUDA events on the same streams",
     }
     # ---- CPU baseline (rank 0, N=1 only) ---------------------------------
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

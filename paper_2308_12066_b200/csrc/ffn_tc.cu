@@ -143,7 +143,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 __device__ __forceinline__ uint16_t bf16_bits(float a) { return __bfloat16_as_ushort(__float2bfloat16_rn(a)); }
 
 struct Sched {
-    int groups, m_tiles, kb_total, kbs, S;
+    int groups, m_tiles, kb_total, kbs, S, max_npad;
     long long tiles, units;
     const int *prefix;  // [groups + 1] tile prefix (smem)
 };
@@ -228,13 +228,14 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
     sc.kb_total = p.K / BK;
     sc.prefix = prefix;
     if (warp == 0) {
-        int run = 0;
+        int run = 0, mx = 16;
         for (int g0 = 0; g0 < sc.groups; g0 += 32) {
             const int g = g0 + lane;
             int nt = 0;
             if (g < sc.groups) {
                 const int ng = (p.mode == kDense) ? p.T : p.hist[p.act[g]];
                 nt = ((ng + BN - 1) / BN) * sc.m_tiles;
+                mx = max(mx, (min(ng, BN) + 15) & ~15);
             }
             int incl = nt;
 #pragma unroll
@@ -245,7 +246,12 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
             if (g < sc.groups) prefix[g] = run + incl - nt;
             run += __shfl_sync(0xffffffffu, incl, 31);
         }
-        if (lane == 0) prefix[sc.groups] = run;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) {
+            prefix[sc.groups] = run;
+            s_flag[1] = mx;
+        }
     }
     if (warp == 1) {  // TMEM: two accumulator stages of BN fp32 columns
         constexpr uint32_t cols = (2 * BN < 32) ? 32 : 2 * BN;
@@ -273,6 +279,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     sc.tiles = prefix[sc.groups];
+    sc.max_npad = s_flag[1];
     {
         // split K only when there are too few tiles to cover the SMs
         int S = 1;
@@ -281,6 +288,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
             const long long q = (want + sc.tiles - 1) / sc.tiles;
             S = (int)(q < sc.kb_total ? q : sc.kb_total);
         }
+        // the fix-up reads S x n partial columns per row: keep it small next
+        // to the tile's own K loop (wide N tiles already carry enough work)
+        S = min(S, max(1, 8 * 16 / min(BN, sc.max_npad)));
         while (S > 1 && ((long long)sc.tiles * S * BN * BM > p.partial_cap || sc.tiles > kCounterInts)) --S;
         sc.kbs = (sc.kb_total + S - 1) / S;
         sc.S = (sc.kb_total + sc.kbs - 1) / sc.kbs;
@@ -292,20 +302,49 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
         if (lane == 0) {
             uint64_t policy;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+            // Weight tiles do not depend on the previous kernel: the first
+            // STAGES of them are issued before griddepcontrol.wait (PDL), the
+            // activation boxes of those stages right after it.
             int stage = 0;
             uint32_t phase = 0;
+            int pre_n = 0, pre_kb[STAGES], pre_row[STAGES], pre_np[STAGES];
+            bool waited = false;
             for (long long u = blockIdx.x; u < sc.units; u += gridDim.x) {
                 const Unit x = decode_unit<BN>(p, sc, u);
                 const int brow = x.row0 + x.n0;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                    if (!waited && pre_n == STAGES) {
+                        pdl_wait();
+                        pdl_trigger();
+                        waited = true;
+                        for (int q = 0; q < pre_n; ++q)
+                            for (int j = 0; j < pre_np[q]; j += kBRowsPerBox)
+                                tma_load_2d(sB + q * kBBytes + j * 128, &bmap, &full[q], pre_kb[q] * BK, pre_row[q] + j);
+                    }
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], kABytes + x.n_pad * 128);
                     tma_load_3d(sA + stage * kABytes, &amap, &full[stage], kb * BK, x.m_tile * BM, x.rec, policy);
-                    for (int j = 0; j < x.n_pad; j += kBRowsPerBox)
-                        tma_load_2d(sB + stage * kBBytes + j * 128, &bmap, &full[stage], kb * BK, brow + j);
+                    if (waited) {
+                        for (int j = 0; j < x.n_pad; j += kBRowsPerBox)
+                            tma_load_2d(sB + stage * kBBytes + j * 128, &bmap, &full[stage], kb * BK, brow + j);
+                    } else {
+                        pre_kb[pre_n] = kb;
+                        pre_row[pre_n] = brow;
+                        pre_np[pre_n] = x.n_pad;
+                        ++pre_n;
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
+            if (!waited) {
+                pdl_wait();
+                pdl_trigger();
+                for (int q = 0; q < pre_n; ++q)
+                    for (int j = 0; j < pre_np[q]; j += kBRowsPerBox)
+                        tma_load_2d(sB + q * kBBytes + j * 128, &bmap, &full[q], pre_kb[q] * BK, pre_row[q] + j);
+            }
+        } else {
+            pdl_wait();  // the rest of warp 0 has nothing to do, but keep semantics uniform
         }
     } else if (warp == 1) {
         // ================= MMA issuer (single thread) ======================
@@ -378,6 +417,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
                     const float *base = p.partial + (size_t)x.tile * sc.S * (BN * BM) + et;
                     for (int n0 = 0; n0 < x.n_valid; n0 += 4) {
                         float a4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
                         for (int s = 0; s < sc.S; ++s) {  // split order: deterministic
                             float v4[4];
 #pragma unroll
@@ -408,6 +448,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
 // xb[r] = bf16(x[perm[r] / k])  (activation rows in routing order)
 __global__ void pack_rows_bf16_kernel(const float *__restrict__ x, const int *__restrict__ perm, int n, int d, int k,
                                       uint16_t *__restrict__ xb) {
+    pdl_wait();
+    pdl_trigger();
     const int vec = d / 8;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * vec;
          i += (long long)gridDim.x * blockDim.x) {
@@ -426,6 +468,8 @@ __global__ void pack_rows_bf16_kernel(const float *__restrict__ x, const int *__
 
 // mixb[t] = bf16(sum_s yw[t*k+s]) in slot (routing) order, linalg.py:45-51
 __global__ void sum_slots_bf16_kernel(const float *__restrict__ yw, int T, int d, int k, uint16_t *__restrict__ mixb) {
+    pdl_wait();
+    pdl_trigger();
     const int vec = d / 4;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)T * vec;
          i += (long long)gridDim.x * blockDim.x) {
@@ -499,8 +543,7 @@ static int launch(const CUtensorMap &amap, const CUtensorMap &bmap, const Params
                                      (int)smem));
         attr = true;
     }
-    grouped_gemm_kernel<BN, STAGES><<<kNumSMs, kThreads, smem, s>>>(amap, bmap, p);
-    PG_CUDA(cudaGetLastError());
+    PG_CUDA(launch_pdl(grouped_gemm_kernel<BN, STAGES>, dim3(kNumSMs), dim3(kThreads), smem, s, amap, bmap, p));
     count_launch();
     return PGMOE_OK;
 }
@@ -528,8 +571,8 @@ bool tc_supported(int d, int f) { return d % 128 == 0 && f % 128 == 0 && d >= 12
 
 int tc_pack_rows(const float *x, const int *perm, int n, int d, int k, uint16_t *xb, cudaStream_t s) {
     if (n == 0) return PGMOE_OK;
-    tc::pack_rows_bf16_kernel<<<tc::launch_grid((long long)n * d / 8), 256, 0, s>>>(x, perm, n, d, k, xb);
-    PG_CUDA(cudaGetLastError());
+    PG_CUDA(launch_pdl(tc::pack_rows_bf16_kernel, dim3(tc::launch_grid((long long)n * d / 8)), dim3(256), 0, s, x,
+                       perm, n, d, k, xb));
     count_launch();
     return PGMOE_OK;
 }
@@ -575,8 +618,8 @@ int dense_tc2(const float *yw, const uint16_t *mixb_ready, int T, int d, int k, 
     const uint16_t *mixb = mixb_ready;
     if (!mixb) {
         if (T > 0) {
-            tc::sum_slots_bf16_kernel<<<tc::launch_grid((long long)T * d / 4), 256, 0, s>>>(yw, T, d, k, mixb_scratch);
-            PG_CUDA(cudaGetLastError());
+            PG_CUDA(launch_pdl(tc::sum_slots_bf16_kernel, dim3(tc::launch_grid((long long)T * d / 4)), dim3(256), 0, s,
+                               yw, T, d, k, mixb_scratch));
             count_launch();
         }
         mixb = mixb_scratch;

@@ -91,6 +91,19 @@ struct pgmoe_model {
     std::vector<TimelineEv> tl;
     cudaEvent_t t0 = nullptr;
     bool t0_recorded = false;
+    // resident decoder iterations are replayed from a CUDA graph per buffer set
+    bool use_graph = true;
+    cudaStream_t cap = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    const float *g_x = nullptr;
+    float *g_y = nullptr;
+    int g_T = -1;
+    int32_t *g_ids = nullptr;
+    float *g_w = nullptr;
+    // host-buffer entry point
+    cudaStream_t io_stream = nullptr;
+    float *io_x = nullptr, *io_y = nullptr, *io_w = nullptr;
+    int32_t *io_ids = nullptr;
     std::mutex mu;
 };
 
@@ -462,6 +475,7 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
     cudaEventCreate(&m->t0);
     m->stats.pinned_hbm_bytes = (int64_t)pinned;
     m->stats.slot_capacity_bytes = (int64_t)m->slot_capacity;
+    if (const char *e = getenv("PGMOE_NO_GRAPH")) m->use_graph = (e[0] == '0');
     *out = m;
     return PGMOE_OK;
 }
@@ -481,6 +495,13 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     for (auto e : m->ffn_b) cudaEventDestroy(e);
     for (auto &e : m->tl) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (m->t0) cudaEventDestroy(m->t0);
+    if (m->gexec) cudaGraphExecDestroy(m->gexec);
+    if (m->io_stream) cudaStreamDestroy(m->io_stream);
+    cudaFree(m->io_x);
+    cudaFree(m->io_y);
+    cudaFree(m->io_ids);
+    cudaFree(m->io_w);
+    if (m->cap) cudaStreamDestroy(m->cap);
     if (m->copy) cudaStreamDestroy(m->copy);
     cudaFree(m->dev_pool);
     if (m->host_pool) cudaFreeHost(m->host_pool);
@@ -604,11 +625,50 @@ extern "C" const void *pgmoe_model_matrix_ptr(pgmoe_model *m, const char *name, 
     return mat_ptr(m, name ? name : "", block, expert, &bytes, &on_host);
 }
 
+// Resident iterations have no host round trip, so the whole block loop
+// (route, pack, up, down, dense per block; PDL edges between them) is
+// captured once per buffer set and replayed as one graph launch.
+static int decoder_iteration_graph(pgmoe_model *m, const float *x_in, int T, float *y_out, int32_t *ids,
+                                   float *w, cudaStream_t s) {
+    if (m->gexec && m->g_x == x_in && m->g_y == y_out && m->g_T == T && m->g_ids == ids && m->g_w == w) {
+        PG_CUDA(cudaGraphLaunch(m->gexec, s));
+        return PGMOE_OK;
+    }
+    if (m->gexec) {
+        cudaGraphExecDestroy(m->gexec);
+        m->gexec = nullptr;
+    }
+    if (!m->cap) PG_CUDA(cudaStreamCreateWithFlags(&m->cap, cudaStreamNonBlocking));
+    PG_CUDA(cudaStreamBeginCapture(m->cap, cudaStreamCaptureModeThreadLocal));
+    const int st = decoder_iteration(m, x_in, T, y_out, ids, w, m->cap);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(m->cap, &graph);
+    if (st != PGMOE_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    PG_CUDA(ce);
+    const cudaError_t ie = cudaGraphInstantiate(&m->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    PG_CUDA(ie);
+    m->g_x = x_in;
+    m->g_y = y_out;
+    m->g_T = T;
+    m->g_ids = ids;
+    m->g_w = w;
+    PG_CUDA(cudaGraphLaunch(m->gexec, s));
+    return PGMOE_OK;
+}
+
 extern "C" int pgmoe_decoder_iteration(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
                                        int32_t *ids_trace, float *w_trace, pgmoe_stream_t stream) {
     PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
     std::lock_guard<std::mutex> g(m->mu);
-    return decoder_iteration(m, x_in, T, y_out, ids_trace, w_trace, reinterpret_cast<cudaStream_t>(stream));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (m->placement == PGMOE_RESIDENT && m->use_graph && !m->timeline && T > 0 && T <= m->max_tokens &&
+        m->e_local == m->cfg.num_experts)
+        return decoder_iteration_graph(m, x_in, T, y_out, ids_trace, w_trace, s);
+    return decoder_iteration(m, x_in, T, y_out, ids_trace, w_trace, s);
 }
 
 static int check_all_routing(pgmoe_model *m) {
@@ -624,39 +684,41 @@ static int check_all_routing(pgmoe_model *m) {
 extern "C" int pgmoe_decoder_iteration_host(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
                                             int32_t *ids_trace, float *w_trace) {
     PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
-    std::lock_guard<std::mutex> g(m->mu);
     const auto &c = m->cfg;
     PG_REQUIRE(T >= 0 && T <= m->max_tokens, PGMOE_E_SHAPE, "T=%d exceeds max_tokens=%d", T, m->max_tokens);
     if (T == 0) return PGMOE_OK;
     const size_t xb = (size_t)T * c.d_model * 4, tb = (size_t)c.num_blocks * T * c.top_k * 4;
-    float *dx = nullptr, *dy = nullptr, *dw = nullptr;
-    int32_t *di = nullptr;
-    cudaStream_t s = nullptr;
-    PG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    PG_CUDA(cudaMallocAsync(&dx, xb, s));
-    PG_CUDA(cudaMallocAsync(&dy, xb, s));
-    if (ids_trace) {
-        PG_CUDA(cudaMallocAsync(&di, tb, s));
-        PG_CUDA(cudaMallocAsync(&dw, tb, s));
-    }
-    PG_CUDA(cudaMemcpyAsync(dx, x_in, xb, cudaMemcpyHostToDevice, s));
-    int st = decoder_iteration(m, dx, T, dy, di, dw, s);
-    if (st == PGMOE_OK) {
-        cudaMemcpyAsync(y_out, dy, xb, cudaMemcpyDeviceToHost, s);
-        if (ids_trace) {
-            cudaMemcpyAsync(ids_trace, di, tb, cudaMemcpyDeviceToHost, s);
-            cudaMemcpyAsync(w_trace, dw, tb, cudaMemcpyDeviceToHost, s);
+    {
+        std::lock_guard<std::mutex> g(m->mu);
+        if (!m->io_stream) {  // persistent I/O buffers: the graph path keys on their addresses
+            const size_t cap_x = (size_t)m->max_tokens * c.d_model * 4;
+            const size_t cap_t = (size_t)c.num_blocks * m->max_tokens * c.top_k * 4;
+            PG_CUDA(cudaStreamCreateWithFlags(&m->io_stream, cudaStreamNonBlocking));
+            PG_CUDA(cudaMalloc(&m->io_x, cap_x));
+            PG_CUDA(cudaMalloc(&m->io_y, cap_x));
+            PG_CUDA(cudaMalloc(&m->io_ids, cap_t));
+            PG_CUDA(cudaMalloc(&m->io_w, cap_t));
         }
     }
-    cudaFreeAsync(dx, s);
-    cudaFreeAsync(dy, s);
-    if (di) { cudaFreeAsync(di, s); cudaFreeAsync(dw, s); }
+    cudaStream_t s = m->io_stream;
+    PG_CUDA(cudaMemcpyAsync(m->io_x, x_in, xb, cudaMemcpyHostToDevice, s));
+    int st = pgmoe_decoder_iteration(m, m->io_x, T, m->io_y, ids_trace ? m->io_ids : nullptr,
+                                     ids_trace ? m->io_w : nullptr, reinterpret_cast<pgmoe_stream_t>(s));
+    if (st == PGMOE_OK) {
+        PG_CUDA(cudaMemcpyAsync(y_out, m->io_y, xb, cudaMemcpyDeviceToHost, s));
+        if (ids_trace) {
+            PG_CUDA(cudaMemcpyAsync(ids_trace, m->io_ids, tb, cudaMemcpyDeviceToHost, s));
+            PG_CUDA(cudaMemcpyAsync(w_trace, m->io_w, tb, cudaMemcpyDeviceToHost, s));
+        }
+    }
     if (cudaStreamSynchronize(s) != cudaSuccess && st == PGMOE_OK) {
         set_error("decoder iteration failed: %s", cudaGetErrorString(cudaGetLastError()));
         st = PGMOE_E_CUDA;
     }
-    cudaStreamDestroy(s);
-    if (st == PGMOE_OK) st = check_all_routing(m);
+    if (st == PGMOE_OK) {
+        std::lock_guard<std::mutex> g(m->mu);
+        st = check_all_routing(m);
+    }
     return st;
 }
 
