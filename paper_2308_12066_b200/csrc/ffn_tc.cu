@@ -281,16 +281,23 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
     sc.tiles = prefix[sc.groups];
     sc.max_npad = s_flag[1];
     {
-        // split K only when there are too few tiles to cover the SMs
+        // Split K when the tiles do not cover the SMs evenly: pick the
+        // smallest split whose units fill >= 93% of the last wave, else the
+        // best one.  The fix-up reads S x n partial columns per row, so wide
+        // N tiles (which carry enough MMA work anyway) split less.
+        const int s_cap = max(1, min(sc.kb_total, 8 * 16 / min(BN, sc.max_npad)));
         int S = 1;
-        const long long want = 2LL * gridDim.x;
-        if (sc.tiles > 0 && sc.tiles < want) {
-            const long long q = (want + sc.tiles - 1) / sc.tiles;
-            S = (int)(q < sc.kb_total ? q : sc.kb_total);
+        float best = 0.f;
+        for (int cand = 1; cand <= s_cap && sc.tiles > 0; ++cand) {
+            const long long u = sc.tiles * cand;
+            const long long waves = (u + gridDim.x - 1) / gridDim.x;
+            const float eff = (float)u / (float)(waves * gridDim.x);
+            if (eff > best + 0.02f) {
+                best = eff;
+                S = cand;
+            }
+            if (eff >= 0.93f) break;
         }
-        // the fix-up reads S x n partial columns per row: keep it small next
-        // to the tile's own K loop (wide N tiles already carry enough work)
-        S = min(S, max(1, 8 * 16 / min(BN, sc.max_npad)));
         while (S > 1 && ((long long)sc.tiles * S * BN * BM > p.partial_cap || sc.tiles > kCounterInts)) --S;
         sc.kbs = (sc.kb_total + S - 1) / S;
         sc.S = (sc.kb_total + sc.kbs - 1) / sc.kbs;

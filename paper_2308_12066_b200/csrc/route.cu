@@ -14,21 +14,37 @@
 // the top-k are recomputed in exactly the reference order (serial
 // __dadd_rn/__dmul_rn) and ranked with the reference key (-logit, id).
 // The fallback count is reported; flips are zero by construction.
+//
+// Two kernels:
+//   route_logits_kernel : grid (token tiles x K splits); each thread owns
+//       V adjacent experts (one 16-byte gate load) for TOK tokens and
+//       accumulates fp64 logits (DFMA) plus the fp32 |p| sum of the bound
+//       (FFMA pipe), reduced in a fixed order into per-split partials.
+//   route_select_kernel : one warp per token sums the split partials in
+//       order, certifies / recomputes, softmax, writes ids & weights; the
+//       last CTA builds histogram, exclusive scan, stable permutation and
+//       the active-expert list.
 #include <algorithm>
 
 #include "common.cuh"
 
 namespace pgmoe {
 
-constexpr int kRouteThreads = 512;
-constexpr int kRouteWarps = kRouteThreads / 32;
+constexpr int kLogitThreads = 256;
+constexpr int kSelectWarps = 8;
+constexpr int kSelectThreads = kSelectWarps * 32;
+constexpr int kMaxSplits = 64;
 
 struct RouteParams {
     const float *x;
     const void *G;
     int T, d, E, k;
+    int tok;      // tokens per logits CTA
+    int splits;   // K splits
     pgmoe_routing out;
-    int *counter;  // workspace: CTAs finished (reset by the last CTA)
+    int *counter;      // workspace: select CTAs finished (reset by the last CTA)
+    double *plogit;    // workspace: [splits][T][E]
+    float *pabs;       // workspace: [splits][T][E]
 };
 
 __device__ __forceinline__ bool better(double fa, int ia, double fb, int ib) {
@@ -62,103 +78,171 @@ __device__ __forceinline__ double warp_sumd(double v) {
 
 // Serial fp64 logit in the reference order (linalg.py:35-37): out += x_i*G_ij.
 template <typename WT>
-__device__ double serial_logit(const double *xs, const WT *G, int d, int E, int j) {
+__device__ double serial_logit(const float *x, const WT *G, int d, int E, int j) {
     double acc = 0.0;
     for (int i = 0; i < d; ++i) {
         double g = (double)WTraits<WT>::f32(G[(size_t)i * E + j]);
-        acc = __dadd_rn(acc, __dmul_rn(xs[i], g));
+        acc = __dadd_rn(acc, __dmul_rn((double)x[i], g));
     }
     return acc;
 }
 
-template <typename WT, int TOK>
-__global__ void __launch_bounds__(kRouteThreads)
-route_kernel(RouteParams p) {
+template <typename WT> struct Vec;
+template <> struct Vec<uint16_t> {
+    static constexpr int N = 8;
+    __device__ __forceinline__ static void load(const uint16_t *p, float (&o)[8]) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            o[2 * i] = __uint_as_float(w[i] << 16);
+            o[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+        }
+    }
+};
+template <> struct Vec<float> {
+    static constexpr int N = 4;
+    __device__ __forceinline__ static void load(const float *p, float (&o)[4]) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+};
+
+// Partial logits of TOK tokens over the CTA's K range; expert columns in
+// groups of V (16-byte gate loads when VECLOAD).
+template <typename WT, int TOK, bool VECLOAD>
+__global__ void __launch_bounds__(kLogitThreads)
+route_logits_kernel(RouteParams p) {
+    constexpr int V = Vec<WT>::N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int d = p.d, E = p.E, k = p.k;
+    const int d = p.d, E = p.E;
     const WT *G = static_cast<const WT *>(p.G);
     const int t0 = blockIdx.x * TOK;
     const int ntok = min(TOK, p.T - t0);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int split = blockIdx.y;
+    const int k0 = (int)((long)d * split / p.splits), k1 = (int)((long)d * (split + 1) / p.splits);
+    const int kn = k1 - k0;
+    const int CG = (E + V - 1) / V;                // column groups
+    const int RG = max(1, kLogitThreads / CG);     // row groups
+    const int tid = threadIdx.x;
+    const int cg = tid % CG, rg = tid / CG;
 
-    // smem carve: x tile [TOK][d] f64 | part [KS][TOK][EL] (val f64, |p| f32) |
-    // logit [TOK][E] f64 | bound [TOK][E] f64
-    const int EL = E < kRouteThreads ? E : kRouteThreads;  // expert lanes
-    const int KS = kRouteThreads / EL;                     // k-splits
-    double *xs = reinterpret_cast<double *>(smem_raw);
-    double *part = xs + (size_t)TOK * d;
-    float *parta = reinterpret_cast<float *>(part + (size_t)KS * TOK * EL);
-    double *logit = reinterpret_cast<double *>(parta + (((size_t)KS * TOK * EL + 1) & ~(size_t)1));
-    double *bound = logit + (size_t)TOK * E;
+    double *xd = reinterpret_cast<double *>(smem_raw);            // [TOK][kn]
+    float *xf = reinterpret_cast<float *>(xd + (size_t)TOK * kn);  // [TOK][kn]
+    double *red = reinterpret_cast<double *>(smem_raw);            // reuse: [RG][TOK][E] f64
+    float *reda = reinterpret_cast<float *>(red + (size_t)RG * TOK * E);  // [RG][TOK][E] f32
 
     pdl_wait();  // x is produced by the previous kernel in the stream
     pdl_trigger();
-    for (int i = tid; i < TOK * d; i += kRouteThreads) {
-        int t = i / d;
-        xs[i] = (t < ntok) ? (double)p.x[(size_t)(t0 + t) * d + (i - t * d)] : 0.0;
+    for (int i = tid; i < TOK * kn; i += kLogitThreads) {
+        const int t = i / kn;
+        const float v = (t < ntok) ? __ldg(p.x + (size_t)(t0 + t) * d + k0 + (i - t * kn)) : 0.f;
+        xd[i] = (double)v;
+        xf[i] = fabsf(v);
     }
     __syncthreads();
 
-    // ---- fast fp64 logits (exact products, any order) + fp32 sum|p| ------
-    // The |p| sum only feeds the error bound, so it runs on the fp32 pipe
-    // next to the DFMAs; its own rounding (< d*2^-24 relative) is covered by
-    // the 1.001 factor below.
-    const int ks = tid / EL, jl = tid - ks * EL;
-    const double u = 1.1102230246251565e-16;  // 2^-53
-    const double gam = (double)d * u / (1.0 - (double)d * u);
-    const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
-    for (int j0 = 0; j0 < E; j0 += EL) {
-        const int j = j0 + jl;
-        if (ks < KS && j < E) {
-            const int i0 = (int)((long)d * ks / KS), i1 = (int)((long)d * (ks + 1) / KS);
-            double acc[TOK];
-            float aab[TOK];
+    double acc[TOK][V];
+    float aab[TOK][V];
+#pragma unroll
+    for (int t = 0; t < TOK; ++t)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            acc[t][v] = 0.0;
+            aab[t][v] = 0.f;
+        }
+    const int j0 = cg * V;
+    if (rg < RG && cg < CG) {
+#pragma unroll 2
+        for (int i = rg; i < kn; i += RG) {
+            float g[V];
+            const WT *row = G + (size_t)(k0 + i) * E;
+            if (VECLOAD) {
+                Vec<WT>::load(row + j0, g);
+            } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v) g[v] = (j0 + v < E) ? WTraits<WT>::f32(__ldg(row + j0 + v)) : 0.f;
+            }
+            double gd[V];
+            float ga[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                gd[v] = (double)g[v];
+                ga[v] = fabsf(g[v]);
+            }
 #pragma unroll
             for (int t = 0; t < TOK; ++t) {
-                acc[t] = 0.0;
-                aab[t] = 0.f;
-            }
-#pragma unroll 8
-            for (int i = i0; i < i1; ++i) {
-                const float gf = WTraits<WT>::f32(__ldg(G + (size_t)i * E + j));
-                const double g = (double)gf;
-                const float ga = fabsf(gf);
+                const double xv = xd[t * kn + i];
+                const float xa = xf[t * kn + i];
 #pragma unroll
-                for (int t = 0; t < TOK; ++t) {
-                    const double xv = xs[t * d + i];
-                    acc[t] = fma(xv, g, acc[t]);  // product exact in fp64: one rounding per add
-                    aab[t] = fmaf(fabsf((float)xv), ga, aab[t]);
+                for (int v = 0; v < V; ++v) {
+                    acc[t][v] = fma(xv, gd[v], acc[t][v]);  // exact product: one rounding per add
+                    aab[t][v] = fmaf(xa, ga[v], aab[t][v]);
                 }
             }
-#pragma unroll
-            for (int t = 0; t < TOK; ++t) {
-                part[((size_t)ks * TOK + t) * EL + jl] = acc[t];
-                parta[((size_t)ks * TOK + t) * EL + jl] = aab[t];
-            }
         }
-        __syncthreads();
-        for (int q = tid; q < TOK * EL; q += kRouteThreads) {
-            const int t = q / EL, jj = q - t * EL;
-            if (j0 + jj >= E) continue;
+    }
+    __syncthreads();  // x tile no longer needed: reuse smem for the reduction
+    if (rg < RG && cg < CG) {
+#pragma unroll
+        for (int t = 0; t < TOK; ++t)
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                if (j0 + v < E) {
+                    red[((size_t)rg * TOK + t) * E + j0 + v] = acc[t][v];
+                    reda[((size_t)rg * TOK + t) * E + j0 + v] = aab[t][v];
+                }
+    }
+    __syncthreads();
+    for (int q = tid; q < ntok * E; q += kLogitThreads) {
+        const int t = q / E, j = q - t * E;
+        double s = 0.0;
+        float a = 0.f;
+        for (int r = 0; r < RG; ++r) {  // fixed order: deterministic
+            s += red[((size_t)r * TOK + t) * E + j];
+            a += reda[((size_t)r * TOK + t) * E + j];
+        }
+        const size_t o = ((size_t)split * p.T + t0 + t) * E + j;
+        p.plogit[o] = s;
+        p.pabs[o] = a;
+    }
+}
+
+template <typename WT>
+__global__ void __launch_bounds__(kSelectThreads)
+route_select_kernel(RouteParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int d = p.d, E = p.E, k = p.k;
+    const WT *G = static_cast<const WT *>(p.G);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double *logit = reinterpret_cast<double *>(smem_raw) + (size_t)warp * 2 * E;
+    double *bound = logit + E;
+
+    pdl_wait();  // partial logits come from route_logits_kernel
+    pdl_trigger();
+    const double u = 1.1102230246251565e-16;  // 2^-53
+    const double gam = (double)d * u / (1.0 - (double)d * u);
+    // fp32 |p| terms round by <= 2^-24 each (d of them) and may flush below
+    // FLT_MIN: pad relatively (1.001) and absolutely (d * 2 * FLT_MIN).
+    const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
+    const double bpad = (double)d * 2.4e-38;
+
+    const int tok = blockIdx.x * kSelectWarps + warp;
+    if (tok < p.T) {
+        double *lg = logit;
+        double *bd = bound;
+        for (int j = lane; j < E; j += 32) {
             double s = 0.0;
             float a = 0.f;
-            for (int z = 0; z < KS; ++z) {  // fixed order: deterministic
-                s += part[((size_t)z * TOK + t) * EL + jj];
-                a += parta[((size_t)z * TOK + t) * EL + jj];
+            for (int z = 0; z < p.splits; ++z) {  // fixed order: deterministic
+                const size_t o = ((size_t)z * p.T + tok) * E + j;
+                s += p.plogit[o];
+                a += p.pabs[o];
             }
-            logit[(size_t)t * E + j0 + jj] = s;
-            // fp32 |p| terms can round down by 2^-24 each and flush below
-            // FLT_MIN: pad relatively and absolutely.
-            bound[(size_t)t * E + j0 + jj] = bscale * (double)a + (double)d * 2.4e-38;
+            lg[j] = s;
+            bd[j] = bscale * (double)a + bpad;
         }
-        __syncthreads();
-    }
-
-    // ---- per-token selection, certification, softmax (one warp/token) ----
-    for (int t = warp; t < ntok; t += kRouteWarps) {
-        double *lg = logit + (size_t)t * E;
-        const double *bd = bound + (size_t)t * E;
-        const int tok = t0 + t;
+        __syncwarp();
         // finite check (core.py:297)
         bool finite = true;
         for (int j = lane; j < E; j += 32) finite &= (bool)isfinite(lg[j]);
@@ -169,67 +253,68 @@ route_kernel(RouteParams p) {
                 p.out.ids[(size_t)tok * k + s] = 0;
                 p.out.w[(size_t)tok * k + s] = 0.f;
             }
-            continue;
-        }
-        int sel[8];
-        uint32_t taken = 0;  // bit q: expert lane + 32*q taken
-        bool certified = true;
-        double minlow = INFINITY;
-        for (int s = 0; s < k; ++s) {
-            double bf = -INFINITY;
-            int bi = -1;
-            for (int j = lane, q = 0; j < E; j += 32, ++q)
-                if (!(taken >> q & 1u) && (bi < 0 || better(lg[j], j, bf, bi))) {
-                    bf = lg[j];
-                    bi = j;
-                }
-            warp_argmax(bf, bi);
-            sel[s] = bi;
-            if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-            const double low = bf - bd[bi];
-            minlow = fmin(minlow, low);
-            double up = -INFINITY;
-            for (int j = lane, q = 0; j < E; j += 32, ++q)
-                if (!(taken >> q & 1u)) up = fmax(up, lg[j] + bd[j]);
-            up = warp_max(up);
-            certified &= (low > up);
-        }
-        if (!certified) {
-            // Candidates that could be in the reference top-k.
-            uint32_t cand = 0;
-            for (int j = lane, q = 0; j < E; j += 32, ++q)
-                if (lg[j] + bd[j] >= minlow) cand |= 1u << q;
-            __syncwarp();
-            for (int j = lane, q = 0; j < E; j += 32, ++q)
-                if (cand >> q & 1u) lg[j] = serial_logit<WT>(xs + (size_t)t * d, G, d, E, j);
-            __syncwarp();
+        } else {
+            int sel[8];
+            uint32_t taken = 0;  // bit q: expert lane + 32*q taken
+            bool certified = true;
+            double minlow = INFINITY;
             for (int s = 0; s < k; ++s) {
                 double bf = -INFINITY;
                 int bi = -1;
                 for (int j = lane, q = 0; j < E; j += 32, ++q)
-                    if ((cand >> q & 1u) && (bi < 0 || better(lg[j], j, bf, bi))) {
+                    if (!(taken >> q & 1u) && (bi < 0 || better(lg[j], j, bf, bi))) {
                         bf = lg[j];
                         bi = j;
                     }
                 warp_argmax(bf, bi);
                 sel[s] = bi;
-                if ((bi & 31) == lane) cand &= ~(1u << (bi >> 5));
+                if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+                const double low = bf - bd[bi];
+                minlow = fmin(minlow, low);
+                double up = -INFINITY;
+                for (int j = lane, q = 0; j < E; j += 32, ++q)
+                    if (!(taken >> q & 1u)) up = fmax(up, lg[j] + bd[j]);
+                up = warp_max(up);
+                certified &= (low > up);
             }
-            if (lane == 0) atomicAdd(p.out.status + 1, 1);
-        }
-        // softmax over all E (linalg.py:54-59), max-subtracted
-        double m = -INFINITY;
-        for (int j = lane; j < E; j += 32) m = fmax(m, lg[j]);
-        m = warp_max(m);
-        double z = 0.0;
-        for (int j = lane; j < E; j += 32) z += exp(lg[j] - m);
-        z = warp_sumd(z);
-        for (int s = 0; s < k; ++s) {
-            const double pr = exp(lg[sel[s]] - m) / z;
-            if (lane == 0) {
-                if (!(pr > 0.0)) atomicCAS(p.out.status, 0, (int)PGMOE_E_GATE_UNDERFLOW);
-                p.out.ids[(size_t)tok * k + s] = sel[s];
-                p.out.w[(size_t)tok * k + s] = __double2float_rn(pr);
+            if (!certified) {
+                // Candidates that could be in the reference top-k: recompute
+                // them in the reference's serial order.
+                uint32_t cand = 0;
+                for (int j = lane, q = 0; j < E; j += 32, ++q)
+                    if (lg[j] + bd[j] >= minlow) cand |= 1u << q;
+                __syncwarp();
+                for (int j = lane, q = 0; j < E; j += 32, ++q)
+                    if (cand >> q & 1u) lg[j] = serial_logit<WT>(p.x + (size_t)tok * d, G, d, E, j);
+                __syncwarp();
+                for (int s = 0; s < k; ++s) {
+                    double bf = -INFINITY;
+                    int bi = -1;
+                    for (int j = lane, q = 0; j < E; j += 32, ++q)
+                        if ((cand >> q & 1u) && (bi < 0 || better(lg[j], j, bf, bi))) {
+                            bf = lg[j];
+                            bi = j;
+                        }
+                    warp_argmax(bf, bi);
+                    sel[s] = bi;
+                    if ((bi & 31) == lane) cand &= ~(1u << (bi >> 5));
+                }
+                if (lane == 0) atomicAdd(p.out.status + 1, 1);
+            }
+            // softmax over all E (linalg.py:54-59), max-subtracted
+            double m = -INFINITY;
+            for (int j = lane; j < E; j += 32) m = fmax(m, lg[j]);
+            m = warp_max(m);
+            double z = 0.0;
+            for (int j = lane; j < E; j += 32) z += exp(lg[j] - m);
+            z = warp_sumd(z);
+            for (int s = 0; s < k; ++s) {
+                const double pr = exp(lg[sel[s]] - m) / z;
+                if (lane == 0) {
+                    if (!(pr > 0.0)) atomicCAS(p.out.status, 0, (int)PGMOE_E_GATE_UNDERFLOW);
+                    p.out.ids[(size_t)tok * k + s] = sel[s];
+                    p.out.w[(size_t)tok * k + s] = __double2float_rn(pr);
+                }
             }
         }
     }
@@ -246,18 +331,17 @@ route_kernel(RouteParams p) {
     __threadfence();
 
     const int N = p.T * k;
-    int *whist = reinterpret_cast<int *>(smem_raw);  // [kRouteWarps][E] -> cursors
-    int *tot = whist + (size_t)kRouteWarps * E;      // [E]
-    for (int i = tid; i < kRouteWarps * E; i += kRouteThreads) whist[i] = 0;
+    int *whist = reinterpret_cast<int *>(smem_raw);  // [kSelectWarps][E] -> cursors
+    int *tot = whist + (size_t)kSelectWarps * E;     // [E]
+    for (int i = tid; i < kSelectWarps * E; i += kSelectThreads) whist[i] = 0;
     __syncthreads();
-    const int seg = (N + kRouteWarps - 1) / kRouteWarps;
+    const int seg = (N + kSelectWarps - 1) / kSelectWarps;
     const int r0 = warp * seg, r1 = min(N, r0 + seg);
     for (int r = r0 + lane; r < r1; r += 32) atomicAdd(&whist[warp * E + __ldcg(p.out.ids + r)], 1);
     __syncthreads();
-    // per-expert totals, then base cursor per (warp, expert)
-    for (int e = tid; e < E; e += kRouteThreads) {
+    for (int e = tid; e < E; e += kSelectThreads) {
         int s = 0;
-        for (int w = 0; w < kRouteWarps; ++w) s += whist[w * E + e];
+        for (int w = 0; w < kSelectWarps; ++w) s += whist[w * E + e];
         tot[e] = s;
     }
     __syncthreads();
@@ -289,9 +373,9 @@ route_kernel(RouteParams p) {
         }
     }
     __syncthreads();
-    for (int e = tid; e < E; e += kRouteThreads) {
+    for (int e = tid; e < E; e += kSelectThreads) {
         int base = tot[e];
-        for (int w = 0; w < kRouteWarps; ++w) {
+        for (int w = 0; w < kSelectWarps; ++w) {
             const int c = whist[w * E + e];
             whist[w * E + e] = base;
             base += c;
@@ -318,44 +402,75 @@ route_kernel(RouteParams p) {
     if (tid == 0) *p.counter = 0;
 }
 
-static size_t route_smem(int TOK, int d, int E) {
-    const int EL = E < kRouteThreads ? E : kRouteThreads;
-    const int KS = kRouteThreads / EL;
-    size_t a = (size_t)TOK * d * 8 + (size_t)KS * TOK * EL * 8 + (((size_t)KS * TOK * EL + 1) & ~(size_t)1) * 4 +
-               (size_t)2 * TOK * E * 8;
-    size_t b = (size_t)(kRouteWarps + 1) * E * 4;
-    return a > b ? a : b;
+static int pick_tok(int T) { return T <= kNumSMs ? 1 : (T <= 2 * kNumSMs ? 2 : 4); }
+
+static int pick_splits(int T, int d, int tok) {
+    const int tiles = (T + tok - 1) / tok;
+    int s = std::max(1, (2 * kNumSMs) / std::max(1, tiles));
+    s = std::min(s, std::max(1, d / 32));  // at least 32 gate rows per CTA
+    s = std::max(s, (int)(((size_t)d * tok * 12 + 131071) / 131072));  // x tile fits in shared memory
+    return std::min(s, kMaxSplits);
+}
+
+static size_t logits_smem(int tok, int d, int splits, int E, int V) {
+    const int kn = (d + splits - 1) / splits;
+    const int CG = (E + V - 1) / V, RG = std::max(1, kLogitThreads / CG);
+    const size_t a = (size_t)tok * kn * 12;
+    const size_t b = (size_t)RG * tok * E * 12;
+    return std::max(a, b);
 }
 
 template <typename WT, int TOK>
-static int launch_route(const RouteParams &p, cudaStream_t s) {
-    const size_t smem = route_smem(TOK, p.d, p.E);
-    PG_REQUIRE(smem <= 220 * 1024, PGMOE_E_CONFIG, "route: d=%d E=%d exceeds shared memory", p.d, p.E);
-    static size_t attr_smem = 0;  // per instantiation: raise the limit once
-    if (smem > attr_smem) {
-        PG_CUDA(cudaFuncSetAttribute(route_kernel<WT, TOK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)std::max<size_t>(smem, 100 * 1024)));
-        attr_smem = std::max<size_t>(smem, 100 * 1024);
+static int launch_logits(const RouteParams &p, cudaStream_t s) {
+    constexpr int V = Vec<WT>::N;
+    const size_t smem = logits_smem(TOK, p.d, p.splits, p.E, V);
+    PG_REQUIRE(smem <= 200 * 1024, PGMOE_E_CONFIG, "route: d=%d E=%d exceeds shared memory", p.d, p.E);
+    const bool vec = (p.E % V == 0) && (reinterpret_cast<uintptr_t>(p.G) % 16 == 0);
+    auto kern = vec ? route_logits_kernel<WT, TOK, true> : route_logits_kernel<WT, TOK, false>;
+    static size_t attr[2] = {0, 0};
+    if (smem > attr[vec]) {
+        const size_t want = std::max<size_t>(smem, 64 * 1024);
+        PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want));
+        attr[vec] = want;
     }
-    const int grid = (p.T + TOK - 1) / TOK;
-    PG_CUDA(launch_pdl(route_kernel<WT, TOK>, dim3(grid), dim3(kRouteThreads), smem, s, p));
+    const dim3 grid((p.T + TOK - 1) / TOK, p.splits);
+    PG_CUDA(launch_pdl(kern, grid, dim3(kLogitThreads), smem, s, p));
     count_launch();
     return PGMOE_OK;
 }
 
 template <typename WT>
-static int route_dispatch(const RouteParams &p, cudaStream_t s) {
-    // about one CTA per SM: more tokens per CTA reuse each gate column load
-    if (p.T <= kNumSMs) return launch_route<WT, 1>(p, s);
-    if (p.T <= 2 * kNumSMs) return launch_route<WT, 2>(p, s);
-    return launch_route<WT, 4>(p, s);
+static int route_dispatch(RouteParams p, cudaStream_t s) {
+    int st;
+    if (p.tok == 1) st = launch_logits<WT, 1>(p, s);
+    else if (p.tok == 2) st = launch_logits<WT, 2>(p, s);
+    else st = launch_logits<WT, 4>(p, s);
+    if (st != PGMOE_OK) return st;
+    const size_t smem = std::max<size_t>((size_t)kSelectWarps * p.E * 16, (size_t)(kSelectWarps + 1) * p.E * 4);
+    static size_t attr = 0;
+    if (smem > attr) {
+        const size_t want = std::max<size_t>(smem, 64 * 1024);
+        PG_CUDA(cudaFuncSetAttribute(route_select_kernel<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want));
+        attr = want;
+    }
+    const int grid = (p.T + kSelectWarps - 1) / kSelectWarps;
+    PG_CUDA(launch_pdl(route_select_kernel<WT>, dim3(grid), dim3(kSelectThreads), smem, s, p));
+    count_launch();
+    return PGMOE_OK;
 }
 
 }  // namespace pgmoe
 
 using namespace pgmoe;
 
-extern "C" size_t pgmoe_route_workspace_bytes(int32_t, int32_t) { return 256; }
+// workspace: [counter | pad to 256 B | plogit f64 [S][T][E] | pabs f32 [S][T][E]]
+extern "C" size_t pgmoe_route_workspace_bytes(int32_t T, int32_t E) {
+    // the split count depends on the call's T (and d); size for the worst T' <= T
+    size_t worst = 0;
+    for (int t = 1; t <= std::max(T, 1); ++t)
+        worst = std::max(worst, (size_t)pick_splits(t, 1 << 20, pick_tok(t)) * t);
+    return 256 + worst * std::max(E, 1) * 12;
+}
 
 extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const void *gate_w,
                                   int32_t wdtype, int32_t E, int32_t k, const pgmoe_routing *out,
@@ -373,7 +488,21 @@ extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const vo
         PG_CUDA(cudaMemsetAsync(out->n_act, 0, sizeof(int32_t), s));
         return PGMOE_OK;
     }
-    RouteParams p{x, gate_w, T, d, E, k, *out, static_cast<int *>(workspace)};
+    char *ws = static_cast<char *>(workspace);
+    RouteParams p{};
+    p.x = x;
+    p.G = gate_w;
+    p.T = T;
+    p.d = d;
+    p.E = E;
+    p.k = k;
+    p.out = *out;
+    p.tok = pick_tok(T);
+    p.splits = pick_splits(T, d, p.tok);
+    p.counter = reinterpret_cast<int *>(ws);
+    const size_t n = (size_t)p.splits * T * E;
+    p.plogit = reinterpret_cast<double *>(ws + 256);
+    p.pabs = reinterpret_cast<float *>(ws + 256 + n * 8);
     if (wdtype == PGMOE_BF16) return route_dispatch<uint16_t>(p, s);
     if (wdtype == PGMOE_F32) return route_dispatch<float>(p, s);
     set_error("unknown weight dtype %d", wdtype);

@@ -94,12 +94,17 @@ struct pgmoe_model {
     // resident decoder iterations are replayed from a CUDA graph per buffer set
     bool use_graph = true;
     cudaStream_t cap = nullptr;
-    cudaGraphExec_t gexec = nullptr;
-    const float *g_x = nullptr;
-    float *g_y = nullptr;
-    int g_T = -1;
-    int32_t *g_ids = nullptr;
-    float *g_w = nullptr;
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        const float *x = nullptr;
+        float *y = nullptr;
+        int T = -1;
+        int32_t *ids = nullptr;
+        float *w = nullptr;
+        unsigned long long last_use = 0;
+    };
+    GraphEntry graphs[8];  // small LRU: callers' output buffers rotate through the allocator
+    unsigned long long graph_clock = 0;
     // host-buffer entry point
     cudaStream_t io_stream = nullptr;
     float *io_x = nullptr, *io_y = nullptr, *io_w = nullptr;
@@ -458,7 +463,8 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
         if ((st = alloc_routing(m->routing[i], max_tokens, c.num_experts, (int)k)) != PGMOE_OK) return fail(st);
         cudaEventCreateWithFlags(&m->routed[i], cudaEventDisableTiming);
     }
-    if (cudaMalloc(&m->route_ws, 256) != cudaSuccess || cudaMemset(m->route_ws, 0, 256) != cudaSuccess)
+    const size_t rws = pgmoe_route_workspace_bytes(max_tokens, c.num_experts);
+    if (cudaMalloc(&m->route_ws, rws) != cudaSuccess || cudaMemset(m->route_ws, 0, rws) != cudaSuccess)
         return fail(PGMOE_E_OOM);
     const size_t T = max_tokens;
     if (cudaMalloc(&m->act_buf[0], T * d * 4) != cudaSuccess ||
@@ -495,7 +501,8 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     for (auto e : m->ffn_b) cudaEventDestroy(e);
     for (auto &e : m->tl) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (m->t0) cudaEventDestroy(m->t0);
-    if (m->gexec) cudaGraphExecDestroy(m->gexec);
+    for (auto &g : m->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     if (m->io_stream) cudaStreamDestroy(m->io_stream);
     cudaFree(m->io_x);
     cudaFree(m->io_y);
@@ -630,13 +637,19 @@ extern "C" const void *pgmoe_model_matrix_ptr(pgmoe_model *m, const char *name, 
 // captured once per buffer set and replayed as one graph launch.
 static int decoder_iteration_graph(pgmoe_model *m, const float *x_in, int T, float *y_out, int32_t *ids,
                                    float *w, cudaStream_t s) {
-    if (m->gexec && m->g_x == x_in && m->g_y == y_out && m->g_T == T && m->g_ids == ids && m->g_w == w) {
-        PG_CUDA(cudaGraphLaunch(m->gexec, s));
-        return PGMOE_OK;
+    ++m->graph_clock;
+    pgmoe_model::GraphEntry *victim = &m->graphs[0];
+    for (auto &g : m->graphs) {
+        if (g.exec && g.x == x_in && g.y == y_out && g.T == T && g.ids == ids && g.w == w) {
+            g.last_use = m->graph_clock;
+            PG_CUDA(cudaGraphLaunch(g.exec, s));
+            return PGMOE_OK;
+        }
+        if (!g.exec || g.last_use < victim->last_use) victim = &g;
     }
-    if (m->gexec) {
-        cudaGraphExecDestroy(m->gexec);
-        m->gexec = nullptr;
+    if (victim->exec) {
+        cudaGraphExecDestroy(victim->exec);
+        victim->exec = nullptr;
     }
     if (!m->cap) PG_CUDA(cudaStreamCreateWithFlags(&m->cap, cudaStreamNonBlocking));
     PG_CUDA(cudaStreamBeginCapture(m->cap, cudaStreamCaptureModeThreadLocal));
@@ -648,15 +661,16 @@ static int decoder_iteration_graph(pgmoe_model *m, const float *x_in, int T, flo
         return st;
     }
     PG_CUDA(ce);
-    const cudaError_t ie = cudaGraphInstantiate(&m->gexec, graph, 0);
+    const cudaError_t ie = cudaGraphInstantiate(&victim->exec, graph, 0);
     cudaGraphDestroy(graph);
     PG_CUDA(ie);
-    m->g_x = x_in;
-    m->g_y = y_out;
-    m->g_T = T;
-    m->g_ids = ids;
-    m->g_w = w;
-    PG_CUDA(cudaGraphLaunch(m->gexec, s));
+    victim->x = x_in;
+    victim->y = y_out;
+    victim->T = T;
+    victim->ids = ids;
+    victim->w = w;
+    victim->last_use = m->graph_clock;
+    PG_CUDA(cudaGraphLaunch(victim->exec, s));
     return PGMOE_OK;
 }
 
