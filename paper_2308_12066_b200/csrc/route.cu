@@ -44,7 +44,8 @@ struct RouteParams {
     pgmoe_routing out;
     int *counter;      // workspace: select CTAs finished (reset by the last CTA)
     double *plogit;    // workspace: [splits][T][E]
-    float *pabs;       // workspace: [splits][T][E]
+    float *pcmax;      // workspace: [splits][E] column max |G| of each K slice (raw gates)
+    const float *gcolmax;  // prepared gates: column max |G| over all rows (else nullptr)
 };
 
 __device__ __forceinline__ bool better(double fa, int ia, double fb, int ib) {
@@ -76,47 +77,67 @@ __device__ __forceinline__ double warp_sumd(double v) {
     return v;
 }
 
-// Serial fp64 logit in the reference order (linalg.py:35-37): out += x_i*G_ij.
-template <typename WT>
-__device__ double serial_logit(const float *x, const WT *G, int d, int E, int j) {
-    double acc = 0.0;
-    for (int i = 0; i < d; ++i) {
-        double g = (double)WTraits<WT>::f32(G[(size_t)i * E + j]);
-        acc = __dadd_rn(acc, __dmul_rn((double)x[i], g));
-    }
-    return acc;
-}
 
-template <typename WT> struct Vec;
+// Gate row loads of V adjacent experts as exact doubles (+ |g| for the
+// column max of raw gates).  Prepared gates are already fp64.
+template <typename GT> struct Vec;
 template <> struct Vec<uint16_t> {
     static constexpr int N = 8;
-    __device__ __forceinline__ static void load(const uint16_t *p, float (&o)[8]) {
+    static constexpr bool kRaw = true;
+    __device__ __forceinline__ static void load(const uint16_t *p, double (&d)[8], float (&a)[8]) {
         const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            o[2 * i] = __uint_as_float(w[i] << 16);
-            o[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+            const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xffff0000u);
+            d[2 * i] = lo; d[2 * i + 1] = hi;
+            a[2 * i] = fabsf(lo); a[2 * i + 1] = fabsf(hi);
         }
     }
+    __device__ __forceinline__ static double one(const uint16_t *p) { return bf16_to_f32(__ldg(p)); }
 };
 template <> struct Vec<float> {
     static constexpr int N = 4;
-    __device__ __forceinline__ static void load(const float *p, float (&o)[4]) {
+    static constexpr bool kRaw = true;
+    __device__ __forceinline__ static void load(const float *p, double (&d)[4], float (&a)[4]) {
         const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
-        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+        a[0] = fabsf(v.x); a[1] = fabsf(v.y); a[2] = fabsf(v.z); a[3] = fabsf(v.w);
     }
+    __device__ __forceinline__ static double one(const float *p) { return __ldg(p); }
 };
+template <> struct Vec<double> {
+    static constexpr int N = 4;
+    static constexpr bool kRaw = false;
+    __device__ __forceinline__ static void load(const double *p, double (&d)[4], float (&)[4]) {
+        const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+        const double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+        d[0] = a.x; d[1] = a.y; d[2] = b.x; d[3] = b.y;
+    }
+    __device__ __forceinline__ static double one(const double *p) { return __ldg(p); }
+};
+template <typename GT> __device__ __forceinline__ double gval(const GT *G, size_t i) { return Vec<GT>::one(G + i); }
+
+// Serial fp64 logit in the reference order (linalg.py:35-37): out += x_i*G_ij.
+template <typename GT>
+__device__ double serial_logit(const float *x, const GT *G, int d, int E, int j) {
+    double acc = 0.0;
+    for (int i = 0; i < d; ++i) acc = __dadd_rn(acc, __dmul_rn((double)x[i], gval(G, (size_t)i * E + j)));
+    return acc;
+}
 
 // Partial logits of TOK tokens over the CTA's K range; expert columns in
-// groups of V (16-byte gate loads when VECLOAD).
-template <typename WT, int TOK, bool VECLOAD>
+// groups of V (16/32-byte gate loads when VECLOAD).  Products of fp32
+// activations and fp32/bf16 gate values are exact in fp64, so every DFMA
+// rounds once, like one step of the reference's serial sum.
+template <typename GT, int TOK, bool VECLOAD>
 __global__ void __launch_bounds__(kLogitThreads)
 route_logits_kernel(RouteParams p) {
-    constexpr int V = Vec<WT>::N;
+    constexpr int V = Vec<GT>::N;
+    constexpr bool kRaw = Vec<GT>::kRaw;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int d = p.d, E = p.E;
-    const WT *G = static_cast<const WT *>(p.G);
+    const GT *G = static_cast<const GT *>(p.G);
     const int t0 = blockIdx.x * TOK;
     const int ntok = min(TOK, p.T - t0);
     const int split = blockIdx.y;
@@ -127,84 +148,77 @@ route_logits_kernel(RouteParams p) {
     const int tid = threadIdx.x;
     const int cg = tid % CG, rg = tid / CG;
 
-    double *xd = reinterpret_cast<double *>(smem_raw);            // [TOK][kn]
-    float *xf = reinterpret_cast<float *>(xd + (size_t)TOK * kn);  // [TOK][kn]
-    double *red = reinterpret_cast<double *>(smem_raw);            // reuse: [RG][TOK][E] f64
-    float *reda = reinterpret_cast<float *>(red + (size_t)RG * TOK * E);  // [RG][TOK][E] f32
+    double *xd = reinterpret_cast<double *>(smem_raw);                    // [TOK][kn]
+    double *red = reinterpret_cast<double *>(smem_raw);                   // reuse: [RG][TOK][E]
+    float *redm = reinterpret_cast<float *>(red + (size_t)RG * TOK * E);  // [RG][E] (raw gates)
 
     pdl_wait();  // x is produced by the previous kernel in the stream
     pdl_trigger();
     for (int i = tid; i < TOK * kn; i += kLogitThreads) {
         const int t = i / kn;
-        const float v = (t < ntok) ? __ldg(p.x + (size_t)(t0 + t) * d + k0 + (i - t * kn)) : 0.f;
-        xd[i] = (double)v;
-        xf[i] = fabsf(v);
+        xd[i] = (t < ntok) ? (double)__ldg(p.x + (size_t)(t0 + t) * d + k0 + (i - t * kn)) : 0.0;
     }
     __syncthreads();
 
     double acc[TOK][V];
-    float aab[TOK][V];
+    float cmax[V];
 #pragma unroll
-    for (int t = 0; t < TOK; ++t)
+    for (int v = 0; v < V; ++v) {
+        cmax[v] = 0.f;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            acc[t][v] = 0.0;
-            aab[t][v] = 0.f;
-        }
+        for (int t = 0; t < TOK; ++t) acc[t][v] = 0.0;
+    }
     const int j0 = cg * V;
     if (rg < RG && cg < CG) {
 #pragma unroll 2
         for (int i = rg; i < kn; i += RG) {
-            float g[V];
-            const WT *row = G + (size_t)(k0 + i) * E;
-            if (VECLOAD) {
-                Vec<WT>::load(row + j0, g);
-            } else {
-#pragma unroll
-                for (int v = 0; v < V; ++v) g[v] = (j0 + v < E) ? WTraits<WT>::f32(__ldg(row + j0 + v)) : 0.f;
-            }
             double gd[V];
             float ga[V];
+            const GT *row = G + (size_t)(k0 + i) * E;
+            if (VECLOAD) {
+                Vec<GT>::load(row + j0, gd, ga);
+            } else {
 #pragma unroll
-            for (int v = 0; v < V; ++v) {
-                gd[v] = (double)g[v];
-                ga[v] = fabsf(g[v]);
+                for (int v = 0; v < V; ++v) {
+                    gd[v] = (j0 + v < E) ? gval(row, j0 + v) : 0.0;
+                    ga[v] = fabsf((float)gd[v]);
+                }
+            }
+            if (kRaw) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) cmax[v] = fmaxf(cmax[v], ga[v]);
             }
 #pragma unroll
             for (int t = 0; t < TOK; ++t) {
                 const double xv = xd[t * kn + i];
-                const float xa = xf[t * kn + i];
 #pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    acc[t][v] = fma(xv, gd[v], acc[t][v]);  // exact product: one rounding per add
-                    aab[t][v] = fmaf(xa, ga[v], aab[t][v]);
-                }
+                for (int v = 0; v < V; ++v) acc[t][v] = fma(xv, gd[v], acc[t][v]);
             }
         }
     }
     __syncthreads();  // x tile no longer needed: reuse smem for the reduction
     if (rg < RG && cg < CG) {
 #pragma unroll
-        for (int t = 0; t < TOK; ++t)
+        for (int v = 0; v < V; ++v)
+            if (j0 + v < E) {
 #pragma unroll
-            for (int v = 0; v < V; ++v)
-                if (j0 + v < E) {
-                    red[((size_t)rg * TOK + t) * E + j0 + v] = acc[t][v];
-                    reda[((size_t)rg * TOK + t) * E + j0 + v] = aab[t][v];
-                }
+                for (int t = 0; t < TOK; ++t) red[((size_t)rg * TOK + t) * E + j0 + v] = acc[t][v];
+                if (kRaw) redm[(size_t)rg * E + j0 + v] = cmax[v];
+            }
     }
     __syncthreads();
     for (int q = tid; q < ntok * E; q += kLogitThreads) {
         const int t = q / E, j = q - t * E;
         double s = 0.0;
-        float a = 0.f;
-        for (int r = 0; r < RG; ++r) {  // fixed order: deterministic
-            s += red[((size_t)r * TOK + t) * E + j];
-            a += reda[((size_t)r * TOK + t) * E + j];
+        for (int r = 0; r < RG; ++r) s += red[((size_t)r * TOK + t) * E + j];  // fixed order
+        p.plogit[((size_t)split * p.T + t0 + t) * E + j] = s;
+    }
+    if (kRaw && blockIdx.x == 0) {
+        for (int j = tid; j < E; j += kLogitThreads) {
+            float m = 0.f;
+            for (int r = 0; r < RG; ++r) m = fmaxf(m, redm[(size_t)r * E + j]);
+            p.pcmax[(size_t)split * E + j] = m;
         }
-        const size_t o = ((size_t)split * p.T + t0 + t) * E + j;
-        p.plogit[o] = s;
-        p.pabs[o] = a;
     }
 }
 
@@ -222,25 +236,28 @@ route_select_kernel(RouteParams p) {
     pdl_trigger();
     const double u = 1.1102230246251565e-16;  // 2^-53
     const double gam = (double)d * u / (1.0 - (double)d * u);
-    // fp32 |p| terms round by <= 2^-24 each (d of them) and may flush below
-    // FLT_MIN: pad relatively (1.001) and absolutely (d * 2 * FLT_MIN).
     const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
-    const double bpad = (double)d * 2.4e-38;
+    const double bpad = 1e-300;  // products are exact in fp64: no underflow below ~1e-90
 
     const int tok = blockIdx.x * kSelectWarps + warp;
     if (tok < p.T) {
         double *lg = logit;
         double *bd = bound;
+        // sum_i |x_i G_ij| <= (sum_i |x_i|) * max_i |G_ij|
+        double xs = 0.0;
+        for (int i = lane; i < d; i += 32) xs += fabs((double)__ldg(p.x + (size_t)tok * d + i));
+        const double xsum = warp_sumd(xs) * (1.0 + 2.0 * gam);  // rounding of the fp64 |x| sum
         for (int j = lane; j < E; j += 32) {
             double s = 0.0;
-            float a = 0.f;
-            for (int z = 0; z < p.splits; ++z) {  // fixed order: deterministic
-                const size_t o = ((size_t)z * p.T + tok) * E + j;
-                s += p.plogit[o];
-                a += p.pabs[o];
+            for (int z = 0; z < p.splits; ++z) s += p.plogit[((size_t)z * p.T + tok) * E + j];  // fixed order
+            float cm = 0.f;
+            if (p.gcolmax) {
+                cm = __ldg(p.gcolmax + j);
+            } else {
+                for (int z = 0; z < p.splits; ++z) cm = fmaxf(cm, p.pcmax[(size_t)z * E + j]);
             }
             lg[j] = s;
-            bd[j] = bscale * (double)a + bpad;
+            bd[j] = bscale * xsum * (double)cm + bpad;
         }
         __syncwarp();
         // finite check (core.py:297)
@@ -402,31 +419,38 @@ route_select_kernel(RouteParams p) {
     if (tid == 0) *p.counter = 0;
 }
 
-static int pick_tok(int T) { return T <= kNumSMs ? 1 : (T <= 2 * kNumSMs ? 2 : 4); }
+static int pick_tok(int T, bool prepared) {
+    if (T <= kNumSMs) return 1;
+    if (T <= 2 * kNumSMs) return 2;
+    if (T <= 4 * kNumSMs || !prepared) return 4;
+    return 8;
+}
 
 static int pick_splits(int T, int d, int tok) {
     const int tiles = (T + tok - 1) / tok;
     int s = std::max(1, (2 * kNumSMs) / std::max(1, tiles));
     s = std::min(s, std::max(1, d / 32));  // at least 32 gate rows per CTA
-    s = std::max(s, (int)(((size_t)d * tok * 12 + 131071) / 131072));  // x tile fits in shared memory
+    s = std::max(s, (int)(((size_t)d * tok * 8 + 131071) / 131072));  // x tile fits in shared memory
     return std::min(s, kMaxSplits);
 }
 
-static size_t logits_smem(int tok, int d, int splits, int E, int V) {
+template <typename GT>
+static size_t logits_smem(int tok, int d, int splits, int E) {
+    constexpr int V = Vec<GT>::N;
     const int kn = (d + splits - 1) / splits;
     const int CG = (E + V - 1) / V, RG = std::max(1, kLogitThreads / CG);
-    const size_t a = (size_t)tok * kn * 12;
-    const size_t b = (size_t)RG * tok * E * 12;
+    const size_t a = (size_t)tok * kn * 8;
+    const size_t b = (size_t)RG * tok * E * 8 + (Vec<GT>::kRaw ? (size_t)RG * E * 4 : 0);
     return std::max(a, b);
 }
 
-template <typename WT, int TOK>
+template <typename GT, int TOK>
 static int launch_logits(const RouteParams &p, cudaStream_t s) {
-    constexpr int V = Vec<WT>::N;
-    const size_t smem = logits_smem(TOK, p.d, p.splits, p.E, V);
+    constexpr int V = Vec<GT>::N;
+    const size_t smem = logits_smem<GT>(TOK, p.d, p.splits, p.E);
     PG_REQUIRE(smem <= 200 * 1024, PGMOE_E_CONFIG, "route: d=%d E=%d exceeds shared memory", p.d, p.E);
     const bool vec = (p.E % V == 0) && (reinterpret_cast<uintptr_t>(p.G) % 16 == 0);
-    auto kern = vec ? route_logits_kernel<WT, TOK, true> : route_logits_kernel<WT, TOK, false>;
+    auto kern = vec ? route_logits_kernel<GT, TOK, true> : route_logits_kernel<GT, TOK, false>;
     static size_t attr[2] = {0, 0};
     if (smem > attr[vec]) {
         const size_t want = std::max<size_t>(smem, 64 * 1024);
@@ -439,37 +463,72 @@ static int launch_logits(const RouteParams &p, cudaStream_t s) {
     return PGMOE_OK;
 }
 
-template <typename WT>
+template <typename GT>
 static int route_dispatch(RouteParams p, cudaStream_t s) {
     int st;
-    if (p.tok == 1) st = launch_logits<WT, 1>(p, s);
-    else if (p.tok == 2) st = launch_logits<WT, 2>(p, s);
-    else st = launch_logits<WT, 4>(p, s);
+    if (p.tok == 1) st = launch_logits<GT, 1>(p, s);
+    else if (p.tok == 2) st = launch_logits<GT, 2>(p, s);
+    else if (p.tok == 4) st = launch_logits<GT, 4>(p, s);
+    else st = launch_logits<double, 8>(p, s);  // only prepared gates use 8 tokens per CTA
     if (st != PGMOE_OK) return st;
     const size_t smem = std::max<size_t>((size_t)kSelectWarps * p.E * 16, (size_t)(kSelectWarps + 1) * p.E * 4);
     static size_t attr = 0;
     if (smem > attr) {
         const size_t want = std::max<size_t>(smem, 64 * 1024);
-        PG_CUDA(cudaFuncSetAttribute(route_select_kernel<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want));
+        PG_CUDA(cudaFuncSetAttribute(route_select_kernel<GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want));
         attr = want;
     }
     const int grid = (p.T + kSelectWarps - 1) / kSelectWarps;
-    PG_CUDA(launch_pdl(route_select_kernel<WT>, dim3(grid), dim3(kSelectThreads), smem, s, p));
+    PG_CUDA(launch_pdl(route_select_kernel<GT>, dim3(grid), dim3(kSelectThreads), smem, s, p));
     count_launch();
     return PGMOE_OK;
+}
+
+// Prepared gate: exact fp64 copy [d][E] then the column max |G| [E] (fp32).
+__global__ void prepare_gate_kernel(const void *g, int wdtype, int d, int E, double *out, float *colmax) {
+    const long long n = (long long)d * E;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = wdtype == PGMOE_BF16 ? (double)bf16_to_f32(static_cast<const uint16_t *>(g)[i])
+                                      : (double)static_cast<const float *>(g)[i];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < E; j += gridDim.x * blockDim.x) {
+        float m = 0.f;
+        for (int i = 0; i < d; ++i) {
+            const size_t o = (size_t)i * E + j;
+            const float v = wdtype == PGMOE_BF16 ? bf16_to_f32(static_cast<const uint16_t *>(g)[o])
+                                                 : static_cast<const float *>(g)[o];
+            m = fmaxf(m, fabsf(v));
+        }
+        colmax[j] = m;
+    }
 }
 
 }  // namespace pgmoe
 
 using namespace pgmoe;
 
-// workspace: [counter | pad to 256 B | plogit f64 [S][T][E] | pabs f32 [S][T][E]]
+// workspace: [counter | pad to 256 B | plogit f64 [S][T][E] | pcmax f32 [S][E]]
 extern "C" size_t pgmoe_route_workspace_bytes(int32_t T, int32_t E) {
     // the split count depends on the call's T (and d); size for the worst T' <= T
     size_t worst = 0;
     for (int t = 1; t <= std::max(T, 1); ++t)
-        worst = std::max(worst, (size_t)pick_splits(t, 1 << 20, pick_tok(t)) * t);
+        for (int prep = 0; prep < 2; ++prep)
+            worst = std::max(worst, (size_t)pick_splits(t, 1 << 20, pick_tok(t, prep)) * (t + 1));
     return 256 + worst * std::max(E, 1) * 12;
+}
+
+extern "C" size_t pgmoe_gate_prepared_bytes(int32_t d, int32_t E) {
+    return (((size_t)d * E * 8 + 15) & ~(size_t)15) + (size_t)E * 4;
+}
+
+extern "C" int pgmoe_gate_prepare(const void *gate_w, int32_t wdtype, int32_t d, int32_t E, void *out,
+                                  pgmoe_stream_t stream) {
+    PG_REQUIRE(wdtype == PGMOE_F32 || wdtype == PGMOE_BF16, PGMOE_E_CONFIG, "gate_prepare: bad dtype %d", wdtype);
+    double *g64 = static_cast<double *>(out);
+    float *cm = reinterpret_cast<float *>(static_cast<char *>(out) + (((size_t)d * E * 8 + 15) & ~(size_t)15));
+    prepare_gate_kernel<<<kNumSMs, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(gate_w, wdtype, d, E, g64, cm);
+    PG_CUDA(cudaGetLastError());
+    count_launch();
+    return PGMOE_OK;
 }
 
 extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const void *gate_w,
@@ -488,6 +547,7 @@ extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const vo
         PG_CUDA(cudaMemsetAsync(out->n_act, 0, sizeof(int32_t), s));
         return PGMOE_OK;
     }
+    const bool prepared = wdtype == PGMOE_GATE_F64;
     char *ws = static_cast<char *>(workspace);
     RouteParams p{};
     p.x = x;
@@ -497,12 +557,16 @@ extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const vo
     p.E = E;
     p.k = k;
     p.out = *out;
-    p.tok = pick_tok(T);
+    p.tok = pick_tok(T, prepared);
     p.splits = pick_splits(T, d, p.tok);
     p.counter = reinterpret_cast<int *>(ws);
     const size_t n = (size_t)p.splits * T * E;
     p.plogit = reinterpret_cast<double *>(ws + 256);
-    p.pabs = reinterpret_cast<float *>(ws + 256 + n * 8);
+    p.pcmax = reinterpret_cast<float *>(ws + 256 + n * 8);
+    p.gcolmax = prepared ? reinterpret_cast<const float *>(static_cast<const char *>(gate_w) +
+                                                           (((size_t)d * E * 8 + 15) & ~(size_t)15))
+                         : nullptr;
+    if (prepared) return route_dispatch<double>(p, s);
     if (wdtype == PGMOE_BF16) return route_dispatch<uint16_t>(p, s);
     if (wdtype == PGMOE_F32) return route_dispatch<float>(p, s);
     set_error("unknown weight dtype %d", wdtype);
