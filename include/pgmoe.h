@@ -51,9 +51,7 @@ typedef enum {
     PGMOE_E_INVARIANT = 10       /* InvariantError       (scheduler.py:127-145) */
 } pgmoe_status;
 
-/* PGMOE_GATE_F64: a gate prepared by pgmoe_gate_prepare (exact fp64 copy +
- * column max), accepted by pgmoe_gate_forward only. */
-typedef enum { PGMOE_F32 = 0, PGMOE_BF16 = 1, PGMOE_GATE_F64 = 2 } pgmoe_dtype;
+typedef enum { PGMOE_F32 = 0, PGMOE_BF16 = 1 } pgmoe_dtype;
 typedef enum { PGMOE_RESIDENT = 0, PGMOE_OFFLOADED = 1 } pgmoe_placement;
 typedef enum { PGMOE_KERNEL_AUTO = 0, PGMOE_KERNEL_SIMT = 1, PGMOE_KERNEL_TCGEN05 = 2 } pgmoe_kernel;
 
@@ -93,13 +91,6 @@ PGMOE_API size_t pgmoe_route_workspace_bytes(int32_t T, int32_t E);
 PGMOE_API int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const void *gate_w,
                        int32_t wdtype, int32_t E, int32_t k, const pgmoe_routing *out,
                        void *workspace, pgmoe_stream_t stream);
-
-/* Gate preparation for K1 (done once per gate matrix, e.g. at load): an
- * exact fp64 copy [d][E] followed by the per-column max |G| [E] (fp32) that
- * bounds the logit error.  `out` holds pgmoe_gate_prepared_bytes(d, E). */
-PGMOE_API size_t pgmoe_gate_prepared_bytes(int32_t d, int32_t E);
-PGMOE_API int pgmoe_gate_prepare(const void *gate_w, int32_t wdtype, int32_t d, int32_t E, void *out,
-                                 pgmoe_stream_t stream);
 
 /* K2 grouped expert FFN with fused combine.  Replaces expert_forward
  * (core.py:308-316) x k plus weighted_sum (linalg.py:45-51): for every

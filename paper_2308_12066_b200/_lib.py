@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "_build", "libpgmoe.so")
 
 OK, E_CONFIG, E_SHAPE, E_GATE_OVERFLOW, E_GATE_UNDERFLOW, E_ROUTING, E_OOM, E_CUDA, E_NCCL, \
     E_WEIGHT_FILE, E_INVARIANT = range(11)
-F32, BF16, GATE_F64 = 0, 1, 2
+F32, BF16 = 0, 1
 RESIDENT, OFFLOADED = 0, 1
 KERNEL_AUTO, KERNEL_SIMT, KERNEL_TCGEN05 = 0, 1, 2
 
@@ -62,7 +62,7 @@ EXPORTS = (
     "pgmoe_moe_block_forward", "pgmoe_model_matrix_ptr", "pgmoe_model_stats", "pgmoe_model_reset_stats",
     "pgmoe_model_timeline_jsonl", "pgmoe_model_set_timeline", "pgmoe_last_error", "pgmoe_version",
     "pgmoe_launch_count", "pgmoe_model_create_ex", "pgmoe_model_expert_records", "pgmoe_gather_rows",
-    "pgmoe_unpermute_combine", "pgmoe_ep_local_routing", "pgmoe_gate_prepared_bytes", "pgmoe_gate_prepare",
+    "pgmoe_unpermute_combine", "pgmoe_ep_local_routing",
 )
 
 _lib = None
@@ -109,8 +109,6 @@ def load():
         "pgmoe_gather_rows": (i32, [vp, vp, i32, i32, i32, vp, vp]),
         "pgmoe_unpermute_combine": (i32, [vp, vp, vp, i32, i32, vp, vp]),
         "pgmoe_ep_local_routing": (i32, [vp, i32, i32, P(Routing), vp]),
-        "pgmoe_gate_prepared_bytes": (sz, [i32, i32]),
-        "pgmoe_gate_prepare": (i32, [vp, i32, i32, i32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -45,7 +45,6 @@ struct RouteParams {
     int *counter;      // workspace: select CTAs finished (reset by the last CTA)
     double *plogit;    // workspace: [splits][T][E]
     float *pcmax;      // workspace: [splits][E] column max |G| of each K slice (raw gates)
-    const float *gcolmax;  // prepared gates: column max |G| over all rows (else nullptr)
 };
 
 __device__ __forceinline__ bool better(double fa, int ia, double fb, int ib) {
@@ -79,42 +78,30 @@ __device__ __forceinline__ double warp_sumd(double v) {
 
 
 // Gate row loads of V adjacent experts as exact doubles (+ |g| for the
-// column max of raw gates).  Prepared gates are already fp64.
+// column max that bounds the logit error).
 template <typename GT> struct Vec;
 template <> struct Vec<uint16_t> {
-    static constexpr int N = 8;
-    static constexpr bool kRaw = true;
-    __device__ __forceinline__ static void load(const uint16_t *p, double (&d)[8], float (&a)[8]) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    static constexpr int N = 4;
+    __device__ __forceinline__ static void load(const uint16_t *p, double (&d)[4], float (&a)[4]) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+        const float f[4] = {__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                            __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u)};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xffff0000u);
-            d[2 * i] = lo; d[2 * i + 1] = hi;
-            a[2 * i] = fabsf(lo); a[2 * i + 1] = fabsf(hi);
+            d[i] = f[i];
+            a[i] = fabsf(f[i]);
         }
     }
     __device__ __forceinline__ static double one(const uint16_t *p) { return bf16_to_f32(__ldg(p)); }
 };
 template <> struct Vec<float> {
     static constexpr int N = 4;
-    static constexpr bool kRaw = true;
     __device__ __forceinline__ static void load(const float *p, double (&d)[4], float (&a)[4]) {
         const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
         d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
         a[0] = fabsf(v.x); a[1] = fabsf(v.y); a[2] = fabsf(v.z); a[3] = fabsf(v.w);
     }
     __device__ __forceinline__ static double one(const float *p) { return __ldg(p); }
-};
-template <> struct Vec<double> {
-    static constexpr int N = 4;
-    static constexpr bool kRaw = false;
-    __device__ __forceinline__ static void load(const double *p, double (&d)[4], float (&)[4]) {
-        const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
-        const double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
-        d[0] = a.x; d[1] = a.y; d[2] = b.x; d[3] = b.y;
-    }
-    __device__ __forceinline__ static double one(const double *p) { return __ldg(p); }
 };
 template <typename GT> __device__ __forceinline__ double gval(const GT *G, size_t i) { return Vec<GT>::one(G + i); }
 
@@ -134,7 +121,6 @@ template <typename GT, int TOK, bool VECLOAD>
 __global__ void __launch_bounds__(kLogitThreads)
 route_logits_kernel(RouteParams p) {
     constexpr int V = Vec<GT>::N;
-    constexpr bool kRaw = Vec<GT>::kRaw;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int d = p.d, E = p.E;
     const GT *G = static_cast<const GT *>(p.G);
@@ -169,30 +155,38 @@ route_logits_kernel(RouteParams p) {
         for (int t = 0; t < TOK; ++t) acc[t][v] = 0.0;
     }
     const int j0 = cg * V;
+    constexpr int U = 4;  // gate rows in flight per thread
     if (rg < RG && cg < CG) {
-#pragma unroll 2
-        for (int i = rg; i < kn; i += RG) {
-            double gd[V];
-            float ga[V];
-            const GT *row = G + (size_t)(k0 + i) * E;
-            if (VECLOAD) {
-                Vec<GT>::load(row + j0, gd, ga);
-            } else {
+        for (int i = rg; i < kn; i += RG * U) {
+            double gd[U][V];
+            float ga[U][V];
 #pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    gd[v] = (j0 + v < E) ? gval(row, j0 + v) : 0.0;
-                    ga[v] = fabsf((float)gd[v]);
+            for (int u = 0; u < U; ++u) {
+                const int ii = i + u * RG;
+                const GT *row = G + (size_t)(k0 + min(ii, kn - 1)) * E;
+                if (VECLOAD) {
+                    Vec<GT>::load(row + j0, gd[u], ga[u]);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        gd[u][v] = (j0 + v < E) ? gval(row, j0 + v) : 0.0;
+                        ga[u][v] = fabsf((float)gd[u][v]);
+                    }
                 }
             }
-            if (kRaw) {
 #pragma unroll
-                for (int v = 0; v < V; ++v) cmax[v] = fmaxf(cmax[v], ga[v]);
-            }
+            for (int u = 0; u < U; ++u) {
+                const int ii = i + u * RG;
+                if (ii < kn) {
 #pragma unroll
-            for (int t = 0; t < TOK; ++t) {
-                const double xv = xd[t * kn + i];
+                    for (int v = 0; v < V; ++v) cmax[v] = fmaxf(cmax[v], ga[u][v]);
 #pragma unroll
-                for (int v = 0; v < V; ++v) acc[t][v] = fma(xv, gd[v], acc[t][v]);
+                    for (int t = 0; t < TOK; ++t) {
+                        const double xv = xd[t * kn + ii];
+#pragma unroll
+                        for (int v = 0; v < V; ++v) acc[t][v] = fma(xv, gd[u][v], acc[t][v]);
+                    }
+                }
             }
         }
     }
@@ -203,7 +197,7 @@ route_logits_kernel(RouteParams p) {
             if (j0 + v < E) {
 #pragma unroll
                 for (int t = 0; t < TOK; ++t) red[((size_t)rg * TOK + t) * E + j0 + v] = acc[t][v];
-                if (kRaw) redm[(size_t)rg * E + j0 + v] = cmax[v];
+                redm[(size_t)rg * E + j0 + v] = cmax[v];
             }
     }
     __syncthreads();
@@ -213,7 +207,7 @@ route_logits_kernel(RouteParams p) {
         for (int r = 0; r < RG; ++r) s += red[((size_t)r * TOK + t) * E + j];  // fixed order
         p.plogit[((size_t)split * p.T + t0 + t) * E + j] = s;
     }
-    if (kRaw && blockIdx.x == 0) {
+    if (blockIdx.x == 0) {
         for (int j = tid; j < E; j += kLogitThreads) {
             float m = 0.f;
             for (int r = 0; r < RG; ++r) m = fmaxf(m, redm[(size_t)r * E + j]);
@@ -245,17 +239,14 @@ route_select_kernel(RouteParams p) {
         double *bd = bound;
         // sum_i |x_i G_ij| <= (sum_i |x_i|) * max_i |G_ij|
         double xs = 0.0;
+#pragma unroll 8
         for (int i = lane; i < d; i += 32) xs += fabs((double)__ldg(p.x + (size_t)tok * d + i));
         const double xsum = warp_sumd(xs) * (1.0 + 2.0 * gam);  // rounding of the fp64 |x| sum
         for (int j = lane; j < E; j += 32) {
             double s = 0.0;
             for (int z = 0; z < p.splits; ++z) s += p.plogit[((size_t)z * p.T + tok) * E + j];  // fixed order
             float cm = 0.f;
-            if (p.gcolmax) {
-                cm = __ldg(p.gcolmax + j);
-            } else {
-                for (int z = 0; z < p.splits; ++z) cm = fmaxf(cm, p.pcmax[(size_t)z * E + j]);
-            }
+            for (int z = 0; z < p.splits; ++z) cm = fmaxf(cm, p.pcmax[(size_t)z * E + j]);
             lg[j] = s;
             bd[j] = bscale * xsum * (double)cm + bpad;
         }
@@ -419,10 +410,10 @@ route_select_kernel(RouteParams p) {
     if (tid == 0) *p.counter = 0;
 }
 
-static int pick_tok(int T, bool prepared) {
+static int pick_tok(int T) {
     if (T <= kNumSMs) return 1;
     if (T <= 2 * kNumSMs) return 2;
-    if (T <= 4 * kNumSMs || !prepared) return 4;
+    if (T <= 4 * kNumSMs) return 4;
     return 8;
 }
 
@@ -440,7 +431,7 @@ static size_t logits_smem(int tok, int d, int splits, int E) {
     const int kn = (d + splits - 1) / splits;
     const int CG = (E + V - 1) / V, RG = std::max(1, kLogitThreads / CG);
     const size_t a = (size_t)tok * kn * 8;
-    const size_t b = (size_t)RG * tok * E * 8 + (Vec<GT>::kRaw ? (size_t)RG * E * 4 : 0);
+    const size_t b = (size_t)RG * tok * E * 8 + (size_t)RG * E * 4;
     return std::max(a, b);
 }
 
@@ -469,7 +460,7 @@ static int route_dispatch(RouteParams p, cudaStream_t s) {
     if (p.tok == 1) st = launch_logits<GT, 1>(p, s);
     else if (p.tok == 2) st = launch_logits<GT, 2>(p, s);
     else if (p.tok == 4) st = launch_logits<GT, 4>(p, s);
-    else st = launch_logits<double, 8>(p, s);  // only prepared gates use 8 tokens per CTA
+    else st = launch_logits<GT, 8>(p, s);
     if (st != PGMOE_OK) return st;
     const size_t smem = std::max<size_t>((size_t)kSelectWarps * p.E * 16, (size_t)(kSelectWarps + 1) * p.E * 4);
     static size_t attr = 0;
@@ -484,24 +475,6 @@ static int route_dispatch(RouteParams p, cudaStream_t s) {
     return PGMOE_OK;
 }
 
-// Prepared gate: exact fp64 copy [d][E] then the column max |G| [E] (fp32).
-__global__ void prepare_gate_kernel(const void *g, int wdtype, int d, int E, double *out, float *colmax) {
-    const long long n = (long long)d * E;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        out[i] = wdtype == PGMOE_BF16 ? (double)bf16_to_f32(static_cast<const uint16_t *>(g)[i])
-                                      : (double)static_cast<const float *>(g)[i];
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < E; j += gridDim.x * blockDim.x) {
-        float m = 0.f;
-        for (int i = 0; i < d; ++i) {
-            const size_t o = (size_t)i * E + j;
-            const float v = wdtype == PGMOE_BF16 ? bf16_to_f32(static_cast<const uint16_t *>(g)[o])
-                                                 : static_cast<const float *>(g)[o];
-            m = fmaxf(m, fabsf(v));
-        }
-        colmax[j] = m;
-    }
-}
-
 }  // namespace pgmoe
 
 using namespace pgmoe;
@@ -511,24 +484,8 @@ extern "C" size_t pgmoe_route_workspace_bytes(int32_t T, int32_t E) {
     // the split count depends on the call's T (and d); size for the worst T' <= T
     size_t worst = 0;
     for (int t = 1; t <= std::max(T, 1); ++t)
-        for (int prep = 0; prep < 2; ++prep)
-            worst = std::max(worst, (size_t)pick_splits(t, 1 << 20, pick_tok(t, prep)) * (t + 1));
+        worst = std::max(worst, (size_t)pick_splits(t, 1 << 20, pick_tok(t)) * (t + 1));
     return 256 + worst * std::max(E, 1) * 12;
-}
-
-extern "C" size_t pgmoe_gate_prepared_bytes(int32_t d, int32_t E) {
-    return (((size_t)d * E * 8 + 15) & ~(size_t)15) + (size_t)E * 4;
-}
-
-extern "C" int pgmoe_gate_prepare(const void *gate_w, int32_t wdtype, int32_t d, int32_t E, void *out,
-                                  pgmoe_stream_t stream) {
-    PG_REQUIRE(wdtype == PGMOE_F32 || wdtype == PGMOE_BF16, PGMOE_E_CONFIG, "gate_prepare: bad dtype %d", wdtype);
-    double *g64 = static_cast<double *>(out);
-    float *cm = reinterpret_cast<float *>(static_cast<char *>(out) + (((size_t)d * E * 8 + 15) & ~(size_t)15));
-    prepare_gate_kernel<<<kNumSMs, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(gate_w, wdtype, d, E, g64, cm);
-    PG_CUDA(cudaGetLastError());
-    count_launch();
-    return PGMOE_OK;
 }
 
 extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const void *gate_w,
@@ -547,7 +504,6 @@ extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const vo
         PG_CUDA(cudaMemsetAsync(out->n_act, 0, sizeof(int32_t), s));
         return PGMOE_OK;
     }
-    const bool prepared = wdtype == PGMOE_GATE_F64;
     char *ws = static_cast<char *>(workspace);
     RouteParams p{};
     p.x = x;
@@ -557,16 +513,12 @@ extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const vo
     p.E = E;
     p.k = k;
     p.out = *out;
-    p.tok = pick_tok(T, prepared);
+    p.tok = pick_tok(T);
     p.splits = pick_splits(T, d, p.tok);
     p.counter = reinterpret_cast<int *>(ws);
     const size_t n = (size_t)p.splits * T * E;
     p.plogit = reinterpret_cast<double *>(ws + 256);
     p.pcmax = reinterpret_cast<float *>(ws + 256 + n * 8);
-    p.gcolmax = prepared ? reinterpret_cast<const float *>(static_cast<const char *>(gate_w) +
-                                                           (((size_t)d * E * 8 + 15) & ~(size_t)15))
-                         : nullptr;
-    if (prepared) return route_dispatch<double>(p, s);
     if (wdtype == PGMOE_BF16) return route_dispatch<uint16_t>(p, s);
     if (wdtype == PGMOE_F32) return route_dispatch<float>(p, s);
     set_error("unknown weight dtype %d", wdtype);

@@ -45,7 +45,6 @@ struct RoutingBuf {
 
 struct BlockW {
     void *gate = nullptr, *pre_gate = nullptr, *dense = nullptr;
-    void *gate64 = nullptr, *pre_gate64 = nullptr;  // prepared (fp64 + column max) copies for K1
     unsigned char *experts = nullptr;  // device (resident) or pinned host (offloaded)
 };
 
@@ -67,8 +66,6 @@ struct pgmoe_model {
     size_t sw = 2, gate_bytes = 0, dense_bytes = 0, w1_bytes = 0, rec_bytes = 0;
     std::vector<BlockW> blocks;
     unsigned char *dev_pool = nullptr;   // gates + dense (+ experts when resident)
-    unsigned char *gprep_pool = nullptr; // prepared gates
-    size_t gprep_bytes = 0;
     unsigned char *host_pool = nullptr;  // pinned experts (offloaded)
     size_t dev_pool_bytes = 0, host_pool_bytes = 0;
     // work buffers
@@ -184,18 +181,6 @@ static void *mat_ptr(pgmoe_model *m, const std::string &name, int b, int e, size
     return nullptr;
 }
 
-static int prepare_block_gates(pgmoe_model *m, int b, cudaStream_t s) {
-    const auto &c = m->cfg;
-    BlockW &bw = m->blocks[b];
-    if (bw.gate)
-        PG_TRY(pgmoe_gate_prepare(bw.gate, m->wdtype, c.d_model, c.num_experts, bw.gate64,
-                                  reinterpret_cast<pgmoe_stream_t>(s)));
-    if (bw.pre_gate)
-        PG_TRY(pgmoe_gate_prepare(bw.pre_gate, m->wdtype, c.d_model, c.num_experts, bw.pre_gate64,
-                                  reinterpret_cast<pgmoe_stream_t>(s)));
-    return PGMOE_OK;
-}
-
 int run_ffn(pgmoe_model *m, const float *x, int T, const void *experts, int indexed,
             const pgmoe_routing *r, cudaStream_t s) {
     const auto &c = m->cfg;
@@ -272,7 +257,7 @@ static int route_into(pgmoe_model *m, const float *x, int T, const void *G, int 
     const auto &c = m->cfg;
     RoutingBuf &rb = m->routing[ri];
     tl_begin(m, "compute", label, block, s);
-    PG_TRY(pgmoe_gate_forward(x, T, c.d_model, G, PGMOE_GATE_F64, c.num_experts, c.top_k, &rb.r, m->route_ws,
+    PG_TRY(pgmoe_gate_forward(x, T, c.d_model, G, m->wdtype, c.num_experts, c.top_k, &rb.r, m->route_ws,
                               reinterpret_cast<pgmoe_stream_t>(s)));
     tl_end(m, s);
     if (mirror) {
@@ -306,12 +291,12 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
         const int ri = b % R;
         int pending_fetch = -1;
         if (has_conv_gate(c, b)) {
-            PG_TRY(route_into(m, cur, T, bw.gate64, ri, off, s, "gate", b));
+            PG_TRY(route_into(m, cur, T, bw.gate, ri, off, s, "gate", b));
             if (off) PG_TRY(issue_fetch(m, b, ri));  // exposed serial fetch
         }
         if (has_pre_gate(c, b)) {
             const int tr = (b + L) % R;
-            PG_TRY(route_into(m, cur, T, bw.pre_gate64, tr, off, s, "pre_gate", b));
+            PG_TRY(route_into(m, cur, T, bw.pre_gate, tr, off, s, "pre_gate", b));
             if (off) pending_fetch = b + L;
         }
         const RoutingBuf &rb = m->routing[ri];
@@ -445,20 +430,6 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
         bw.dense = p;
         p += m->dense_bytes;
     }
-    {
-        m->gprep_bytes = (pgmoe_gate_prepared_bytes(c.d_model, c.num_experts) + 255) & ~size_t(255);
-        size_t ng = 0;
-        for (size_t b = 0; b < nb; ++b) ng += has_conv_gate(c, b) + has_pre_gate(c, b);
-        if (cudaMalloc(&m->gprep_pool, std::max<size_t>(ng, 1) * m->gprep_bytes) != cudaSuccess) {
-            set_error("OOM: prepared gates");
-            return fail(PGMOE_E_OOM);
-        }
-        unsigned char *q = m->gprep_pool;
-        for (size_t b = 0; b < nb; ++b) {
-            if (has_conv_gate(c, b)) { m->blocks[b].gate64 = q; q += m->gprep_bytes; }
-            if (has_pre_gate(c, b)) { m->blocks[b].pre_gate64 = q; q += m->gprep_bytes; }
-        }
-    }
     if (placement == PGMOE_RESIDENT) {
         for (size_t b = 0; b < nb; ++b) { m->blocks[b].experts = p; p += E * m->rec_bytes; }
     } else {
@@ -541,7 +512,6 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     if (m->cap) cudaStreamDestroy(m->cap);
     if (m->copy) cudaStreamDestroy(m->copy);
     cudaFree(m->dev_pool);
-    cudaFree(m->gprep_pool);
     if (m->host_pool) cudaFreeHost(m->host_pool);
     cudaFree(m->slots);
     cudaFree(m->route_ws);
@@ -596,8 +566,6 @@ extern "C" int pgmoe_model_init_weights(pgmoe_model *m) {
         return PGMOE_OK;
     };
     int st = run(jobs);
-    for (int b = 0; b < nb && st == PGMOE_OK; ++b) st = prepare_block_gates(m, b, s);
-    if (st == PGMOE_OK) st = cudaStreamSynchronize(s) == cudaSuccess ? PGMOE_OK : PGMOE_E_CUDA;
     if (st == PGMOE_OK && !off) {
         std::vector<GenJob> ej;
         for (int b = 0; b < nb; ++b)
@@ -644,10 +612,6 @@ extern "C" int pgmoe_model_set_matrix(pgmoe_model *m, const char *name, int32_t 
     PG_REQUIRE(nbytes == want, PGMOE_E_SHAPE, "matrix %s expects %zu bytes, got %zu", name, want, nbytes);
     if (on_host) memcpy(dst, host_data, nbytes);
     else PG_CUDA(cudaMemcpy(dst, host_data, nbytes, cudaMemcpyHostToDevice));
-    if (std::string(name) == "gate" || std::string(name) == "pre_gate") {
-        PG_TRY(prepare_block_gates(m, block, nullptr));
-        PG_CUDA(cudaDeviceSynchronize());
-    }
     return PGMOE_OK;
 }
 
@@ -787,7 +751,7 @@ extern "C" int pgmoe_moe_block_forward(pgmoe_model *m, int32_t block, const floa
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const BlockW &bw = m->blocks[block];
     if (r_out && has_pre_gate(c, block))
-        PG_TRY(pgmoe_gate_forward(x, T, c.d_model, bw.pre_gate64, PGMOE_GATE_F64, c.num_experts, c.top_k, r_out,
+        PG_TRY(pgmoe_gate_forward(x, T, c.d_model, bw.pre_gate, m->wdtype, c.num_experts, c.top_k, r_out,
                                   m->route_ws, stream));
     PG_REQUIRE(r_in != nullptr, PGMOE_E_ROUTING, "no routing decision available");
     if (T == 0) return PGMOE_OK;
