@@ -207,8 +207,9 @@ def run_ours(args, rank: int, world: int):
         if world > 1:
             torch.distributed.barrier()
 
+    y_buf = torch.empty_like(x)
     for _ in range(args.warmup):
-        model.decoder_iteration(x)
+        model.decoder_iteration(x, out=y_buf)
     torch.cuda.synchronize()
 
     # ---- timed region: device-resident inputs (resident: CUDA-graph replay) --
@@ -222,7 +223,7 @@ def run_ours(args, rank: int, world: int):
     ev0.record(stream)
     y = None
     for _ in range(args.steps):
-        y, _, _ = model.decoder_iteration(x)
+        y, _, _ = model.decoder_iteration(x, out=y_buf)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()

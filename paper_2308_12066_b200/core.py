@@ -347,15 +347,17 @@ class DeviceModel:
         return t.view(shape)
 
     # -- execution --
-    def decoder_iteration(self, x: torch.Tensor, trace: bool = False, stream=None):
+    def decoder_iteration(self, x: torch.Tensor, trace: bool = False, stream=None, out: torch.Tensor = None):
         """core.py:342-383 for T tokens (x: cuda fp32 [T][d]).
-        Returns (y, ids [nb][T][k], w [nb][T][k]) — trace tensors None unless asked."""
+        Returns (y, ids [nb][T][k], w [nb][T][k]) — trace tensors None unless asked.
+        Resident models replay a CUDA graph keyed by the buffer addresses, so
+        passing a persistent `out` keeps every call on the replay path."""
         c = self.config
         if x.dim() != 2 or x.shape[1] != c.d_model:
             raise ShapeError(f"expected [T][{c.d_model}] input, got {tuple(x.shape)}")
         T = x.shape[0]
         x = x.contiguous()
-        y = torch.empty_like(x)
+        y = out if out is not None else torch.empty_like(x)
         ids = w = None
         if trace:
             ids = torch.empty((c.num_blocks, T, c.top_k), dtype=torch.int32, device=x.device)

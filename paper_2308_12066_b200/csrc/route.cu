@@ -410,10 +410,12 @@ route_select_kernel(RouteParams p) {
     if (tid == 0) *p.counter = 0;
 }
 
+// Tokens per logits CTA: more tokens re-read each gate row fewer times;
+// K splits (up to d/32) keep the grid >= ~2 CTAs per SM at small T.
 static int pick_tok(int T) {
-    if (T <= kNumSMs) return 1;
-    if (T <= 2 * kNumSMs) return 2;
-    if (T <= 4 * kNumSMs) return 4;
+    if (T < 64) return 1;
+    if (T < 128) return 2;
+    if (T < 256) return 4;
     return 8;
 }
 
