@@ -182,6 +182,17 @@ PGMOE_API int pgmoe_model_set_matrix(pgmoe_model *m, const char *name, int32_t b
 PGMOE_API int pgmoe_model_get_matrix(pgmoe_model *m, const char *name, int32_t block, int32_t expert,
                            void *host_data, size_t nbytes);
 
+/* The model's configuration and weight dtype. */
+PGMOE_API int pgmoe_model_config(pgmoe_model *m, pgmoe_config *cfg, int32_t *wdtype);
+
+/* PGMOE1 weight files (model_io.py:1-105): header-only read (no GPU needed),
+ * load into a model of matching dimensions (fp32 file -> model dtype, RNE for
+ * bf16; expert-parallel shards keep their own experts), and save (fp32).
+ * Malformed files return PGMOE_E_WEIGHT_FILE with the reference's messages. */
+PGMOE_API int pgmoe_weight_file_config(const char *path, pgmoe_config *out);
+PGMOE_API int pgmoe_model_load_pgmoe1(pgmoe_model *m, const char *path);
+PGMOE_API int pgmoe_model_save_pgmoe1(pgmoe_model *m, const char *path);
+
 /* Kernel family for K2/K3 (AUTO: tcgen05 for bf16, SIMT for fp32). */
 PGMOE_API int pgmoe_model_set_kernel(pgmoe_model *m, int32_t kernel);
 

@@ -8,7 +8,7 @@ __version__ = "0.1.0"
 
 _CORE_NAMES = ("ModelConfig", "RoutingDecision", "DeviceModel", "DeviceRouting", "route", "expert_ffn",
                "dense", "fill_weights", "gate_forward", "expert_forward", "moe_block_forward",
-               "decoder_iteration", "token_inputs", "clear_cache")
+               "decoder_iteration", "token_inputs", "clear_cache", "weight_file_config")
 
 
 def __getattr__(name):  # torch is imported lazily so the package imports without it

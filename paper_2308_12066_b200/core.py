@@ -310,6 +310,19 @@ class DeviceModel:
         except Exception:
             pass
 
+    @classmethod
+    def load(cls, path: str, dtype: str = "bf16", placement: str = "resident", max_tokens: int = 256,
+             kernel: str = "auto", seed: int = 0) -> "DeviceModel":
+        """model_io.load_model (model_io.py:63-105): a PGMOE1 file into a new model."""
+        cfg = weight_file_config(path, seed=seed)
+        m = cls(cfg, dtype=dtype, placement=placement, max_tokens=max_tokens, kernel=kernel, init="none")
+        _lib.check(m._L.pgmoe_model_load_pgmoe1(m._h, str(path).encode()))
+        return m
+
+    def save(self, path: str) -> None:
+        """model_io.save_model (model_io.py:39-60): fp32 PGMOE1 file."""
+        _lib.check(self._L.pgmoe_model_save_pgmoe1(self._h, str(path).encode()))
+
     def set_kernel(self, kernel: str) -> None:
         _lib.check(self._L.pgmoe_model_set_kernel(self._h, _KERNEL[kernel]))
 
@@ -413,6 +426,14 @@ class DeviceModel:
         buf = ctypes.create_string_buffer(int(n) + 1)
         self._L.pgmoe_model_timeline_jsonl(self._h, buf, n + 1)
         return [json.loads(line) for line in buf.value.decode().splitlines() if line]
+
+
+def weight_file_config(path: str, seed: int = 0) -> ModelConfig:
+    """Header of a PGMOE1 file (model_io.py:20-21, :70-86) as a ModelConfig."""
+    c = _lib.Config()
+    _lib.check(_lib.load().pgmoe_weight_file_config(str(path).encode(), ctypes.byref(c)))
+    return ModelConfig(d_model=c.d_model, d_ff=c.d_ff, num_blocks=c.num_blocks, num_experts=c.num_experts,
+                       top_k=c.top_k, activation_level=c.activation_level, seed=seed)
 
 
 def _wrap_device_ptr(ptr: int, numel: int, dtype: torch.dtype) -> torch.Tensor:

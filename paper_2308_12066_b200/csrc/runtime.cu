@@ -527,6 +527,13 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     return PGMOE_OK;
 }
 
+extern "C" int pgmoe_model_config(pgmoe_model *m, pgmoe_config *cfg, int32_t *wdtype) {
+    PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
+    if (cfg) *cfg = m->cfg;
+    if (wdtype) *wdtype = m->wdtype;
+    return PGMOE_OK;
+}
+
 extern "C" int pgmoe_model_set_kernel(pgmoe_model *m, int32_t kernel) {
     PG_REQUIRE(kernel >= PGMOE_KERNEL_AUTO && kernel <= PGMOE_KERNEL_TCGEN05, PGMOE_E_CONFIG, "bad kernel %d", kernel);
     m->kernel = kernel;

@@ -212,7 +212,15 @@ def switch_fixture():
     return out
 
 
+def pgmoe1_fixture():
+    """A PGMOE1 file written by the reference's own save_model (model_io.py:39-60)."""
+    from moesim.model_io import save_model
+    cfg = moesim.ModelConfig(d_model=16, d_ff=24, num_blocks=3, num_experts=4, top_k=1, seed=11)
+    save_model(mcore.init_model(cfg), os.path.join(HERE, "small_d16_f24_b3_e4.pgmoe1"))
+
+
 def main():
+    pgmoe1_fixture()
     fixtures = {
         "rng.json": rng_fixture,
         "linalg.json": linalg_fixture,
