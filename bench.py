@@ -283,6 +283,9 @@ def run_ours(args, rank: int, world: int):
     # ---- end-to-end through the C ABI with host buffers -----------------
     y_host = torch.empty_like(x_host).pin_memory()
     e2e_steps = max(1, min(args.steps, 3))
+    # one untimed call: the host entry point's device buffers (and, resident,
+    # its CUDA graph) are created on first use
+    _lib.check(L.pgmoe_decoder_iteration_host(model._h, _ptr(x_host), T, _ptr(y_host), None, None))
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):

@@ -233,23 +233,38 @@ route_select_kernel(RouteParams p) {
     const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
     const double bpad = 1e-300;  // products are exact in fp64: no underflow below ~1e-90
 
-    const int tok = blockIdx.x * kSelectWarps + warp;
+    // (1) per-token sum|x| (warp t), (2) all threads reduce the K-split
+    // partials of the CTA's tokens in split order, (3) one warp per token
+    // certifies and selects.  sum_i |x_i G_ij| <= (sum_i |x_i|) max_i |G_ij|.
+    __shared__ double s_xsum[kSelectWarps];
+    const int tok0 = blockIdx.x * kSelectWarps;
+    const int ntok = min(kSelectWarps, p.T - tok0);
+    if (warp < ntok) {
+        double xs = 0.0;
+#pragma unroll 8
+        for (int i = lane; i < d; i += 32) xs += fabs((double)__ldg(p.x + (size_t)(tok0 + warp) * d + i));
+        xs = warp_sumd(xs);
+        if (lane == 0) s_xsum[warp] = xs * (1.0 + 2.0 * gam);  // rounding of the fp64 |x| sum
+    }
+    __syncthreads();
+    for (int q = tid; q < ntok * E; q += kSelectThreads) {
+        const int t = q / E, j = q - t * E;
+        double sum = 0.0;
+        float cm = 0.f;
+#pragma unroll 4
+        for (int z = 0; z < p.splits; ++z) {  // fixed order: deterministic
+            sum += __ldcg(p.plogit + ((size_t)z * p.T + tok0 + t) * E + j);
+            cm = fmaxf(cm, __ldcg(p.pcmax + (size_t)z * E + j));
+        }
+        double *lgt = reinterpret_cast<double *>(smem_raw) + (size_t)t * 2 * E;
+        lgt[j] = sum;
+        lgt[E + j] = bscale * s_xsum[t] * (double)cm + bpad;
+    }
+    __syncthreads();
+    const int tok = tok0 + warp;
     if (tok < p.T) {
         double *lg = logit;
         double *bd = bound;
-        // sum_i |x_i G_ij| <= (sum_i |x_i|) * max_i |G_ij|
-        double xs = 0.0;
-#pragma unroll 8
-        for (int i = lane; i < d; i += 32) xs += fabs((double)__ldg(p.x + (size_t)tok * d + i));
-        const double xsum = warp_sumd(xs) * (1.0 + 2.0 * gam);  // rounding of the fp64 |x| sum
-        for (int j = lane; j < E; j += 32) {
-            double s = 0.0;
-            for (int z = 0; z < p.splits; ++z) s += p.plogit[((size_t)z * p.T + tok) * E + j];  // fixed order
-            float cm = 0.f;
-            for (int z = 0; z < p.splits; ++z) cm = fmaxf(cm, p.pcmax[(size_t)z * E + j]);
-            lg[j] = s;
-            bd[j] = bscale * xsum * (double)cm + bpad;
-        }
         __syncwarp();
         // finite check (core.py:297)
         bool finite = true;
@@ -422,7 +437,8 @@ static int pick_tok(int T) {
 static int pick_splits(int T, int d, int tok) {
     const int tiles = (T + tok - 1) / tok;
     int s = std::max(1, (2 * kNumSMs) / std::max(1, tiles));
-    s = std::min(s, std::max(1, d / 32));  // at least 32 gate rows per CTA
+    s = std::min(s, std::max(1, d / 64));  // at least 64 gate rows per CTA
+    s = std::min(s, 16);                   // keeps the select kernel's split reduction short
     s = std::max(s, (int)(((size_t)d * tok * 8 + 131071) / 131072));  // x tile fits in shared memory
     return std::min(s, kMaxSplits);
 }
