@@ -54,6 +54,9 @@ typedef enum {
 typedef enum { PGMOE_F32 = 0, PGMOE_BF16 = 1 } pgmoe_dtype;
 typedef enum { PGMOE_RESIDENT = 0, PGMOE_OFFLOADED = 1 } pgmoe_placement;
 typedef enum { PGMOE_KERNEL_AUTO = 0, PGMOE_KERNEL_SIMT = 1, PGMOE_KERNEL_TCGEN05 = 2 } pgmoe_kernel;
+/* Expert migration policy of an offloaded model (scheduler.py:36-49).  The
+ * resident strategy is PGMOE_RESIDENT placement. */
+typedef enum { PGMOE_PRE_GATED = 0, PGMOE_ON_DEMAND = 1, PGMOE_PREFETCH_ALL = 2 } pgmoe_strategy;
 
 /* core.py:34-70 ModelConfig (dtype_bytes is implied by the weight dtype). */
 typedef struct {
@@ -192,6 +195,11 @@ PGMOE_API int pgmoe_model_config(pgmoe_model *m, pgmoe_config *cfg, int32_t *wdt
 PGMOE_API int pgmoe_weight_file_config(const char *path, pgmoe_config *out);
 PGMOE_API int pgmoe_model_load_pgmoe1(pgmoe_model *m, const char *path);
 PGMOE_API int pgmoe_model_save_pgmoe1(pgmoe_model *m, const char *path);
+
+/* Migration strategy of an offloaded model (default pre_gated).  Numerical
+ * outputs are identical under every strategy; only the copy schedule and
+ * the HBM footprint change (prefetch_all reserves two whole-block slots). */
+PGMOE_API int pgmoe_model_set_strategy(pgmoe_model *m, int32_t strategy);
 
 /* Kernel family for K2/K3 (AUTO: tcgen05 for bf16, SIMT for fp32). */
 PGMOE_API int pgmoe_model_set_kernel(pgmoe_model *m, int32_t kernel);

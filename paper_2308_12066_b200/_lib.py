@@ -63,7 +63,7 @@ EXPORTS = (
     "pgmoe_model_timeline_jsonl", "pgmoe_model_set_timeline", "pgmoe_last_error", "pgmoe_version",
     "pgmoe_launch_count", "pgmoe_model_create_ex", "pgmoe_model_expert_records", "pgmoe_gather_rows",
     "pgmoe_unpermute_combine", "pgmoe_ep_local_routing", "pgmoe_model_config", "pgmoe_weight_file_config",
-    "pgmoe_model_load_pgmoe1", "pgmoe_model_save_pgmoe1",
+    "pgmoe_model_load_pgmoe1", "pgmoe_model_save_pgmoe1", "pgmoe_model_set_strategy",
 )
 
 _lib = None
@@ -111,6 +111,7 @@ def load():
         "pgmoe_unpermute_combine": (i32, [vp, vp, vp, i32, i32, vp, vp]),
         "pgmoe_ep_local_routing": (i32, [vp, i32, i32, P(Routing), vp]),
         "pgmoe_model_config": (i32, [vp, P(Config), P(i32)]),
+        "pgmoe_model_set_strategy": (i32, [vp, i32]),
         "pgmoe_weight_file_config": (i32, [ctypes.c_char_p, P(Config)]),
         "pgmoe_model_load_pgmoe1": (i32, [vp, ctypes.c_char_p]),
         "pgmoe_model_save_pgmoe1": (i32, [vp, ctypes.c_char_p]),

@@ -323,6 +323,14 @@ class DeviceModel:
         """model_io.save_model (model_io.py:39-60): fp32 PGMOE1 file."""
         _lib.check(self._L.pgmoe_model_save_pgmoe1(self._h, str(path).encode()))
 
+    STRATEGIES = {"pre_gated": 0, "on_demand": 1, "prefetch_all": 2}
+
+    def set_strategy(self, strategy: str) -> None:
+        """Migration policy of an offloaded model (scheduler.py:36-49)."""
+        if strategy not in self.STRATEGIES:
+            raise ConfigError(f"unknown strategy {strategy!r}; choose from {sorted(self.STRATEGIES)}")
+        _lib.check(self._L.pgmoe_model_set_strategy(self._h, self.STRATEGIES[strategy]))
+
     def set_kernel(self, kernel: str) -> None:
         _lib.check(self._L.pgmoe_model_set_kernel(self._h, _KERNEL[kernel]))
 

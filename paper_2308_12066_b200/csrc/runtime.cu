@@ -63,6 +63,7 @@ struct pgmoe_model {
     pgmoe_config cfg{};
     int wdtype = PGMOE_BF16, placement = PGMOE_RESIDENT, max_tokens = 0, kernel = PGMOE_KERNEL_AUTO;
     int e_begin = 0, e_local = 0;  // expert range held by this model (expert parallelism)
+    int strategy = PGMOE_PRE_GATED;  // offloaded migration policy (scheduler.py:36-49)
     size_t sw = 2, gate_bytes = 0, dense_bytes = 0, w1_bytes = 0, rec_bytes = 0;
     std::vector<BlockW> blocks;
     unsigned char *dev_pool = nullptr;   // gates + dense (+ experts when resident)
@@ -82,6 +83,7 @@ struct pgmoe_model {
     int slot_experts = 0;
     cudaStream_t copy = nullptr;
     std::vector<cudaEvent_t> ready, done, routed;
+    cudaEvent_t gated = nullptr;  // on_demand: compute reached the block
     std::vector<bool> slot_used;
     // stats
     pgmoe_stats stats{};
@@ -252,6 +254,25 @@ static int issue_fetch(pgmoe_model *m, int tb, int ri) {
     return PGMOE_OK;
 }
 
+// prefetch_all (scheduler.py:336-342): the whole expert set of block `tb`
+// (one contiguous DMA of E records) into slot `ri`, indexed by expert id.
+static int issue_fetch_all(pgmoe_model *m, int tb, int ri) {
+    const int E = m->e_local;
+    if (m->slot_used[ri]) PG_CUDA(cudaStreamWaitEvent(m->copy, m->done[ri], 0));
+    if (!m->cp_a.empty()) PG_CUDA(cudaEventRecord(m->cp_a[tb], m->copy));
+    tl_begin(m, "transfer", "fetch[" + std::to_string(E) + "]", tb, m->copy);
+    PG_CUDA(cudaMemcpyAsync(m->slots + (size_t)ri * m->slot_capacity, m->blocks[tb].experts, (size_t)E * m->rec_bytes,
+                            cudaMemcpyHostToDevice, m->copy));
+    tl_end(m, m->copy);
+    if (!m->cp_b.empty()) PG_CUDA(cudaEventRecord(m->cp_b[tb], m->copy));
+    PG_CUDA(cudaEventRecord(m->ready[ri], m->copy));
+    m->stats.h2d_copies++;
+    m->stats.h2d_bytes += (int64_t)E * (int64_t)m->rec_bytes;
+    m->slot_used[ri] = true;
+    if ((int)m->nact_iter.size() == m->cfg.num_blocks) m->nact_iter[tb] = E;
+    return PGMOE_OK;
+}
+
 static int route_into(pgmoe_model *m, const float *x, int T, const void *G, int ri, bool mirror,
                       cudaStream_t s, const char *label, int block) {
     const auto &c = m->cfg;
@@ -285,26 +306,44 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
         m->t0_recorded = true;
     }
     if (off) m->nact_iter.assign(nb, 0);
+    // Migration policy (scheduler.py:287-373), offloaded placement only:
+    //   pre_gated    : block b+L's routed experts leave as soon as K1 decides
+    //                  them, overlapping block b; block 0's fetch is exposed
+    //   on_demand    : block b's routed experts are fetched when block b
+    //                  starts, serial with its compute
+    //   prefetch_all : block b+1's whole expert set streams during block b;
+    //                  block 0's set is an exposed head transfer
+    const int strat = off ? m->strategy : PGMOE_PRE_GATED;
+    const bool prefetch_all = off && strat == PGMOE_PREFETCH_ALL;
     const float *cur = x_in;
     for (int b = 0; b < nb; ++b) {
         const BlockW &bw = m->blocks[b];
         const int ri = b % R;
         int pending_fetch = -1;
+        if (prefetch_all) {
+            if (b == 0) PG_TRY(issue_fetch_all(m, 0, 0));
+            if (b + 1 < nb) PG_TRY(issue_fetch_all(m, b + 1, (b + 1) % R));
+        }
         if (has_conv_gate(c, b)) {
-            PG_TRY(route_into(m, cur, T, bw.gate, ri, off, s, "gate", b));
-            if (off) PG_TRY(issue_fetch(m, b, ri));  // exposed serial fetch
+            PG_TRY(route_into(m, cur, T, bw.gate, ri, off && !prefetch_all, s, "gate", b));
+            if (off && strat == PGMOE_PRE_GATED) PG_TRY(issue_fetch(m, b, ri));  // exposed serial fetch
         }
         if (has_pre_gate(c, b)) {
             const int tr = (b + L) % R;
-            PG_TRY(route_into(m, cur, T, bw.pre_gate, tr, off, s, "pre_gate", b));
-            if (off) pending_fetch = b + L;
+            PG_TRY(route_into(m, cur, T, bw.pre_gate, tr, off && !prefetch_all, s, "pre_gate", b));
+            if (off && strat == PGMOE_PRE_GATED) pending_fetch = b + L;
+        }
+        if (off && strat == PGMOE_ON_DEMAND) {  // fetch starts once compute reaches block b
+            PG_CUDA(cudaEventRecord(m->gated, s));
+            PG_CUDA(cudaStreamWaitEvent(m->copy, m->gated, 0));
+            PG_TRY(issue_fetch(m, b, ri));
         }
         const RoutingBuf &rb = m->routing[ri];
         const void *experts = off ? (const void *)(m->slots + (size_t)ri * m->slot_capacity)
                                   : (const void *)bw.experts;
         if (off) PG_CUDA(cudaStreamWaitEvent(s, m->ready[ri], 0));
         tl_begin(m, "compute", "experts", b, s);
-        PG_TRY(run_ffn(m, cur, T, experts, off ? 1 : 0, &rb.r, s));
+        PG_TRY(run_ffn(m, cur, T, experts, (off && !prefetch_all) ? 1 : 0, &rb.r, s));
         tl_end(m, s);
         if (off) {
             PG_CUDA(cudaEventRecord(m->done[ri], s));
@@ -448,6 +487,7 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
         }
         if (cudaStreamCreateWithFlags(&m->copy, cudaStreamNonBlocking) != cudaSuccess) return fail(PGMOE_E_CUDA);
         m->ready.resize(R); m->done.resize(R); m->slot_used.assign(R, false);
+        cudaEventCreateWithFlags(&m->gated, cudaEventDisableTiming);
         for (int i = 0; i < R; ++i) {
             cudaEventCreateWithFlags(&m->ready[i], cudaEventDisableTiming);
             cudaEventCreateWithFlags(&m->done[i], cudaEventDisableTiming);
@@ -497,6 +537,7 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     for (auto e : m->ready) cudaEventDestroy(e);
     for (auto e : m->done) cudaEventDestroy(e);
     for (auto e : m->routed) cudaEventDestroy(e);
+    if (m->gated) cudaEventDestroy(m->gated);
     for (auto e : m->cp_a) cudaEventDestroy(e);
     for (auto e : m->cp_b) cudaEventDestroy(e);
     for (auto e : m->ffn_b) cudaEventDestroy(e);
@@ -531,6 +572,34 @@ extern "C" int pgmoe_model_config(pgmoe_model *m, pgmoe_config *cfg, int32_t *wd
     PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
     if (cfg) *cfg = m->cfg;
     if (wdtype) *wdtype = m->wdtype;
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_model_set_strategy(pgmoe_model *m, int32_t strategy) {
+    PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
+    PG_REQUIRE(strategy >= PGMOE_PRE_GATED && strategy <= PGMOE_PREFETCH_ALL, PGMOE_E_CONFIG,
+               "unknown strategy %d", strategy);
+    PG_REQUIRE(m->placement == PGMOE_OFFLOADED, PGMOE_E_CONFIG, "migration strategies need an offloaded model");
+    PG_REQUIRE(strategy != PGMOE_PRE_GATED || m->cfg.activation_level >= 1, PGMOE_E_CONFIG,
+               "pre_gated strategy requires a model with activation_level >= 1");
+    std::lock_guard<std::mutex> g(m->mu);
+    if (strategy == PGMOE_PREFETCH_ALL && m->slot_experts < m->e_local) {  // slots must hold a whole block
+        PG_CUDA(cudaDeviceSynchronize());
+        const int R = m->cfg.activation_level + 1;
+        const size_t cap = (size_t)m->e_local * m->rec_bytes;
+        unsigned char *ns = nullptr;
+        if (cudaMalloc(&ns, cap * R) != cudaSuccess) {
+            set_error("OOM: %zu B of HBM for %d whole-block expert slots", cap * R, R);
+            return PGMOE_E_OOM;
+        }
+        cudaFree(m->slots);
+        m->slots = ns;
+        m->slot_capacity = cap;
+        m->slot_experts = m->e_local;
+        m->stats.slot_capacity_bytes = (int64_t)cap;
+        m->slot_used.assign(R, false);
+    }
+    m->strategy = strategy;
     return PGMOE_OK;
 }
 
