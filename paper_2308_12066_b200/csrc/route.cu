@@ -15,15 +15,15 @@
 // __dadd_rn/__dmul_rn) and ranked with the reference key (-logit, id).
 // The fallback count is reported; flips are zero by construction.
 //
-// Two kernels:
-//   route_logits_kernel : grid (token tiles x K splits); each thread owns
-//       V adjacent experts (one 16-byte gate load) for TOK tokens and
-//       accumulates fp64 logits (DFMA) plus the fp32 |p| sum of the bound
-//       (FFMA pipe), reduced in a fixed order into per-split partials.
-//   route_select_kernel : one warp per token sums the split partials in
-//       order, certifies / recomputes, softmax, writes ids & weights; the
-//       last CTA builds histogram, exclusive scan, stable permutation and
-//       the active-expert list.
+// One kernel, grid (token tiles x K splits):
+//   1. every CTA accumulates fp64 partial logits of TOK tokens over its K
+//      slice (V adjacent experts per thread, exact products -> one rounding
+//      per DFMA) and the slice's column max |G|;
+//   2. the last CTA of a token tile (atomic ticket) sums the split partials
+//      in split order, bounds the error by sum|x| * max|G|, certifies or
+//      recomputes, softmaxes and writes ids & weights (one warp per token);
+//   3. the last token tile builds the histogram, exclusive scan, stable
+//      permutation and active-expert list.
 #include <algorithm>
 
 #include "common.cuh"
@@ -31,8 +31,9 @@
 namespace pgmoe {
 
 constexpr int kLogitThreads = 256;
-constexpr int kSelectWarps = 8;
-constexpr int kSelectThreads = kSelectWarps * 32;
+constexpr int kSelectWarps = 8;  // one warp per token of a tile (TOK <= 8)
+constexpr int kSelectThreads = kLogitThreads;
+constexpr int kMaxTiles = 8192;
 constexpr int kMaxSplits = 64;
 
 struct RouteParams {
@@ -42,9 +43,10 @@ struct RouteParams {
     int tok;      // tokens per logits CTA
     int splits;   // K splits
     pgmoe_routing out;
-    int *counter;      // workspace: select CTAs finished (reset by the last CTA)
+    int *counter;      // workspace: token tiles finished (reset by the last one)
+    int *tile_counter; // workspace: [tiles] K splits finished per token tile
     double *plogit;    // workspace: [splits][T][E]
-    float *pcmax;      // workspace: [splits][E] column max |G| of each K slice (raw gates)
+    float *pcmax;      // workspace: [tiles][splits][E] column max |G| of each K slice
 };
 
 __device__ __forceinline__ bool better(double fa, int ia, double fb, int ib) {
@@ -113,18 +115,216 @@ __device__ double serial_logit(const float *x, const GT *G, int d, int E, int j)
     return acc;
 }
 
-// Partial logits of TOK tokens over the CTA's K range; expert columns in
-// groups of V (16/32-byte gate loads when VECLOAD).  Products of fp32
-// activations and fp32/bf16 gate values are exact in fp64, so every DFMA
-// rounds once, like one step of the reference's serial sum.
+// Phase 2: tokens [tok0, tok0+ntok) of tile `tile`, all splits present.
+template <typename GT>
+__device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, unsigned char *smem_raw) {
+    const int d = p.d, E = p.E, k = p.k;
+    const GT *G = static_cast<const GT *>(p.G);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double *logit = reinterpret_cast<double *>(smem_raw) + (size_t)warp * 2 * E;
+    double *bound = logit + E;
+    __shared__ double s_xsum[kSelectWarps];
+    const double u = 1.1102230246251565e-16;  // 2^-53
+    const double gam = (double)d * u / (1.0 - (double)d * u);
+    const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
+    const double bpad = 1e-300;  // products are exact in fp64: no underflow below ~1e-90
+    // sum_i |x_i G_ij| <= (sum_i |x_i|) * max_i |G_ij|
+    if (warp < ntok) {
+        double xs = 0.0;
+#pragma unroll 8
+        for (int i = lane; i < d; i += 32) xs += fabs((double)__ldg(p.x + (size_t)(tok0 + warp) * d + i));
+        xs = warp_sumd(xs);
+        if (lane == 0) s_xsum[warp] = xs * (1.0 + 2.0 * gam);  // rounding of the fp64 |x| sum
+    }
+    __syncthreads();
+    for (int q = tid; q < ntok * E; q += kSelectThreads) {
+        const int t = q / E, j = q - t * E;
+        double sum = 0.0;
+        float cm = 0.f;
+#pragma unroll 4
+        for (int z = 0; z < p.splits; ++z) {  // fixed order: deterministic
+            sum += __ldcg(p.plogit + ((size_t)z * p.T + tok0 + t) * E + j);
+            cm = fmaxf(cm, __ldcg(p.pcmax + ((size_t)tile * p.splits + z) * E + j));
+        }
+        double *lgt = reinterpret_cast<double *>(smem_raw) + (size_t)t * 2 * E;
+        lgt[j] = sum;
+        lgt[E + j] = bscale * s_xsum[t] * (double)cm + bpad;
+    }
+    __syncthreads();
+    const int tok = tok0 + warp;
+    if (warp < ntok) {  // tok < p.T follows
+        double *lg = logit;
+        double *bd = bound;
+        __syncwarp();
+        // finite check (core.py:297)
+        bool finite = true;
+        for (int j = lane; j < E; j += 32) finite &= (bool)isfinite(lg[j]);
+        finite = __all_sync(0xffffffffu, finite);
+        if (!finite) {
+            if (lane == 0) atomicCAS(p.out.status, 0, (int)PGMOE_E_GATE_OVERFLOW);
+            for (int s = lane; s < k; s += 32) {
+                p.out.ids[(size_t)tok * k + s] = 0;
+                p.out.w[(size_t)tok * k + s] = 0.f;
+            }
+        } else {
+            int sel[8];
+            uint32_t taken = 0;  // bit q: expert lane + 32*q taken
+            bool certified = true;
+            double minlow = INFINITY;
+            for (int s = 0; s < k; ++s) {
+                double bf = -INFINITY;
+                int bi = -1;
+                for (int j = lane, q = 0; j < E; j += 32, ++q)
+                    if (!(taken >> q & 1u) && (bi < 0 || better(lg[j], j, bf, bi))) {
+                        bf = lg[j];
+                        bi = j;
+                    }
+                warp_argmax(bf, bi);
+                sel[s] = bi;
+                if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+                const double low = bf - bd[bi];
+                minlow = fmin(minlow, low);
+                double up = -INFINITY;
+                for (int j = lane, q = 0; j < E; j += 32, ++q)
+                    if (!(taken >> q & 1u)) up = fmax(up, lg[j] + bd[j]);
+                up = warp_max(up);
+                certified &= (low > up);
+            }
+            if (!certified) {
+                // Candidates that could be in the reference top-k: recompute
+                // them in the reference's serial order.
+                uint32_t cand = 0;
+                for (int j = lane, q = 0; j < E; j += 32, ++q)
+                    if (lg[j] + bd[j] >= minlow) cand |= 1u << q;
+                __syncwarp();
+                for (int j = lane, q = 0; j < E; j += 32, ++q)
+                    if (cand >> q & 1u) lg[j] = serial_logit<GT>(p.x + (size_t)tok * d, G, d, E, j);
+                __syncwarp();
+                for (int s = 0; s < k; ++s) {
+                    double bf = -INFINITY;
+                    int bi = -1;
+                    for (int j = lane, q = 0; j < E; j += 32, ++q)
+                        if ((cand >> q & 1u) && (bi < 0 || better(lg[j], j, bf, bi))) {
+                            bf = lg[j];
+                            bi = j;
+                        }
+                    warp_argmax(bf, bi);
+                    sel[s] = bi;
+                    if ((bi & 31) == lane) cand &= ~(1u << (bi >> 5));
+                }
+                if (lane == 0) atomicAdd(p.out.status + 1, 1);
+            }
+            // softmax over all E (linalg.py:54-59), max-subtracted
+            double m = -INFINITY;
+            for (int j = lane; j < E; j += 32) m = fmax(m, lg[j]);
+            m = warp_max(m);
+            double z = 0.0;
+            for (int j = lane; j < E; j += 32) z += exp(lg[j] - m);
+            z = warp_sumd(z);
+            for (int s = 0; s < k; ++s) {
+                const double pr = exp(lg[sel[s]] - m) / z;
+                if (lane == 0) {
+                    if (!(pr > 0.0)) atomicCAS(p.out.status, 0, (int)PGMOE_E_GATE_UNDERFLOW);
+                    p.out.ids[(size_t)tok * k + s] = sel[s];
+                    p.out.w[(size_t)tok * k + s] = __double2float_rn(pr);
+                }
+            }
+        }
+    }
+
+}
+
+// Phase 3: histogram, exclusive scan, stable permutation, active list.
+__device__ void permute_all(const RouteParams &p, unsigned char *smem_raw) {
+    const int E = p.E, k = p.k;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = p.T * k;
+    int *whist = reinterpret_cast<int *>(smem_raw);  // [kSelectWarps][E] -> cursors
+    int *tot = whist + (size_t)kSelectWarps * E;     // [E]
+    for (int i = tid; i < kSelectWarps * E; i += kSelectThreads) whist[i] = 0;
+    __syncthreads();
+    const int seg = (N + kSelectWarps - 1) / kSelectWarps;
+    const int r0 = warp * seg, r1 = min(N, r0 + seg);
+    for (int r = r0 + lane; r < r1; r += 32) atomicAdd(&whist[warp * E + __ldcg(p.out.ids + r)], 1);
+    __syncthreads();
+    for (int e = tid; e < E; e += kSelectThreads) {
+        int s = 0;
+        for (int w = 0; w < kSelectWarps; ++w) s += whist[w * E + e];
+        tot[e] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of tot over E, active list
+        int run = 0, nact = 0;
+        for (int e0 = 0; e0 < E; e0 += 32) {
+            const int e = e0 + lane;
+            const int h = e < E ? tot[e] : 0;
+            int incl = h;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const unsigned am = __ballot_sync(0xffffffffu, h > 0);
+            if (e < E) {
+                const int ex = run + incl - h;
+                p.out.hist[e] = h;
+                p.out.off[e] = ex;
+                tot[e] = ex;  // reuse as exclusive offset
+                if (h > 0) p.out.act[nact + __popc(am & ((1u << lane) - 1u))] = e;
+            }
+            run += __shfl_sync(0xffffffffu, incl, 31);
+            nact += __popc(am);
+        }
+        if (lane == 0) {
+            p.out.off[E] = run;
+            *p.out.n_act = nact;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += kSelectThreads) {
+        int base = tot[e];
+        for (int w = 0; w < kSelectWarps; ++w) {
+            const int c = whist[w * E + e];
+            whist[w * E + e] = base;
+            base += c;
+        }
+    }
+    __syncthreads();
+    const unsigned ltmask = (1u << lane) - 1u;
+    for (int c0 = r0; c0 < r1; c0 += 32) {
+        const int r = c0 + lane;
+        const bool valid = r < r1;
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            const int e = __ldcg(p.out.ids + r);
+            const unsigned grp = __match_any_sync(vm, e);
+            const int rank = __popc(grp & ltmask);
+            const int pos = whist[warp * E + e] + rank;
+            p.out.perm[pos] = r;
+            p.out.w_perm[pos] = __ldcg(p.out.w + r);
+            __syncwarp(vm);
+            if (rank == __popc(grp) - 1) whist[warp * E + e] += __popc(grp);
+        }
+        __syncwarp();
+    }
+}
+
+// Tokens per logits CTA: more tokens re-read each gate row fewer times;
+// K splits (up to d/32) keep the grid >= ~2 CTAs per SM at small T.
+
+// Partial logits of TOK tokens over the CTA's K range (phase 1), then the
+// tile / global last-arriver phases.  Products of fp32 activations and
+// fp32/bf16 gate values are exact in fp64, so every DFMA rounds once, like
+// one step of the reference's serial sum.
 template <typename GT, int TOK, bool VECLOAD>
 __global__ void __launch_bounds__(kLogitThreads)
-route_logits_kernel(RouteParams p) {
+route_kernel(RouteParams p) {
     constexpr int V = Vec<GT>::N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int d = p.d, E = p.E;
     const GT *G = static_cast<const GT *>(p.G);
-    const int t0 = blockIdx.x * TOK;
+    const int tile = blockIdx.x;
+    const int t0 = tile * TOK;
     const int ntok = min(TOK, p.T - t0);
     const int split = blockIdx.y;
     const int k0 = (int)((long)d * split / p.splits), k1 = (int)((long)d * (split + 1) / p.splits);
@@ -136,7 +336,7 @@ route_logits_kernel(RouteParams p) {
 
     double *xd = reinterpret_cast<double *>(smem_raw);                    // [TOK][kn]
     double *red = reinterpret_cast<double *>(smem_raw);                   // reuse: [RG][TOK][E]
-    float *redm = reinterpret_cast<float *>(red + (size_t)RG * TOK * E);  // [RG][E] (raw gates)
+    float *redm = reinterpret_cast<float *>(red + (size_t)RG * TOK * E);  // [RG][E]
 
     pdl_wait();  // x is produced by the previous kernel in the stream
     pdl_trigger();
@@ -207,226 +407,38 @@ route_logits_kernel(RouteParams p) {
         for (int r = 0; r < RG; ++r) s += red[((size_t)r * TOK + t) * E + j];  // fixed order
         p.plogit[((size_t)split * p.T + t0 + t) * E + j] = s;
     }
-    if (blockIdx.x == 0) {
-        for (int j = tid; j < E; j += kLogitThreads) {
-            float m = 0.f;
-            for (int r = 0; r < RG; ++r) m = fmaxf(m, redm[(size_t)r * E + j]);
-            p.pcmax[(size_t)split * E + j] = m;
-        }
-    }
-}
-
-template <typename WT>
-__global__ void __launch_bounds__(kSelectThreads)
-route_select_kernel(RouteParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int d = p.d, E = p.E, k = p.k;
-    const WT *G = static_cast<const WT *>(p.G);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double *logit = reinterpret_cast<double *>(smem_raw) + (size_t)warp * 2 * E;
-    double *bound = logit + E;
-
-    pdl_wait();  // partial logits come from route_logits_kernel
-    pdl_trigger();
-    const double u = 1.1102230246251565e-16;  // 2^-53
-    const double gam = (double)d * u / (1.0 - (double)d * u);
-    const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
-    const double bpad = 1e-300;  // products are exact in fp64: no underflow below ~1e-90
-
-    // (1) per-token sum|x| (warp t), (2) all threads reduce the K-split
-    // partials of the CTA's tokens in split order, (3) one warp per token
-    // certifies and selects.  sum_i |x_i G_ij| <= (sum_i |x_i|) max_i |G_ij|.
-    __shared__ double s_xsum[kSelectWarps];
-    const int tok0 = blockIdx.x * kSelectWarps;
-    const int ntok = min(kSelectWarps, p.T - tok0);
-    if (warp < ntok) {
-        double xs = 0.0;
-#pragma unroll 8
-        for (int i = lane; i < d; i += 32) xs += fabs((double)__ldg(p.x + (size_t)(tok0 + warp) * d + i));
-        xs = warp_sumd(xs);
-        if (lane == 0) s_xsum[warp] = xs * (1.0 + 2.0 * gam);  // rounding of the fp64 |x| sum
-    }
-    __syncthreads();
-    for (int q = tid; q < ntok * E; q += kSelectThreads) {
-        const int t = q / E, j = q - t * E;
-        double sum = 0.0;
-        float cm = 0.f;
-#pragma unroll 4
-        for (int z = 0; z < p.splits; ++z) {  // fixed order: deterministic
-            sum += __ldcg(p.plogit + ((size_t)z * p.T + tok0 + t) * E + j);
-            cm = fmaxf(cm, __ldcg(p.pcmax + (size_t)z * E + j));
-        }
-        double *lgt = reinterpret_cast<double *>(smem_raw) + (size_t)t * 2 * E;
-        lgt[j] = sum;
-        lgt[E + j] = bscale * s_xsum[t] * (double)cm + bpad;
-    }
-    __syncthreads();
-    const int tok = tok0 + warp;
-    if (tok < p.T) {
-        double *lg = logit;
-        double *bd = bound;
-        __syncwarp();
-        // finite check (core.py:297)
-        bool finite = true;
-        for (int j = lane; j < E; j += 32) finite &= (bool)isfinite(lg[j]);
-        finite = __all_sync(0xffffffffu, finite);
-        if (!finite) {
-            if (lane == 0) atomicCAS(p.out.status, 0, (int)PGMOE_E_GATE_OVERFLOW);
-            for (int s = lane; s < k; s += 32) {
-                p.out.ids[(size_t)tok * k + s] = 0;
-                p.out.w[(size_t)tok * k + s] = 0.f;
-            }
-        } else {
-            int sel[8];
-            uint32_t taken = 0;  // bit q: expert lane + 32*q taken
-            bool certified = true;
-            double minlow = INFINITY;
-            for (int s = 0; s < k; ++s) {
-                double bf = -INFINITY;
-                int bi = -1;
-                for (int j = lane, q = 0; j < E; j += 32, ++q)
-                    if (!(taken >> q & 1u) && (bi < 0 || better(lg[j], j, bf, bi))) {
-                        bf = lg[j];
-                        bi = j;
-                    }
-                warp_argmax(bf, bi);
-                sel[s] = bi;
-                if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-                const double low = bf - bd[bi];
-                minlow = fmin(minlow, low);
-                double up = -INFINITY;
-                for (int j = lane, q = 0; j < E; j += 32, ++q)
-                    if (!(taken >> q & 1u)) up = fmax(up, lg[j] + bd[j]);
-                up = warp_max(up);
-                certified &= (low > up);
-            }
-            if (!certified) {
-                // Candidates that could be in the reference top-k: recompute
-                // them in the reference's serial order.
-                uint32_t cand = 0;
-                for (int j = lane, q = 0; j < E; j += 32, ++q)
-                    if (lg[j] + bd[j] >= minlow) cand |= 1u << q;
-                __syncwarp();
-                for (int j = lane, q = 0; j < E; j += 32, ++q)
-                    if (cand >> q & 1u) lg[j] = serial_logit<WT>(p.x + (size_t)tok * d, G, d, E, j);
-                __syncwarp();
-                for (int s = 0; s < k; ++s) {
-                    double bf = -INFINITY;
-                    int bi = -1;
-                    for (int j = lane, q = 0; j < E; j += 32, ++q)
-                        if ((cand >> q & 1u) && (bi < 0 || better(lg[j], j, bf, bi))) {
-                            bf = lg[j];
-                            bi = j;
-                        }
-                    warp_argmax(bf, bi);
-                    sel[s] = bi;
-                    if ((bi & 31) == lane) cand &= ~(1u << (bi >> 5));
-                }
-                if (lane == 0) atomicAdd(p.out.status + 1, 1);
-            }
-            // softmax over all E (linalg.py:54-59), max-subtracted
-            double m = -INFINITY;
-            for (int j = lane; j < E; j += 32) m = fmax(m, lg[j]);
-            m = warp_max(m);
-            double z = 0.0;
-            for (int j = lane; j < E; j += 32) z += exp(lg[j] - m);
-            z = warp_sumd(z);
-            for (int s = 0; s < k; ++s) {
-                const double pr = exp(lg[sel[s]] - m) / z;
-                if (lane == 0) {
-                    if (!(pr > 0.0)) atomicCAS(p.out.status, 0, (int)PGMOE_E_GATE_UNDERFLOW);
-                    p.out.ids[(size_t)tok * k + s] = sel[s];
-                    p.out.w[(size_t)tok * k + s] = __double2float_rn(pr);
-                }
-            }
-        }
+    for (int j = tid; j < E; j += kLogitThreads) {
+        float m = 0.f;
+        for (int r = 0; r < RG; ++r) m = fmaxf(m, redm[(size_t)r * E + j]);
+        p.pcmax[((size_t)tile * p.splits + split) * E + j] = m;
     }
 
-    // ---- last CTA: histogram, exclusive scan, stable permutation ---------
+    // ---- phase 2: the last split of this token tile selects ---------------
     __shared__ int s_last;
     __syncthreads();
     if (tid == 0) {
+        __threadfence();
+        s_last = (atomicAdd(p.tile_counter + tile, 1) == p.splits - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    select_tile<GT>(p, tile, t0, ntok, smem_raw);
+
+    // ---- phase 3: the last token tile permutes ----------------------------
+    __syncthreads();
+    if (tid == 0) {
+        p.tile_counter[tile] = 0;
         __threadfence();
         s_last = (atomicAdd(p.counter, 1) == (int)gridDim.x - 1);
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-
-    const int N = p.T * k;
-    int *whist = reinterpret_cast<int *>(smem_raw);  // [kSelectWarps][E] -> cursors
-    int *tot = whist + (size_t)kSelectWarps * E;     // [E]
-    for (int i = tid; i < kSelectWarps * E; i += kSelectThreads) whist[i] = 0;
-    __syncthreads();
-    const int seg = (N + kSelectWarps - 1) / kSelectWarps;
-    const int r0 = warp * seg, r1 = min(N, r0 + seg);
-    for (int r = r0 + lane; r < r1; r += 32) atomicAdd(&whist[warp * E + __ldcg(p.out.ids + r)], 1);
-    __syncthreads();
-    for (int e = tid; e < E; e += kSelectThreads) {
-        int s = 0;
-        for (int w = 0; w < kSelectWarps; ++w) s += whist[w * E + e];
-        tot[e] = s;
-    }
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan of tot over E, active list
-        int run = 0, nact = 0;
-        for (int e0 = 0; e0 < E; e0 += 32) {
-            const int e = e0 + lane;
-            const int h = e < E ? tot[e] : 0;
-            int incl = h;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const unsigned am = __ballot_sync(0xffffffffu, h > 0);
-            if (e < E) {
-                const int ex = run + incl - h;
-                p.out.hist[e] = h;
-                p.out.off[e] = ex;
-                tot[e] = ex;  // reuse as exclusive offset
-                if (h > 0) p.out.act[nact + __popc(am & ((1u << lane) - 1u))] = e;
-            }
-            run += __shfl_sync(0xffffffffu, incl, 31);
-            nact += __popc(am);
-        }
-        if (lane == 0) {
-            p.out.off[E] = run;
-            *p.out.n_act = nact;
-        }
-    }
-    __syncthreads();
-    for (int e = tid; e < E; e += kSelectThreads) {
-        int base = tot[e];
-        for (int w = 0; w < kSelectWarps; ++w) {
-            const int c = whist[w * E + e];
-            whist[w * E + e] = base;
-            base += c;
-        }
-    }
-    __syncthreads();
-    const unsigned ltmask = (1u << lane) - 1u;
-    for (int c0 = r0; c0 < r1; c0 += 32) {
-        const int r = c0 + lane;
-        const bool valid = r < r1;
-        const unsigned vm = __ballot_sync(0xffffffffu, valid);
-        if (valid) {
-            const int e = __ldcg(p.out.ids + r);
-            const unsigned grp = __match_any_sync(vm, e);
-            const int rank = __popc(grp & ltmask);
-            const int pos = whist[warp * E + e] + rank;
-            p.out.perm[pos] = r;
-            p.out.w_perm[pos] = __ldcg(p.out.w + r);
-            __syncwarp(vm);
-            if (rank == __popc(grp) - 1) whist[warp * E + e] += __popc(grp);
-        }
-        __syncwarp();
-    }
+    permute_all(p, smem_raw);
     if (tid == 0) *p.counter = 0;
 }
 
-// Tokens per logits CTA: more tokens re-read each gate row fewer times;
-// K splits (up to d/32) keep the grid >= ~2 CTAs per SM at small T.
 static int pick_tok(int T) {
     if (T < 64) return 1;
     if (T < 128) return 2;
@@ -444,22 +456,24 @@ static int pick_splits(int T, int d, int tok) {
 }
 
 template <typename GT>
-static size_t logits_smem(int tok, int d, int splits, int E) {
+static size_t route_smem(int tok, int d, int splits, int E) {
     constexpr int V = Vec<GT>::N;
     const int kn = (d + splits - 1) / splits;
     const int CG = (E + V - 1) / V, RG = std::max(1, kLogitThreads / CG);
-    const size_t a = (size_t)tok * kn * 8;
-    const size_t b = (size_t)RG * tok * E * 8 + (size_t)RG * E * 4;
-    return std::max(a, b);
+    const size_t a = (size_t)tok * kn * 8;                              // x tile
+    const size_t b = (size_t)RG * tok * E * 8 + (size_t)RG * E * 4;    // split reduction
+    const size_t c = (size_t)kSelectWarps * E * 16;                     // select: logit + bound
+    const size_t e = (size_t)(kSelectWarps + 1) * E * 4;                // permutation
+    return std::max(std::max(a, b), std::max(c, e));
 }
 
 template <typename GT, int TOK>
-static int launch_logits(const RouteParams &p, cudaStream_t s) {
+static int launch_route(const RouteParams &p, cudaStream_t s) {
     constexpr int V = Vec<GT>::N;
-    const size_t smem = logits_smem<GT>(TOK, p.d, p.splits, p.E);
+    const size_t smem = route_smem<GT>(TOK, p.d, p.splits, p.E);
     PG_REQUIRE(smem <= 200 * 1024, PGMOE_E_CONFIG, "route: d=%d E=%d exceeds shared memory", p.d, p.E);
     const bool vec = (p.E % V == 0) && (reinterpret_cast<uintptr_t>(p.G) % 16 == 0);
-    auto kern = vec ? route_logits_kernel<GT, TOK, true> : route_logits_kernel<GT, TOK, false>;
+    auto kern = vec ? route_kernel<GT, TOK, true> : route_kernel<GT, TOK, false>;
     static size_t attr[2] = {0, 0};
     if (smem > attr[vec]) {
         const size_t want = std::max<size_t>(smem, 64 * 1024);
@@ -474,36 +488,29 @@ static int launch_logits(const RouteParams &p, cudaStream_t s) {
 
 template <typename GT>
 static int route_dispatch(RouteParams p, cudaStream_t s) {
-    int st;
-    if (p.tok == 1) st = launch_logits<GT, 1>(p, s);
-    else if (p.tok == 2) st = launch_logits<GT, 2>(p, s);
-    else if (p.tok == 4) st = launch_logits<GT, 4>(p, s);
-    else st = launch_logits<GT, 8>(p, s);
-    if (st != PGMOE_OK) return st;
-    const size_t smem = std::max<size_t>((size_t)kSelectWarps * p.E * 16, (size_t)(kSelectWarps + 1) * p.E * 4);
-    static size_t attr = 0;
-    if (smem > attr) {
-        const size_t want = std::max<size_t>(smem, 64 * 1024);
-        PG_CUDA(cudaFuncSetAttribute(route_select_kernel<GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want));
-        attr = want;
-    }
-    const int grid = (p.T + kSelectWarps - 1) / kSelectWarps;
-    PG_CUDA(launch_pdl(route_select_kernel<GT>, dim3(grid), dim3(kSelectThreads), smem, s, p));
-    count_launch();
-    return PGMOE_OK;
+    PG_REQUIRE((p.T + p.tok - 1) / p.tok <= kMaxTiles, PGMOE_E_CONFIG, "route: T=%d too large", p.T);
+    if (p.tok == 1) return launch_route<GT, 1>(p, s);
+    if (p.tok == 2) return launch_route<GT, 2>(p, s);
+    if (p.tok == 4) return launch_route<GT, 4>(p, s);
+    return launch_route<GT, 8>(p, s);
 }
 
 }  // namespace pgmoe
 
 using namespace pgmoe;
 
-// workspace: [counter | pad to 256 B | plogit f64 [S][T][E] | pcmax f32 [S][E]]
+// workspace: [counter | tile counters [kMaxTiles] | plogit f64 [S][T][E] | pcmax f32 [tiles][S][E]]
+static size_t ws_head() { return 256 + (size_t)kMaxTiles * 4; }
+
 extern "C" size_t pgmoe_route_workspace_bytes(int32_t T, int32_t E) {
     // the split count depends on the call's T (and d); size for the worst T' <= T
     size_t worst = 0;
-    for (int t = 1; t <= std::max(T, 1); ++t)
-        worst = std::max(worst, (size_t)pick_splits(t, 1 << 20, pick_tok(t)) * (t + 1));
-    return 256 + worst * std::max(E, 1) * 12;
+    for (int t = 1; t <= std::max(T, 1); ++t) {
+        const int tok = pick_tok(t), sp = pick_splits(t, 1 << 20, tok);
+        const size_t tiles = (t + tok - 1) / tok;
+        worst = std::max(worst, (size_t)sp * t * 8 + tiles * sp * 4);
+    }
+    return ws_head() + worst * std::max(E, 1) + 256;
 }
 
 extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const void *gate_w,
@@ -534,9 +541,10 @@ extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const vo
     p.tok = pick_tok(T);
     p.splits = pick_splits(T, d, p.tok);
     p.counter = reinterpret_cast<int *>(ws);
+    p.tile_counter = reinterpret_cast<int *>(ws + 256);
     const size_t n = (size_t)p.splits * T * E;
-    p.plogit = reinterpret_cast<double *>(ws + 256);
-    p.pcmax = reinterpret_cast<float *>(ws + 256 + n * 8);
+    p.plogit = reinterpret_cast<double *>(ws + ws_head());
+    p.pcmax = reinterpret_cast<float *>(ws + ws_head() + n * 8);
     if (wdtype == PGMOE_BF16) return route_dispatch<uint16_t>(p, s);
     if (wdtype == PGMOE_F32) return route_dispatch<float>(p, s);
     set_error("unknown weight dtype %d", wdtype);
