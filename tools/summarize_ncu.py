@@ -79,16 +79,29 @@ def main():
     caps = [c for r in args.rep for c in read_rep(r)]
     summary = {"note": args.note, "captures": caps, "kernels": {}, "launch_shares": {}}
     for lab, sub in labels.items():
+        # "substr@0+1": one logical launch made of several captures (summed),
+        # e.g. the expert FFN = the up- and the down-projection GEMM
+        pick = None
+        if "@" in sub:
+            sub, idx = sub.split("@")
+            pick = [int(i) for i in idx.split("+")]
         ks = [c for c in caps if sub in c["kernel"]]
         if not ks:
             continue
-        n = len(ks)
-        rd = sum(c.get("dram__bytes_read.sum", 0) for c in ks) / n
-        wr = sum(c.get("dram__bytes_write.sum", 0) for c in ks) / n
+        if pick is not None:
+            ks = [ks[i] for i in pick if i < len(ks)]
+            rd = sum(c.get("dram__bytes_read.sum", 0) for c in ks)
+            wr = sum(c.get("dram__bytes_write.sum", 0) for c in ks)
+            n = 1
+        else:
+            n = len(ks)
+            rd = sum(c.get("dram__bytes_read.sum", 0) for c in ks) / n
+            wr = sum(c.get("dram__bytes_write.sum", 0) for c in ks) / n
         summary["kernels"][lab] = {
             "kernel": ks[0]["kernel"], "captures": n,
             "dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
             "duration_us_cold": sum(c.get("gpu__time_duration.sum", 0) for c in ks) / n * 1e6,
+            "captures_used": len(ks),
             "dram_pct_peak": sum(c.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 0) for c in ks) / n,
             "tensor_pipe_pct": sum(c.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", 0)
                                    for c in ks) / n,
