@@ -146,6 +146,9 @@ struct Sched {
     int groups, m_tiles, kb_total, kbs, S, max_npad;
     long long tiles, units;
     const int *prefix;  // [groups + 1] tile prefix (smem)
+    const int *g_rec;   // [groups] weight record index (smem)
+    const int *g_row0;  // [groups] first activation row (smem)
+    const int *g_ng;    // [groups] tokens routed to the group (smem)
 };
 
 struct Unit {
@@ -167,17 +170,9 @@ __device__ __forceinline__ Unit decode_unit(const Params &p, const Sched &sc, lo
     const int local = x.tile - sc.prefix[lo];
     const int n_tile = local / sc.m_tiles;
     x.m_tile = local - n_tile * sc.m_tiles;
-    int ng;
-    if (p.mode == kDense) {
-        ng = p.T;
-        x.row0 = 0;
-        x.rec = 0;
-    } else {
-        const int e = p.act[x.g];
-        ng = p.hist[e];
-        x.row0 = p.off[e];
-        x.rec = p.indexed_by_act ? x.g : e;
-    }
+    const int ng = sc.g_ng[lo];
+    x.row0 = sc.g_row0[lo];
+    x.rec = sc.g_rec[lo];
     x.n0 = n_tile * BN;
     x.n_valid = min(BN, ng - x.n0);
     x.n_pad = max(16, (x.n_valid + 15) & ~15);
@@ -218,6 +213,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     int *s_flag = reinterpret_cast<int *>(tmem_slot + 1);
     int *prefix = s_flag + 4;
+    int *g_rec = prefix + kMaxGroups + 1;
+    int *g_row0 = g_rec + kMaxGroups;
+    int *g_ng = g_row0 + kMaxGroups;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -227,13 +225,27 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
     sc.m_tiles = p.M / BM;
     sc.kb_total = p.K / BK;
     sc.prefix = prefix;
+    sc.g_rec = g_rec;
+    sc.g_row0 = g_row0;
+    sc.g_ng = g_ng;
     if (warp == 0) {
         int run = 0, mx = 16;
         for (int g0 = 0; g0 < sc.groups; g0 += 32) {
             const int g = g0 + lane;
             int nt = 0;
             if (g < sc.groups) {
-                const int ng = (p.mode == kDense) ? p.T : p.hist[p.act[g]];
+                int ng, e = 0;
+                if (p.mode == kDense) {
+                    ng = p.T;
+                    g_rec[g] = 0;
+                    g_row0[g] = 0;
+                } else {
+                    e = p.act[g];
+                    ng = p.hist[e];
+                    g_rec[g] = p.indexed_by_act ? g : e;
+                    g_row0[g] = p.off[e];
+                }
+                g_ng[g] = ng;
                 nt = ((ng + BN - 1) / BN) * sc.m_tiles;
                 mx = max(mx, (min(ng, BN) + 15) & ~15);
             }
@@ -495,7 +507,7 @@ __global__ void sum_slots_bf16_kernel(const float *__restrict__ yw, int T, int d
 
 template <int BN, int STAGES>
 constexpr size_t smem_bytes() {
-    return 1024 + (size_t)STAGES * (kABytes + BN * 128) + (2 * STAGES + 4) * 8 + 32 + (kMaxGroups + 1) * 4;
+    return 1024 + (size_t)STAGES * (kABytes + BN * 128) + (2 * STAGES + 4) * 8 + 32 + (4 * kMaxGroups + 1) * 4;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
