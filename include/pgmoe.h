@@ -153,6 +153,9 @@ typedef struct {
     int64_t route_flips;          /* always 0: certified routing */
     double h2d_seconds;           /* copy-stream busy time (CUDA events) */
     double last_step_seconds;
+    int64_t cache_bytes;          /* HBM expert-cache region (0 = no cache) */
+    int64_t cache_hits, cache_misses;
+    int64_t d2d_bytes;            /* cache <-> working-slot copies */
 } pgmoe_stats;
 
 /* init_model (core.py:266) + placement (tiers.py:134-157).  max_tokens
@@ -200,6 +203,17 @@ PGMOE_API int pgmoe_model_save_pgmoe1(pgmoe_model *m, const char *path);
  * outputs are identical under every strategy; only the copy schedule and
  * the HBM footprint change (prefetch_all reserves two whole-block slots). */
 PGMOE_API int pgmoe_model_set_strategy(pgmoe_model *m, int32_t strategy);
+
+/* HBM expert cache of an offloaded model (cache.py:49-103): policy 0 none,
+ * 1 LIFO, 2 LFU, 3 LRU; capacity = fraction of all expert bytes.  Keys are
+ * (block, expert); accesses follow each fetch list in order (active experts
+ * ascending, or all experts for prefetch_all).  Hits cost an HBM copy
+ * instead of a PCIe transfer; outputs are unchanged. */
+PGMOE_API int pgmoe_model_set_cache(pgmoe_model *m, int32_t policy, double capacity_fraction);
+/* Replays an access sequence through the cache index (no GPU needed):
+ * hit[i] and the number of entries access i evicted. */
+PGMOE_API int pgmoe_cache_replay(int32_t policy, int32_t capacity_records, const int32_t *blocks,
+                                 const int32_t *experts, int32_t n, int32_t *hit, int32_t *n_evicted);
 
 /* Kernel family for K2/K3 (AUTO: tcgen05 for bf16, SIMT for fp32). */
 PGMOE_API int pgmoe_model_set_kernel(pgmoe_model *m, int32_t kernel);

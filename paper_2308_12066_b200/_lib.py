@@ -51,7 +51,9 @@ class Stats(ctypes.Structure):
                 ("eq1_peak_bytes", ctypes.c_int64), ("ledger_peak_bytes", ctypes.c_int64),
                 ("h2d_bytes", ctypes.c_int64), ("h2d_copies", ctypes.c_int64),
                 ("route_fallbacks", ctypes.c_int64), ("route_flips", ctypes.c_int64),
-                ("h2d_seconds", ctypes.c_double), ("last_step_seconds", ctypes.c_double)]
+                ("h2d_seconds", ctypes.c_double), ("last_step_seconds", ctypes.c_double),
+                ("cache_bytes", ctypes.c_int64), ("cache_hits", ctypes.c_int64), ("cache_misses", ctypes.c_int64),
+                ("d2d_bytes", ctypes.c_int64)]
 
 
 EXPORTS = (
@@ -63,7 +65,8 @@ EXPORTS = (
     "pgmoe_model_timeline_jsonl", "pgmoe_model_set_timeline", "pgmoe_last_error", "pgmoe_version",
     "pgmoe_launch_count", "pgmoe_model_create_ex", "pgmoe_model_expert_records", "pgmoe_gather_rows",
     "pgmoe_unpermute_combine", "pgmoe_ep_local_routing", "pgmoe_model_config", "pgmoe_weight_file_config",
-    "pgmoe_model_load_pgmoe1", "pgmoe_model_save_pgmoe1", "pgmoe_model_set_strategy",
+    "pgmoe_model_load_pgmoe1", "pgmoe_model_save_pgmoe1", "pgmoe_model_set_strategy", "pgmoe_model_set_cache",
+    "pgmoe_cache_replay",
 )
 
 _lib = None
@@ -112,6 +115,8 @@ def load():
         "pgmoe_ep_local_routing": (i32, [vp, i32, i32, P(Routing), vp]),
         "pgmoe_model_config": (i32, [vp, P(Config), P(i32)]),
         "pgmoe_model_set_strategy": (i32, [vp, i32]),
+        "pgmoe_model_set_cache": (i32, [vp, i32, ctypes.c_double]),
+        "pgmoe_cache_replay": (i32, [i32, i32, vp, vp, i32, vp, vp]),
         "pgmoe_weight_file_config": (i32, [ctypes.c_char_p, P(Config)]),
         "pgmoe_model_load_pgmoe1": (i32, [vp, ctypes.c_char_p]),
         "pgmoe_model_save_pgmoe1": (i32, [vp, ctypes.c_char_p]),

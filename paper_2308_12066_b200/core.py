@@ -331,6 +331,14 @@ class DeviceModel:
             raise ConfigError(f"unknown strategy {strategy!r}; choose from {sorted(self.STRATEGIES)}")
         _lib.check(self._L.pgmoe_model_set_strategy(self._h, self.STRATEGIES[strategy]))
 
+    CACHE_POLICIES = {"none": 0, "lifo": 1, "lfu": 2, "lru": 3}
+
+    def set_cache(self, policy: str, capacity_fraction: float) -> None:
+        """HBM expert cache (cache.py:49-103) of an offloaded model."""
+        if policy not in self.CACHE_POLICIES:
+            raise ConfigError(f"unknown cache policy {policy!r}; choose from {sorted(self.CACHE_POLICIES)}")
+        _lib.check(self._L.pgmoe_model_set_cache(self._h, self.CACHE_POLICIES[policy], float(capacity_fraction)))
+
     def set_kernel(self, kernel: str) -> None:
         _lib.check(self._L.pgmoe_model_set_kernel(self._h, _KERNEL[kernel]))
 

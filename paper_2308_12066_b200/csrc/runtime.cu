@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "expert_cache.h"
 #include "kernels.h"
 #include "rng.h"
 
@@ -64,6 +65,12 @@ struct pgmoe_model {
     int wdtype = PGMOE_BF16, placement = PGMOE_RESIDENT, max_tokens = 0, kernel = PGMOE_KERNEL_AUTO;
     int e_begin = 0, e_local = 0;  // expert range held by this model (expert parallelism)
     int strategy = PGMOE_PRE_GATED;  // offloaded migration policy (scheduler.py:36-49)
+    // optional HBM expert cache (cache.py): entries live in `cache_region`; a
+    // hit is a D2D copy into the block's working slot, an inserted miss is
+    // copied on from the slot, all on the copy stream (FIFO: no slot hazards)
+    ExpertCacheIndex *cache = nullptr;
+    unsigned char *cache_region = nullptr;
+    int64_t cache_seq = 0;
     size_t sw = 2, gate_bytes = 0, dense_bytes = 0, w1_bytes = 0, rec_bytes = 0;
     std::vector<BlockW> blocks;
     unsigned char *dev_pool = nullptr;   // gates + dense (+ experts when resident)
@@ -221,6 +228,36 @@ static void tl_end(pgmoe_model *m, cudaStream_t s) {
     cudaEventRecord(m->tl.back().b, s);
 }
 
+// Cached fetch of `n` experts (ids `ids`, in access order) of block `tb` into
+// the working slot `dst`: the reference's cache.access per expert
+// (scheduler.py:295-311), hits copied from the cache region (D2D), misses
+// from pinned host memory, inserted misses copied on into the cache.
+static int fetch_cached(pgmoe_model *m, int tb, const int32_t *ids, int n, unsigned char *dst, int *misses) {
+    const unsigned char *src = m->blocks[tb].experts;
+    const size_t rec = m->rec_bytes;
+    int miss = 0;
+    for (int i = 0; i < n; ++i) {
+        const CacheOutcome o = m->cache->access(ExpertCacheIndex::key(tb, ids[i]), m->cache_seq++);
+        unsigned char *w = dst + (size_t)i * rec;
+        if (o.hit) {
+            PG_CUDA(cudaMemcpyAsync(w, m->cache_region + (size_t)o.slot * rec, rec, cudaMemcpyDeviceToDevice, m->copy));
+            m->stats.d2d_bytes += (int64_t)rec;
+            continue;
+        }
+        ++miss;
+        PG_CUDA(cudaMemcpyAsync(w, src + (size_t)ids[i] * rec, rec, cudaMemcpyHostToDevice, m->copy));
+        m->stats.h2d_copies++;
+        if (o.inserted) {
+            PG_CUDA(cudaMemcpyAsync(m->cache_region + (size_t)o.slot * rec, w, rec, cudaMemcpyDeviceToDevice, m->copy));
+            m->stats.d2d_bytes += (int64_t)rec;
+        }
+    }
+    m->stats.cache_hits = m->cache->hits();
+    m->stats.cache_misses = m->cache->misses();
+    *misses = miss;
+    return PGMOE_OK;
+}
+
 // Issue the H2D migration of block `tb`'s routed experts into slot `ri`
 // (scheduler.py:287-330 `issue`, made real).  Waits on the host for K1's
 // active list (pinned mirror), then enqueues one DMA per expert on the copy
@@ -237,18 +274,23 @@ static int issue_fetch(pgmoe_model *m, int tb, int ri) {
     tl_begin(m, "transfer", "fetch[" + std::to_string(n) + "]", tb, m->copy);
     unsigned char *dst = m->slots + (size_t)ri * m->slot_capacity;
     const unsigned char *src = m->blocks[tb].experts;
-    for (int i = 0; i < n;) {  // coalesce runs of consecutive experts into one DMA
-        int j = i + 1;
-        while (j < n && rb.act_host[j] == rb.act_host[j - 1] + 1) ++j;
-        PG_CUDA(cudaMemcpyAsync(dst + (size_t)i * m->rec_bytes, src + (size_t)rb.act_host[i] * m->rec_bytes,
-                                (size_t)(j - i) * m->rec_bytes, cudaMemcpyHostToDevice, m->copy));
-        m->stats.h2d_copies++;
-        i = j;
+    int misses = n;
+    if (m->cache) {
+        PG_TRY(fetch_cached(m, tb, rb.act_host, n, dst, &misses));
+    } else {
+        for (int i = 0; i < n;) {  // coalesce runs of consecutive experts into one DMA
+            int j = i + 1;
+            while (j < n && rb.act_host[j] == rb.act_host[j - 1] + 1) ++j;
+            PG_CUDA(cudaMemcpyAsync(dst + (size_t)i * m->rec_bytes, src + (size_t)rb.act_host[i] * m->rec_bytes,
+                                    (size_t)(j - i) * m->rec_bytes, cudaMemcpyHostToDevice, m->copy));
+            m->stats.h2d_copies++;
+            i = j;
+        }
     }
     tl_end(m, m->copy);
     if (!m->cp_b.empty()) PG_CUDA(cudaEventRecord(m->cp_b[tb], m->copy));
     PG_CUDA(cudaEventRecord(m->ready[ri], m->copy));
-    m->stats.h2d_bytes += (int64_t)n * (int64_t)m->rec_bytes;
+    m->stats.h2d_bytes += (int64_t)misses * (int64_t)m->rec_bytes;
     m->slot_used[ri] = true;
     if ((int)m->nact_iter.size() == c.num_blocks) m->nact_iter[tb] = n;
     return PGMOE_OK;
@@ -261,13 +303,20 @@ static int issue_fetch_all(pgmoe_model *m, int tb, int ri) {
     if (m->slot_used[ri]) PG_CUDA(cudaStreamWaitEvent(m->copy, m->done[ri], 0));
     if (!m->cp_a.empty()) PG_CUDA(cudaEventRecord(m->cp_a[tb], m->copy));
     tl_begin(m, "transfer", "fetch[" + std::to_string(E) + "]", tb, m->copy);
-    PG_CUDA(cudaMemcpyAsync(m->slots + (size_t)ri * m->slot_capacity, m->blocks[tb].experts, (size_t)E * m->rec_bytes,
-                            cudaMemcpyHostToDevice, m->copy));
+    int misses = E;
+    if (m->cache) {
+        std::vector<int32_t> all(E);
+        for (int e = 0; e < E; ++e) all[e] = e;
+        PG_TRY(fetch_cached(m, tb, all.data(), E, m->slots + (size_t)ri * m->slot_capacity, &misses));
+    } else {
+        PG_CUDA(cudaMemcpyAsync(m->slots + (size_t)ri * m->slot_capacity, m->blocks[tb].experts,
+                                (size_t)E * m->rec_bytes, cudaMemcpyHostToDevice, m->copy));
+        m->stats.h2d_copies++;
+    }
     tl_end(m, m->copy);
     if (!m->cp_b.empty()) PG_CUDA(cudaEventRecord(m->cp_b[tb], m->copy));
     PG_CUDA(cudaEventRecord(m->ready[ri], m->copy));
-    m->stats.h2d_copies++;
-    m->stats.h2d_bytes += (int64_t)E * (int64_t)m->rec_bytes;
+    m->stats.h2d_bytes += (int64_t)misses * (int64_t)m->rec_bytes;
     m->slot_used[ri] = true;
     if ((int)m->nact_iter.size() == m->cfg.num_blocks) m->nact_iter[tb] = E;
     return PGMOE_OK;
@@ -543,6 +592,8 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     for (auto e : m->ffn_b) cudaEventDestroy(e);
     for (auto &e : m->tl) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (m->t0) cudaEventDestroy(m->t0);
+    delete m->cache;
+    cudaFree(m->cache_region);
     for (auto &g : m->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     if (m->io_stream) cudaStreamDestroy(m->io_stream);
@@ -600,6 +651,46 @@ extern "C" int pgmoe_model_set_strategy(pgmoe_model *m, int32_t strategy) {
         m->slot_used.assign(R, false);
     }
     m->strategy = strategy;
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_model_set_cache(pgmoe_model *m, int32_t policy, double capacity_fraction) {
+    PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
+    PG_REQUIRE(policy >= kCacheNone && policy <= kCacheLru, PGMOE_E_CONFIG, "unknown cache policy %d", policy);
+    PG_REQUIRE(capacity_fraction >= 0.0 && capacity_fraction <= 1.0, PGMOE_E_CONFIG,
+               "capacity_fraction must be in [0, 1]");
+    PG_REQUIRE(m->placement == PGMOE_OFFLOADED, PGMOE_E_CONFIG, "the expert cache serves offloaded models");
+    std::lock_guard<std::mutex> g(m->mu);
+    PG_CUDA(cudaDeviceSynchronize());
+    delete m->cache;
+    m->cache = nullptr;
+    cudaFree(m->cache_region);
+    m->cache_region = nullptr;
+    m->stats.cache_bytes = 0;
+    if (policy == kCacheNone) return PGMOE_OK;
+    // cache.py: capacity = fraction of all expert bytes (scheduler.py:269-271)
+    const double total = (double)m->cfg.num_blocks * m->e_local * (double)(2.0 * m->cfg.d_model * m->cfg.d_ff *
+                                                                          (double)m->sw);
+    const int records = (int)((capacity_fraction * total) / (double)(2.0 * m->cfg.d_model * m->cfg.d_ff * m->sw));
+    if (records > 0 && cudaMalloc(&m->cache_region, (size_t)records * m->rec_bytes) != cudaSuccess) {
+        set_error("OOM: %d expert records of HBM cache", records);
+        return PGMOE_E_OOM;
+    }
+    m->cache = new ExpertCacheIndex(records, policy);
+    m->cache_seq = 0;
+    m->stats.cache_bytes = (int64_t)records * (int64_t)m->rec_bytes;
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_cache_replay(int32_t policy, int32_t capacity_records, const int32_t *blocks,
+                                  const int32_t *experts, int32_t n, int32_t *hit, int32_t *n_evicted) {
+    PG_REQUIRE(policy >= kCacheLifo && policy <= kCacheLru, PGMOE_E_CONFIG, "unknown cache policy %d", policy);
+    ExpertCacheIndex c(capacity_records, policy);
+    for (int i = 0; i < n; ++i) {
+        const CacheOutcome o = c.access(ExpertCacheIndex::key(blocks[i], experts[i]), i);
+        hit[i] = o.hit ? 1 : 0;
+        n_evicted[i] = (int32_t)o.evicted.size();
+    }
     return PGMOE_OK;
 }
 
@@ -915,9 +1006,11 @@ extern "C" int pgmoe_model_stats(pgmoe_model *m, pgmoe_stats *out) {
 extern "C" int pgmoe_model_reset_stats(pgmoe_model *m) {
     std::lock_guard<std::mutex> g(m->mu);
     const int64_t pinned = m->stats.pinned_hbm_bytes, slot = m->stats.slot_capacity_bytes;
+    const int64_t cb = m->stats.cache_bytes;
     m->stats = pgmoe_stats{};
     m->stats.pinned_hbm_bytes = pinned;
     m->stats.slot_capacity_bytes = slot;
+    m->stats.cache_bytes = cb;
     return PGMOE_OK;
 }
 

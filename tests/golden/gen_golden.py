@@ -219,6 +219,24 @@ def pgmoe1_fixture():
     save_model(mcore.init_model(cfg), os.path.join(HERE, "small_d16_f24_b3_e4.pgmoe1"))
 
 
+def cache_fixture():
+    """moesim.ExpertCache (cache.py:49-103) on Zipf and uniform traces."""
+    from moesim.cache import ExpertCache
+    cfg = moesim.ModelConfig(d_model=4, d_ff=8, num_blocks=6, num_experts=32, top_k=1, seed=0)
+    out = []
+    for skew, seed in ((1.0, 1), (0.0, 2), (1.4, 3)):
+        trace = mcore.gen_routing_trace(cfg, 400, skew, seed)
+        keys = [(b, d.expert_ids[0]) for it in trace.decisions for b, d in enumerate(it)]
+        for policy in ("lifo", "lfu", "lru"):
+            for cap in (0, 1, 7, 40, 120):
+                c = ExpertCache(cap * 100, policy)
+                res = [c.access(k, 100, i) for i, k in enumerate(keys)]
+                out.append({"skew": skew, "policy": policy, "capacity_records": cap,
+                            "blocks": [k[0] for k in keys], "experts": [k[1] for k in keys],
+                            "hit": [int(r.hit) for r in res], "n_evicted": [len(r.evicted) for r in res]})
+    return out
+
+
 def main():
     pgmoe1_fixture()
     fixtures = {
@@ -227,6 +245,7 @@ def main():
         "gate.json": gate_fixture,
         "decoder_small.json": small_decoder_fixture,
         "switch.json": switch_fixture,
+        "cache.json": cache_fixture,
     }
     meta = {"generator": "tests/golden/gen_golden.py", "reference": "moesim " + moesim.__version__,
             "python": sys.version.split()[0]}

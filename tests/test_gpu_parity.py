@@ -462,3 +462,34 @@ def test_strategies_change_the_schedule_not_the_math(strategy):
             assert fetch[b]["start_s"] >= dense[b - 1]["end_s"] - 1e-6
     res.close()
     m.close()
+
+
+@pytest.mark.parametrize("strategy", ["pre_gated", "prefetch_all"])
+@pytest.mark.parametrize("policy", ["lru", "lfu", "lifo"])
+def test_expert_cache_saves_pcie_not_math(strategy, policy):
+    """cache.py: with the whole expert set cacheable, a repeated iteration
+    moves nothing over PCIe; a small cache moves less; outputs unchanged."""
+    dims = og.Dims(256, 512, 4, 8, 1, seed=6)
+    T = 8
+    x0 = torch.from_numpy(tokens(256, T)).cuda()
+    ref = _device_model(dims, "bf16", "resident", max_tokens=T)
+    y_ref, _, _ = ref.decoder_iteration(x0)
+    m = _device_model(dims, "bf16", "offloaded", max_tokens=T)
+    m.set_strategy(strategy)
+    m.set_cache(policy, 1.0)
+    m.decoder_iteration(x0)
+    m.reset_stats()
+    y, _, _ = m.decoder_iteration(x0)
+    torch.cuda.synchronize()
+    st = m.stats()
+    assert torch.equal(y, y_ref)
+    assert st["h2d_bytes"] == 0 and st["cache_hits"] > 0
+    m.set_cache(policy, 0.3)
+    m.reset_stats()
+    m.decoder_iteration(x0)
+    y2, _, _ = m.decoder_iteration(x0)
+    torch.cuda.synchronize()
+    assert torch.equal(y2, y_ref)
+    m.set_cache("none", 0.0)
+    ref.close()
+    m.close()
