@@ -493,3 +493,31 @@ def test_expert_cache_saves_pcie_not_math(strategy, policy):
     m.set_cache("none", 0.0)
     ref.close()
     m.close()
+
+
+@pytest.mark.parametrize("level", [0, 2])
+@pytest.mark.parametrize("placement", ["resident", "offloaded"])
+def test_activation_levels_wiring_and_migration(level, placement):
+    """core.py:73-89: level 0 = conventional gating (every block its own gate,
+    on-demand fetch when offloaded), level 2 = decisions two blocks ahead
+    (three expert slots).  Device decisions equal the oracle's decoder run on
+    the device's own block inputs; offloaded equals resident."""
+    p = P()
+    dims = og.Dims(128, 256, 5, 8, 2, activation_level=level, seed=9)
+    T = 12
+    x0 = tokens(128, T, seed=3)
+    res = _device_model(dims, "f32", "resident", max_tokens=T)
+    om = og.OracleModel(dims, "f32")
+    outs = _teacher_forced_chain(res, om, x0, TOL["f32"])
+    y, ids, w = res.decoder_iteration(torch.from_numpy(x0).cuda(), trace=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y, outs[-1])
+    if placement == "offloaded":
+        off = _device_model(dims, "f32", "offloaded", max_tokens=T)
+        if level == 0:
+            off.set_strategy("on_demand")
+        y2, ids2, _ = off.decoder_iteration(torch.from_numpy(x0).cuda(), trace=True)
+        torch.cuda.synchronize()
+        assert torch.equal(ids2, ids) and torch.equal(y2, y)
+        off.close()
+    res.close()
