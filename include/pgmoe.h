@@ -78,6 +78,7 @@ typedef struct {
     int32_t *status; /* [4] [0] device error code, [1] tokens that needed the
                         serial-fp64 recompute, [2] routing flips (0 by
                         construction), [3] reserved */
+    int32_t *inv;    /* [T*k] optional (may be NULL): position of entry t*k+s in perm */
 } pgmoe_routing;
 
 /* ---------------------------------------------------------------- kernels */

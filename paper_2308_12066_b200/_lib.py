@@ -43,7 +43,7 @@ class Config(ctypes.Structure):
 
 class Routing(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
-                ("ids", "w", "hist", "off", "perm", "w_perm", "act", "n_act", "status")]
+                ("ids", "w", "hist", "off", "perm", "w_perm", "act", "n_act", "status", "inv")]
 
 
 class Stats(ctypes.Structure):

@@ -160,7 +160,7 @@ class DeviceRouting:
         a = self.act_n.data_ptr()
         self._c = _lib.Routing(self.ids.data_ptr(), self.w.data_ptr(), self.hist.data_ptr(),
                                self.off.data_ptr(), self.perm.data_ptr(), self.w_perm.data_ptr(),
-                               a, a + 4 * E, self.status.data_ptr())
+                               a, a + 4 * E, self.status.data_ptr(), None)
 
     @property
     def c(self) -> _lib.Routing:

@@ -53,6 +53,11 @@ struct Params {
     int indexed_by_act;
     float *out_f32;       // kDown: yw [T*k][M] ; kDense: y [T][M]
     uint16_t *out_bf16;   // kUp: hb [T*k][M] ; kDown (k == 1): mixb [T][M]
+    // kDense: the next block's routing is already known (pre-gate), so the
+    // epilogue also writes the next up-projection's packed bf16 operand:
+    // next_xb[next_inv[t*k+s]][m] = bf16(y[t][m])
+    uint16_t *next_xb;
+    const int *next_inv;
     int *counters;
     float *partial;
     long long partial_cap;  // floats
@@ -194,6 +199,10 @@ __device__ __forceinline__ void store_out(const Params &p, const Unit &x, int n,
         if (p.out_bf16) p.out_bf16[(size_t)dst * p.M + m] = bf16_bits(y);  // top-1: mix == w*y
     } else {
         p.out_f32[(size_t)col * p.M + m] = v;
+        if (p.next_xb) {
+            const uint16_t b = bf16_bits(v);
+            for (int s = 0; s < p.k; ++s) p.next_xb[(size_t)__ldg(p.next_inv + (size_t)col * p.k + s) * p.M + m] = b;
+        }
     }
 }
 
@@ -598,7 +607,7 @@ int tc_pack_rows(const float *x, const int *perm, int n, int d, int k, uint16_t 
 
 int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
                    const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, void *ws,
-                   size_t ws_bytes, cudaStream_t s) {
+                   size_t ws_bytes, cudaStream_t s, bool xb_ready) {
     PG_REQUIRE(tc_supported(d, f), PGMOE_E_CONFIG, "tcgen05 path needs d, f multiples of 128 and f >= d");
     PG_REQUIRE((reinterpret_cast<uintptr_t>(experts) & 15) == 0 && stride % 16 == 0, PGMOE_E_CONFIG,
                "expert records must be 16-byte aligned");
@@ -607,7 +616,7 @@ int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *exper
     // cache), both <= 1024; the extent only bounds TMA address generation.
     const int rec_extent = 1024;
     const int bn = (n >= 2048) ? 256 : 64;
-    PG_TRY(tc_pack_rows(x, r->perm, n, d, k, xb, s));
+    if (!xb_ready) PG_TRY(tc_pack_rows(x, r->perm, n, d, k, xb, s));
     tc::Params p{};
     p.T = T;
     p.k = k;
@@ -632,7 +641,8 @@ int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *exper
 }
 
 int dense_tc2(const float *yw, const uint16_t *mixb_ready, int T, int d, int k, const void *dense_w, float *y,
-              uint16_t *mixb_scratch, void *ws, size_t ws_bytes, cudaStream_t s) {
+              uint16_t *mixb_scratch, void *ws, size_t ws_bytes, cudaStream_t s, uint16_t *next_xb,
+              const int *next_inv) {
     PG_REQUIRE(d % 128 == 0, PGMOE_E_CONFIG, "tcgen05 dense needs d multiple of 128");
     const uint16_t *mixb = mixb_ready;
     if (!mixb) {
@@ -650,6 +660,8 @@ int dense_tc2(const float *yw, const uint16_t *mixb_ready, int T, int d, int k, 
     p.T = T;
     p.k = k;
     p.out_f32 = y;
+    p.next_xb = next_xb;
+    p.next_inv = next_inv;
     CUtensorMap wmap, bmap;
     PG_TRY(tc::make_wmap(&wmap, dense_w, d, d, 1, (size_t)d * d * 2));
     PG_TRY(tc::make_bmap(&bmap, mixb, d, T));
@@ -664,14 +676,15 @@ int expert_ffn_tc(const float *x, int T, int d, int f, int k, const void *expert
                   cudaStream_t s) {
     uint16_t *hb = reinterpret_cast<uint16_t *>(h);
     uint16_t *xb = hb + (size_t)T * k * f;
-    return expert_ffn_tc2(x, T, d, f, k, experts, stride, indexed_by_act, r, xb, hb, yw, nullptr, ws, ws_bytes, s);
+    return expert_ffn_tc2(x, T, d, f, k, experts, stride, indexed_by_act, r, xb, hb, yw, nullptr, ws, ws_bytes, s,
+                          false);
 }
 
 int dense_tc(const float *yw, int T, int d, int k, const void *dense_w, float *y, void *ws, size_t ws_bytes,
              cudaStream_t s) {
     uint16_t *mixb = nullptr;
     PG_CUDA(cudaMallocAsync(&mixb, (size_t)std::max(T, 1) * d * 2, s));
-    int st = dense_tc2(yw, nullptr, T, d, k, dense_w, y, mixb, ws, ws_bytes, s);
+    int st = dense_tc2(yw, nullptr, T, d, k, dense_w, y, mixb, ws, ws_bytes, s, nullptr, nullptr);
     cudaFreeAsync(mixb, s);
     return st;
 }

@@ -25,8 +25,11 @@ bool tc_supported(int d, int f);
 // projection's epilogue so the dense layer reads it directly.
 int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
                    const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, void *ws,
-                   size_t ws_bytes, cudaStream_t s);
+                   size_t ws_bytes, cudaStream_t s, bool xb_ready);
+// next_xb / next_inv (optional): scatter y as the next block's packed bf16
+// up-projection operand (the next block's routing is already known).
 int dense_tc2(const float *yw, const uint16_t *mixb_ready, int T, int d, int k, const void *dense_w, float *y,
-              uint16_t *mixb_scratch, void *ws, size_t ws_bytes, cudaStream_t s);
+              uint16_t *mixb_scratch, void *ws, size_t ws_bytes, cudaStream_t s, uint16_t *next_xb,
+              const int *next_inv);
 
 }  // namespace pgmoe

@@ -301,6 +301,7 @@ __device__ void permute_all(const RouteParams &p, unsigned char *smem_raw) {
             const int rank = __popc(grp & ltmask);
             const int pos = whist[warp * E + e] + rank;
             p.out.perm[pos] = r;
+            if (p.out.inv) p.out.inv[r] = pos;
             p.out.w_perm[pos] = __ldcg(p.out.w + r);
             __syncwarp(vm);
             if (rank == __popc(grp) - 1) whist[warp * E + e] += __popc(grp);

@@ -151,8 +151,8 @@ static int validate_config(const pgmoe_config *c) {
 
 static int alloc_routing(RoutingBuf &rb, int T, int E, int k) {
     const size_t n = (size_t)T * k;
-    // layout: ids | w | perm | w_perm | hist | off | act | n_act | status
-    size_t bytes = n * 4 * 4 + (size_t)E * 4 + (size_t)(E + 1) * 4 + (size_t)(E + 1) * 4 + 16 + 256;
+    // layout: ids | w | perm | w_perm | inv | hist | off | act | n_act | status
+    size_t bytes = n * 4 * 5 + (size_t)E * 4 + (size_t)(E + 1) * 4 + (size_t)(E + 1) * 4 + 16 + 256;
     PG_CUDA(cudaMalloc(&rb.mem, bytes));
     PG_CUDA(cudaMemset(rb.mem, 0, bytes));
     char *p = static_cast<char *>(rb.mem);
@@ -160,6 +160,7 @@ static int alloc_routing(RoutingBuf &rb, int T, int E, int k) {
     rb.r.w = reinterpret_cast<float *>(p); p += n * 4;
     rb.r.perm = reinterpret_cast<int32_t *>(p); p += n * 4;
     rb.r.w_perm = reinterpret_cast<float *>(p); p += n * 4;
+    rb.r.inv = reinterpret_cast<int32_t *>(p); p += n * 4;
     rb.r.hist = reinterpret_cast<int32_t *>(p); p += (size_t)E * 4;
     rb.r.off = reinterpret_cast<int32_t *>(p); p += (size_t)(E + 1) * 4;
     rb.r.act = reinterpret_cast<int32_t *>(p);
@@ -190,27 +191,32 @@ static void *mat_ptr(pgmoe_model *m, const std::string &name, int b, int e, size
     return nullptr;
 }
 
+static bool use_tc(const pgmoe_model *m) {
+    return m->wdtype == PGMOE_BF16 && m->kernel != PGMOE_KERNEL_SIMT && tc_supported(m->cfg.d_model, m->cfg.d_ff);
+}
+
+// xb_ready: the previous block's dense epilogue already wrote this block's
+// packed bf16 operand (its routing was known before that dense ran).
 int run_ffn(pgmoe_model *m, const float *x, int T, const void *experts, int indexed,
-            const pgmoe_routing *r, cudaStream_t s) {
+            const pgmoe_routing *r, cudaStream_t s, bool xb_ready = false) {
     const auto &c = m->cfg;
-    const bool tc = m->wdtype == PGMOE_BF16 && m->kernel != PGMOE_KERNEL_SIMT &&
-                    tc_supported(c.d_model, c.d_ff);
+    const bool tc = use_tc(m);
     if (m->kernel == PGMOE_KERNEL_TCGEN05)
         PG_REQUIRE(tc, PGMOE_E_CONFIG, "tcgen05 kernels need bf16 weights and d, f multiples of 128");
     if (tc)
         return expert_ffn_tc2(x, T, c.d_model, c.d_ff, c.top_k, experts, m->rec_bytes, indexed, r, m->xb, m->hb,
-                              m->yw, c.top_k == 1 ? m->mixb : nullptr, m->tc_ws, m->tc_ws_bytes, s);
+                              m->yw, c.top_k == 1 ? m->mixb : nullptr, m->tc_ws, m->tc_ws_bytes, s, xb_ready);
     return expert_ffn_simt(x, T, c.d_model, c.d_ff, c.top_k, experts, m->rec_bytes, m->wdtype, indexed,
                            r, m->h, m->yw, s);
 }
 
-int run_dense(pgmoe_model *m, int T, const void *dense, float *y, cudaStream_t s) {
+// next (optional): the following block's routing, for the fused operand pack.
+int run_dense(pgmoe_model *m, int T, const void *dense, float *y, cudaStream_t s,
+              const pgmoe_routing *next = nullptr) {
     const auto &c = m->cfg;
-    const bool tc = m->wdtype == PGMOE_BF16 && m->kernel != PGMOE_KERNEL_SIMT &&
-                    tc_supported(c.d_model, c.d_ff);
-    if (tc)
+    if (use_tc(m))
         return dense_tc2(m->yw, c.top_k == 1 ? m->mixb : nullptr, T, c.d_model, c.top_k, dense, y, m->mixb,
-                         m->tc_ws, m->tc_ws_bytes, s);
+                         m->tc_ws, m->tc_ws_bytes, s, next ? m->xb : nullptr, next ? next->inv : nullptr);
     return dense_simt(m->yw, T, c.d_model, c.top_k, dense, m->wdtype, y, s);
 }
 
@@ -364,6 +370,7 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
     //                  block 0's set is an exposed head transfer
     const int strat = off ? m->strategy : PGMOE_PRE_GATED;
     const bool prefetch_all = off && strat == PGMOE_PREFETCH_ALL;
+    bool xb_ready = false;
     const float *cur = x_in;
     for (int b = 0; b < nb; ++b) {
         const BlockW &bw = m->blocks[b];
@@ -392,7 +399,7 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
                                   : (const void *)bw.experts;
         if (off) PG_CUDA(cudaStreamWaitEvent(s, m->ready[ri], 0));
         tl_begin(m, "compute", "experts", b, s);
-        PG_TRY(run_ffn(m, cur, T, experts, (off && !prefetch_all) ? 1 : 0, &rb.r, s));
+        PG_TRY(run_ffn(m, cur, T, experts, (off && !prefetch_all) ? 1 : 0, &rb.r, s, xb_ready));
         tl_end(m, s);
         if (off) {
             PG_CUDA(cudaEventRecord(m->done[ri], s));
@@ -400,7 +407,12 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
         }
         float *nxt = (b == nb - 1) ? y_out : m->act_buf[b & 1];
         tl_begin(m, "compute", "non_moe", b, s);
-        PG_TRY(run_dense(m, T, bw.dense, nxt, s));
+        // Pre-gating at work: block b+1's routing is already on the device
+        // (unless b+1 carries a conventional gate), so this dense layer also
+        // writes b+1's packed up-projection operand and b+1 skips the pack.
+        const bool fuse_next = use_tc(m) && b + 1 < nb && !has_conv_gate(c, b + 1);
+        PG_TRY(run_dense(m, T, bw.dense, nxt, s, fuse_next ? &m->routing[(b + 1) % R].r : nullptr));
+        xb_ready = fuse_next;
         tl_end(m, s);
         if (ids_trace) {
             PG_CUDA(cudaMemcpyAsync(ids_trace + (size_t)b * tk, rb.r.ids, tk * 4, cudaMemcpyDeviceToDevice, s));
