@@ -302,22 +302,24 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
     sc.tiles = prefix[sc.groups];
     sc.max_npad = s_flag[1];
     {
-        // Split K when the tiles do not cover the SMs evenly: pick the
-        // smallest split whose units fill >= 93% of the last wave, else the
-        // best one.  The fix-up reads S x n partial columns per row, so wide
-        // N tiles (which carry enough MMA work anyway) split less.
+        // Split K (a) to cover the SMs when there are fewer tiles than CTAs,
+        // (b) to even out the last wave when a split of >= 8 k-blocks per unit
+        // fills it >= 5% better.  The fix-up reads S x n partial columns per
+        // row, so wide N tiles split less.
         const int s_cap = max(1, min(sc.kb_total, 8 * 16 / min(BN, sc.max_npad)));
+        auto eff = [&](int c) {
+            const long long u = sc.tiles * c;
+            return (float)u / (float)(((u + gridDim.x - 1) / gridDim.x) * gridDim.x);
+        };
         int S = 1;
-        float best = 0.f;
-        for (int cand = 1; cand <= s_cap && sc.tiles > 0; ++cand) {
-            const long long u = sc.tiles * cand;
-            const long long waves = (u + gridDim.x - 1) / gridDim.x;
-            const float eff = (float)u / (float)(waves * gridDim.x);
-            if (eff > best + 0.02f) {
-                best = eff;
-                S = cand;
-            }
-            if (eff >= 0.93f) break;
+        if (sc.tiles > 0 && sc.tiles < (long long)gridDim.x) {
+            float best = eff(1);
+            for (int cand = 2; cand <= s_cap; ++cand)
+                if (eff(cand) > best + 0.02f) { best = eff(cand); S = cand; }
+        } else if (sc.tiles > 0) {
+            float best = eff(1);
+            for (int cand = 2; cand <= s_cap && sc.kb_total / cand >= 8; ++cand)
+                if (eff(cand) > best + 0.05f) { best = eff(cand); S = cand; }
         }
         while (S > 1 && ((long long)sc.tiles * S * BN * BM > p.partial_cap || sc.tiles > kCounterInts)) --S;
         sc.kbs = (sc.kb_total + S - 1) / S;
