@@ -260,8 +260,12 @@ def run_ours(args, rank: int, world: int):
         _, ids, _ = model.decoder_iteration(x, trace=True)
         torch.cuda.synchronize()
         nact_total = sum(len(torch.unique(ids[b])) for b in range(nb)) * prof_steps
-    act_bytes_per_token = 2 * d * 4 + 2 * f * 4   # x read, yw write, h write+read (fp32)
+    # per routed token: bf16 x packed+read, bf16 h write+read, fp32 yw + bf16 mix written
+    act_bytes_per_token = 2 * d * 2 + 2 * f * 2 + d * 6
     ffn_bytes = nact_total * rec + prof_steps * nb * T * act_bytes_per_token
+    fused = st.get("fused_blocks", 0) > 0
+    if fused:  # the dense layer runs inside the same launch: its weights and activations
+        ffn_bytes += prof_steps * nb * (d * d * sw + T * d * (2 + 4))
     ffn_gbs = ffn_bytes / ffn_s / 1e9 if ffn_s > 0 else None
     h2d_s = sum(e["end_s"] - e["start_s"] for e in fetch)
     pcie_gbs = measure_pcie_gbs(torch)
@@ -319,7 +323,7 @@ def run_ours(args, rank: int, world: int):
         "block_roofline": {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / block_ms, 4),
                            "bound": "pcie" if pcie_b and pcie_b / (pcie_gbs * 1e9) >= hbm_b / (hbm_peak * 1e9) else "hbm",
                            "n_act_avg": round(nact_avg, 2)},
-        "roofline": {"bound": "hbm", "kernel": "expert FFN (K2 up+down)",
+        "roofline": {"bound": "hbm", "kernel": "K2 up+down" + (" + K3 dense, one launch" if fused else ""),
                      "achieved": round(ffn_gbs, 1) if ffn_gbs else None, "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(ffn_gbs / hbm_peak, 4) if ffn_gbs else None,
                      "traffic": ncu_traffic("ffn"), "peak_kind": peak_kind,

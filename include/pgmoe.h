@@ -157,6 +157,7 @@ typedef struct {
     int64_t cache_bytes;          /* HBM expert-cache region (0 = no cache) */
     int64_t cache_hits, cache_misses;
     int64_t d2d_bytes;            /* cache <-> working-slot copies */
+    int64_t fused_blocks;         /* blocks whose dense layer ran inside the expert-FFN launch */
 } pgmoe_stats;
 
 /* init_model (core.py:266) + placement (tiers.py:134-157).  max_tokens

@@ -53,7 +53,7 @@ class Stats(ctypes.Structure):
                 ("route_fallbacks", ctypes.c_int64), ("route_flips", ctypes.c_int64),
                 ("h2d_seconds", ctypes.c_double), ("last_step_seconds", ctypes.c_double),
                 ("cache_bytes", ctypes.c_int64), ("cache_hits", ctypes.c_int64), ("cache_misses", ctypes.c_int64),
-                ("d2d_bytes", ctypes.c_int64)]
+                ("d2d_bytes", ctypes.c_int64), ("fused_blocks", ctypes.c_int64)]
 
 
 EXPORTS = (

@@ -1,11 +1,12 @@
 // ffn_tc.cu — K2/K3 on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
 //
-// One persistent, warp-specialised grouped GEMM serves the three dense
-// contractions of a block (core.py:308-316, :338):
+// One persistent, warp-specialised kernel runs the dense contractions of a
+// block as consecutive PHASES of a single launch (core.py:308-316, :338):
 //   up   : hb[r][m]  = bf16(relu(W1_e[m] . xb[r]))              (M = f, K = d)
 //   down : yw[perm[r]][m] = w_perm[r] * (W2_e[m] . hb[r])       (M = d, K = f)
 //          (+ mixb[perm[r]][m] = bf16(that) when top_k == 1)
 //   dense: y[t][m]  = D[m] . mixb[t]                            (M = d, K = d)
+//          (+ the next block's packed operand, see next_xb)
 // "Swap-AB": weight rows fill the 128-row UMMA M dimension and the few
 // routed tokens of an expert are the N dimension (padded to 16), so every
 // weight tile is streamed from HBM exactly once; the kernel is bound by
@@ -13,15 +14,21 @@
 //
 // Both operands arrive by TMA into 128-byte-swizzled K-major tiles: the
 // weights through a 3-D map over the expert records (K, rows, record) and
-// the activations (bf16 rows packed once per GEMM in routing order, so an
-// expert's tokens are contiguous) through a 2-D map in 16-row boxes.
+// the activations (bf16 rows in routing order, so an expert's tokens are
+// contiguous) through a 2-D map in 16-row boxes.  A phase's activations are
+// the previous phase's output, so a grid-wide barrier separates phases; its
+// latency is hidden because the producer keeps streaming the next phase's
+// WEIGHT tiles into free pipeline stages and only defers their activation
+// boxes until the barrier opens (the same trick hides the programmatic-
+// dependent-launch wait of phase 0).
 //
-// Warp roles (192 threads, one CTA per SM):
+// Warp roles (192 threads, one CTA per SM, grid = #SMs so all CTAs are
+// co-resident for the barrier):
 //   warp 0      : TMA producer (one elected lane)
 //   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2-5   : epilogue — tcgen05.ld the fp32 accumulator, ReLU / combine
-//                 weight / scatter, or the split-K fix-up
-// Launches with few tiles split K across CTAs; the last CTA to finish a tile
+//                 weight / scatter, or the split-K fix-up; signals phases
+// Phases with few tiles split K across CTAs; the last CTA to finish a tile
 // (atomic ticket) sums the partials in split order — deterministic — and
 // runs the epilogue.
 #include <cuda.h>
@@ -42,23 +49,31 @@ constexpr int BK = 64;                // bf16 elements per 128-byte swizzle row
 constexpr int kABytes = BM * BK * 2;  // 16 KB
 constexpr int kBRowsPerBox = 16;      // activation rows per TMA box (2 KB)
 constexpr int kMaxGroups = 1024;
+constexpr int kMaxPhases = 3;
 constexpr int kCounterInts = 8192;    // split-K tile tickets at the head of the workspace
+constexpr int kSyncInts = 16;         // phase barriers + exit ticket, after the tickets
 
 enum Mode { kUp = 0, kDown = 1, kDense = 2 };
 
+struct PhaseDesc {
+    int mode, M, K;
+    float *out_f32;      // kDown: yw [T*k][M] ; kDense: y [T][M]
+    uint16_t *out_bf16;  // kUp: hb [T*k][M] ; kDown (k == 1): mixb [T][M]
+};
+
 struct Params {
-    int mode, M, K, T, k;
+    int nphase, T, k;
+    PhaseDesc ph[kMaxPhases];
     const int *act, *n_act, *off, *hist, *perm;
     const float *w_perm;
     int indexed_by_act;
-    float *out_f32;       // kDown: yw [T*k][M] ; kDense: y [T][M]
-    uint16_t *out_bf16;   // kUp: hb [T*k][M] ; kDown (k == 1): mixb [T][M]
-    // kDense: the next block's routing is already known (pre-gate), so the
-    // epilogue also writes the next up-projection's packed bf16 operand:
+    // dense epilogue: the next block's routing is already known (pre-gate),
+    // so it also writes the next up-projection's packed bf16 operand:
     // next_xb[next_inv[t*k+s]][m] = bf16(y[t][m])
     uint16_t *next_xb;
     const int *next_inv;
-    int *counters;
+    int *counters;   // [kCounterInts] split-K tickets
+    int *sync;       // [kSyncInts] phase_done[kMaxPhases], exit ticket
     float *partial;
     long long partial_cap;  // floats
 };
@@ -147,38 +162,63 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 }
 __device__ __forceinline__ uint16_t bf16_bits(float a) { return __bfloat16_as_ushort(__float2bfloat16_rn(a)); }
 
-struct Sched {
-    int groups, m_tiles, kb_total, kbs, S, max_npad;
-    long long tiles, units;
-    const int *prefix;  // [groups + 1] tile prefix (smem)
-    const int *g_rec;   // [groups] weight record index (smem)
-    const int *g_row0;  // [groups] first activation row (smem)
-    const int *g_ng;    // [groups] tokens routed to the group (smem)
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+struct PhaseSched {
+    int mode, M, K, m_tiles, kb_total, kbs, S;
+    long long tiles, units, unit0;
 };
 
 struct Unit {
-    int g, m_tile, n0, n_valid, n_pad, kb0, kb1, tile, s, row0, rec;
+    int ph, g, m_tile, n0, n_valid, n_pad, kb0, kb1, tile, s, row0, rec;
+};
+
+struct Groups {
+    int n;              // expert groups (routing)
+    int T;              // tokens (dense)
+    const int *ntp;     // [n + 1] prefix of N tiles per group (smem)
+    const int *rec, *row0, *ng;  // per group (smem)
 };
 
 template <int BN>
-__device__ __forceinline__ Unit decode_unit(const Params &p, const Sched &sc, long long u) {
+__device__ __forceinline__ Unit decode_unit(const PhaseSched *ps, int nphase, const Groups &gr, long long u) {
     Unit x;
-    x.tile = (int)(u / sc.S);
-    x.s = (int)(u - (long long)x.tile * sc.S);
-    int lo = 0, hi = sc.groups - 1;  // last g with prefix[g] <= tile
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sc.prefix[mid] <= x.tile) lo = mid;
-        else hi = mid - 1;
+    int ph = 0;
+    while (ph + 1 < nphase && u >= ps[ph + 1].unit0) ++ph;
+    const PhaseSched &sc = ps[ph];
+    const long long lu = u - sc.unit0;
+    x.ph = ph;
+    x.tile = (int)(lu / sc.S);
+    x.s = (int)(lu - (long long)x.tile * sc.S);
+    int ng;
+    if (sc.mode == kDense) {
+        x.g = 0;
+        const int n_tile = x.tile / sc.m_tiles;
+        x.m_tile = x.tile - n_tile * sc.m_tiles;
+        x.n0 = n_tile * BN;
+        ng = gr.T;
+        x.row0 = 0;
+        x.rec = 0;
+    } else {
+        int lo = 0, hi = gr.n - 1;  // last g with ntp[g] * m_tiles <= tile
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (gr.ntp[mid] * sc.m_tiles <= x.tile) lo = mid;
+            else hi = mid - 1;
+        }
+        x.g = lo;
+        const int local = x.tile - gr.ntp[lo] * sc.m_tiles;
+        const int n_tile = local / sc.m_tiles;
+        x.m_tile = local - n_tile * sc.m_tiles;
+        x.n0 = n_tile * BN;
+        ng = gr.ng[lo];
+        x.row0 = gr.row0[lo];
+        x.rec = gr.rec[lo];
     }
-    x.g = lo;
-    const int local = x.tile - sc.prefix[lo];
-    const int n_tile = local / sc.m_tiles;
-    x.m_tile = local - n_tile * sc.m_tiles;
-    const int ng = sc.g_ng[lo];
-    x.row0 = sc.g_row0[lo];
-    x.rec = sc.g_rec[lo];
-    x.n0 = n_tile * BN;
     x.n_valid = min(BN, ng - x.n0);
     x.n_pad = max(16, (x.n_valid + 15) & ~15);
     x.kb0 = x.s * sc.kbs;
@@ -186,29 +226,35 @@ __device__ __forceinline__ Unit decode_unit(const Params &p, const Sched &sc, lo
     return x;
 }
 
-template <int BN>
-__device__ __forceinline__ void store_out(const Params &p, const Unit &x, int n, int m, float v) {
+__device__ __forceinline__ void store_out(const Params &p, const PhaseDesc &pd, const Unit &x, int n, int m,
+                                          float v) {
     const int col = x.n0 + n;
-    if (p.mode == kUp) {
-        p.out_bf16[(size_t)(x.row0 + col) * p.M + m] = bf16_bits(fmaxf(v, 0.f));  // relu, linalg.py:41-42
-    } else if (p.mode == kDown) {
+    if (pd.mode == kUp) {
+        pd.out_bf16[(size_t)(x.row0 + col) * pd.M + m] = bf16_bits(fmaxf(v, 0.f));  // relu, linalg.py:41-42
+    } else if (pd.mode == kDown) {
         const int r = x.row0 + col;
         const int dst = __ldg(p.perm + r);
         const float y = __ldg(p.w_perm + r) * v;  // combine weight (linalg.py:45-51)
-        p.out_f32[(size_t)dst * p.M + m] = y;
-        if (p.out_bf16) p.out_bf16[(size_t)dst * p.M + m] = bf16_bits(y);  // top-1: mix == w*y
+        pd.out_f32[(size_t)dst * pd.M + m] = y;
+        if (pd.out_bf16) pd.out_bf16[(size_t)dst * pd.M + m] = bf16_bits(y);  // top-1: mix == w*y
     } else {
-        p.out_f32[(size_t)col * p.M + m] = v;
+        pd.out_f32[(size_t)col * pd.M + m] = v;
         if (p.next_xb) {
             const uint16_t b = bf16_bits(v);
-            for (int s = 0; s < p.k; ++s) p.next_xb[(size_t)__ldg(p.next_inv + (size_t)col * p.k + s) * p.M + m] = b;
+            for (int s = 0; s < p.k; ++s) p.next_xb[(size_t)__ldg(p.next_inv + (size_t)col * p.k + s) * pd.M + m] = b;
         }
     }
 }
 
+struct DeferredB {
+    int stage, kb, row, npad;
+};
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, Params p) {
+block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant__ CUtensorMap b0,
+                  const __grid_constant__ CUtensorMap a1, const __grid_constant__ CUtensorMap b1,
+                  const __grid_constant__ CUtensorMap a2, const __grid_constant__ CUtensorMap b2, Params p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                             ~uintptr_t(1023));
@@ -221,41 +267,40 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     int *s_flag = reinterpret_cast<int *>(tmem_slot + 1);
-    int *prefix = s_flag + 4;
-    int *g_rec = prefix + kMaxGroups + 1;
+    int *ntp = s_flag + 4;
+    int *g_rec = ntp + kMaxGroups + 1;
     int *g_row0 = g_rec + kMaxGroups;
     int *g_ng = g_row0 + kMaxGroups;
+    const CUtensorMap *amaps[3] = {&a0, &a1, &a2};
+    const CUtensorMap *bmaps[3] = {&b0, &b1, &b2};
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    bool has_expert_phase = false, has_dense = false;
+    for (int i = 0; i < p.nphase; ++i) {
+        has_expert_phase |= p.ph[i].mode != kDense;
+        has_dense |= p.ph[i].mode == kDense;
+    }
 
     // ---- schedule (identical in every CTA) --------------------------------
-    Sched sc;
-    sc.groups = (p.mode == kDense) ? 1 : *p.n_act;
-    sc.m_tiles = p.M / BM;
-    sc.kb_total = p.K / BK;
-    sc.prefix = prefix;
-    sc.g_rec = g_rec;
-    sc.g_row0 = g_row0;
-    sc.g_ng = g_ng;
+    Groups gr;
+    gr.n = has_expert_phase ? *p.n_act : 0;
+    gr.T = p.T;
+    gr.ntp = ntp;
+    gr.rec = g_rec;
+    gr.row0 = g_row0;
+    gr.ng = g_ng;
     if (warp == 0) {
         int run = 0, mx = 16;
-        for (int g0 = 0; g0 < sc.groups; g0 += 32) {
+        for (int g0 = 0; g0 < gr.n; g0 += 32) {
             const int g = g0 + lane;
             int nt = 0;
-            if (g < sc.groups) {
-                int ng, e = 0;
-                if (p.mode == kDense) {
-                    ng = p.T;
-                    g_rec[g] = 0;
-                    g_row0[g] = 0;
-                } else {
-                    e = p.act[g];
-                    ng = p.hist[e];
-                    g_rec[g] = p.indexed_by_act ? g : e;
-                    g_row0[g] = p.off[e];
-                }
+            if (g < gr.n) {
+                const int e = p.act[g];
+                const int ng = p.hist[e];
+                g_rec[g] = p.indexed_by_act ? g : e;
+                g_row0[g] = p.off[e];
                 g_ng[g] = ng;
-                nt = ((ng + BN - 1) / BN) * sc.m_tiles;
+                nt = (ng + BN - 1) / BN;
                 mx = max(mx, (min(ng, BN) + 15) & ~15);
             }
             int incl = nt;
@@ -264,14 +309,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
                 const int v = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += v;
             }
-            if (g < sc.groups) prefix[g] = run + incl - nt;
+            if (g < gr.n) ntp[g] = run + incl - nt;
             run += __shfl_sync(0xffffffffu, incl, 31);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (lane == 0) {
-            prefix[sc.groups] = run;
+            ntp[gr.n] = run;
             s_flag[1] = mx;
+            s_flag[2] = run;
         }
     }
     if (warp == 1) {  // TMEM: two accumulator stages of BN fp32 columns
@@ -292,21 +338,39 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid == 96) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&amap) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&bmap) : "memory");
+        for (int i = 0; i < p.nphase; ++i) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(amaps[i]) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(bmaps[i]) : "memory");
+        }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    sc.tiles = prefix[sc.groups];
-    sc.max_npad = s_flag[1];
-    {
+    const int max_npad_expert = s_flag[1], ntiles_expert = s_flag[2];
+
+    PhaseSched ps[kMaxPhases];
+    long long total_units = 0;
+    for (int i = 0; i < p.nphase; ++i) {
+        PhaseSched &sc = ps[i];
+        sc.mode = p.ph[i].mode;
+        sc.M = p.ph[i].M;
+        sc.K = p.ph[i].K;
+        sc.m_tiles = sc.M / BM;
+        sc.kb_total = sc.K / BK;
+        int max_npad;
+        if (sc.mode == kDense) {
+            sc.tiles = (long long)((p.T + BN - 1) / BN) * sc.m_tiles;
+            max_npad = max(16, (min(p.T, BN) + 15) & ~15);
+        } else {
+            sc.tiles = (long long)ntiles_expert * sc.m_tiles;
+            max_npad = max_npad_expert;
+        }
         // Split K (a) to cover the SMs when there are fewer tiles than CTAs,
         // (b) to even out the last wave when a split of >= 8 k-blocks per unit
         // fills it >= 5% better.  The fix-up reads S x n partial columns per
         // row, so wide N tiles split less.
-        const int s_cap = max(1, min(sc.kb_total, 8 * 16 / min(BN, sc.max_npad)));
+        const int s_cap = max(1, min(sc.kb_total, 8 * 16 / min(BN, max_npad)));
         auto eff = [&](int c) {
             const long long u = sc.tiles * c;
             return (float)u / (float)(((u + gridDim.x - 1) / gridDim.x) * gridDim.x);
@@ -324,64 +388,97 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
         while (S > 1 && ((long long)sc.tiles * S * BN * BM > p.partial_cap || sc.tiles > kCounterInts)) --S;
         sc.kbs = (sc.kb_total + S - 1) / S;
         sc.S = (sc.kb_total + sc.kbs - 1) / sc.kbs;
+        sc.units = sc.tiles * sc.S;
+        sc.unit0 = total_units;
+        total_units += sc.units;
     }
-    sc.units = sc.tiles * sc.S;
+    int *phase_done = p.sync;
 
     if (warp == 0) {
-        // ================= TMA producer: weight tile + activation rows =====
+        // ================= TMA producer ====================================
+        // Weight tiles never depend on earlier work: they are issued as soon
+        // as a stage is free.  A phase's activation boxes wait for its gate —
+        // griddepcontrol.wait (PDL) for phase 0, the grid barrier on the
+        // previous phase otherwise — and are deferred (at most STAGES) until
+        // then, so the gate's latency overlaps weight streaming.
         if (lane == 0) {
             uint64_t policy;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-            // Weight tiles do not depend on the previous kernel: the first
-            // STAGES of them are issued before griddepcontrol.wait (PDL), the
-            // activation boxes of those stages right after it.
             int stage = 0;
             uint32_t phase = 0;
-            int pre_n = 0, pre_kb[STAGES], pre_row[STAGES], pre_np[STAGES];
-            bool waited = false;
-            for (long long u = blockIdx.x; u < sc.units; u += gridDim.x) {
-                const Unit x = decode_unit<BN>(p, sc, u);
+            int open_ph = -1;  // gates of phases <= open_ph are open
+            DeferredB dq[STAGES];
+            int nd = 0;
+            auto open_gate = [&](int ph, bool block) -> bool {
+                if (ph == 0) {
+                    if (!block) return false;
+                    pdl_wait();
+                    pdl_trigger();
+                    return true;
+                }
+                if (block) {
+                    while (ld_acquire(phase_done + ph - 1) < (int)gridDim.x) __nanosleep(64);
+                } else if (ld_acquire(phase_done + ph - 1) < (int)gridDim.x) {
+                    return false;
+                }
+                // phase ph-1's outputs were written through the generic proxy
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                return true;
+            };
+            auto flush = [&](int ph) {
+                for (int q = 0; q < nd; ++q)
+                    for (int j = 0; j < dq[q].npad; j += kBRowsPerBox)
+                        tma_load_2d(sB + dq[q].stage * kBBytes + j * 128, bmaps[ph], &full[dq[q].stage],
+                                    dq[q].kb * BK, dq[q].row + j);
+                nd = 0;
+            };
+            for (long long u = blockIdx.x; u < total_units; u += gridDim.x) {
+                const Unit x = decode_unit<BN>(ps, p.nphase, gr, u);
+                while (open_ph < x.ph - 1) {  // an earlier gate must open first
+                    open_gate(open_ph + 1, true);
+                    flush(open_ph + 1);
+                    ++open_ph;
+                }
                 const int brow = x.row0 + x.n0;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
-                    if (!waited && pre_n == STAGES) {
-                        pdl_wait();
-                        pdl_trigger();
-                        waited = true;
-                        for (int q = 0; q < pre_n; ++q)
-                            for (int j = 0; j < pre_np[q]; j += kBRowsPerBox)
-                                tma_load_2d(sB + q * kBBytes + j * 128, &bmap, &full[q], pre_kb[q] * BK, pre_row[q] + j);
-                    }
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], kABytes + x.n_pad * 128);
-                    tma_load_3d(sA + stage * kABytes, &amap, &full[stage], kb * BK, x.m_tile * BM, x.rec, policy);
-                    if (waited) {
+                    tma_load_3d(sA + stage * kABytes, amaps[x.ph], &full[stage], kb * BK, x.m_tile * BM, x.rec,
+                                policy);
+                    if (open_ph < x.ph && open_gate(x.ph, false)) {
+                        flush(x.ph);
+                        open_ph = x.ph;
+                    }
+                    if (open_ph >= x.ph) {
                         for (int j = 0; j < x.n_pad; j += kBRowsPerBox)
-                            tma_load_2d(sB + stage * kBBytes + j * 128, &bmap, &full[stage], kb * BK, brow + j);
+                            tma_load_2d(sB + stage * kBBytes + j * 128, bmaps[x.ph], &full[stage], kb * BK,
+                                        brow + j);
                     } else {
-                        pre_kb[pre_n] = kb;
-                        pre_row[pre_n] = brow;
-                        pre_np[pre_n] = x.n_pad;
-                        ++pre_n;
+                        dq[nd++] = {stage, kb, brow, x.n_pad};
+                        if (nd == STAGES) {  // every stage waits on the gate now
+                            open_gate(x.ph, true);
+                            flush(x.ph);
+                            open_ph = x.ph;
+                        }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
-            if (!waited) {
+            if (nd > 0) {
+                open_gate(open_ph + 1, true);
+                flush(open_ph + 1);
+            }
+            if (open_ph < 0) {  // no phase-0 work here: still honour PDL before exiting
                 pdl_wait();
                 pdl_trigger();
-                for (int q = 0; q < pre_n; ++q)
-                    for (int j = 0; j < pre_np[q]; j += kBRowsPerBox)
-                        tma_load_2d(sB + q * kBBytes + j * 128, &bmap, &full[q], pre_kb[q] * BK, pre_row[q] + j);
             }
-        } else {
-            pdl_wait();  // the rest of warp 0 has nothing to do, but keep semantics uniform
         }
     } else if (warp == 1) {
         // ================= MMA issuer (single thread) ======================
         int stage = 0, cnt = 0;
         uint32_t phase = 0;
-        for (long long u = blockIdx.x; u < sc.units; u += gridDim.x, ++cnt) {
-            const Unit x = decode_unit<BN>(p, sc, u);
+        for (long long u = blockIdx.x; u < total_units; u += gridDim.x, ++cnt) {
+            const Unit x = decode_unit<BN>(ps, p.nphase, gr, u);
             const int acc = cnt & 1;
             mbar_wait(&tempty[acc], ((cnt >> 1) & 1) ^ 1);
             tc_fence_after();
@@ -391,11 +488,11 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t a0 = smem_u32(sA + stage * kABytes);
-                    const uint32_t b0 = smem_u32(sB + stage * kBBytes);
+                    const uint32_t a_s = smem_u32(sA + stage * kABytes);
+                    const uint32_t b_s = smem_u32(sB + stage * kBBytes);
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk)
-                        umma_bf16(tmem_d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc,
+                        umma_bf16(tmem_d, sw128_desc(a_s + kk * 32), sw128_desc(b_s + kk * 32), idesc,
                                   (kb > x.kb0 || kk > 0) ? 1u : 0u);
                     umma_commit(&empty[stage]);
                 }
@@ -409,9 +506,19 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
         // ================= epilogue: TMEM -> registers -> global ===========
         const int q = warp & 3;        // TMEM lane quarter this warp may access
         const int et = q * 32 + lane;  // accumulator row 0..127
-        int cnt = 0;
-        for (long long u = blockIdx.x; u < sc.units; u += gridDim.x, ++cnt) {
-            const Unit x = decode_unit<BN>(p, sc, u);
+        int cnt = 0, signalled = 0;    // phases [0, signalled) reported done
+        auto signal_upto = [&](int ph_end) {
+            for (; signalled < ph_end; ++signalled) {
+                __threadfence();
+                named_sync(1, 128);
+                if (et == 0) atomicAdd(phase_done + signalled, 1);
+            }
+        };
+        for (long long u = blockIdx.x; u < total_units; u += gridDim.x, ++cnt) {
+            const Unit x = decode_unit<BN>(ps, p.nphase, gr, u);
+            signal_upto(x.ph);
+            const PhaseDesc &pd = p.ph[x.ph];
+            const PhaseSched &sc = ps[x.ph];
             const int acc = cnt & 1;
             mbar_wait(&tfull[acc], (cnt >> 1) & 1);
             tc_fence_after();
@@ -423,7 +530,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
                     tmem_ld16(taddr + c0, v);
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        if (c0 + j < x.n_valid) store_out<BN>(p, x, c0 + j, m, v[j]);
+                        if (c0 + j < x.n_valid) store_out(p, pd, x, c0 + j, m, v[j]);
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[acc]);
@@ -458,13 +565,14 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
                         }
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
-                            if (n0 + j < x.n_valid) store_out<BN>(p, x, n0 + j, m, a4[j]);
+                            if (n0 + j < x.n_valid) store_out(p, pd, x, n0 + j, m, a4[j]);
                     }
                     if (et == 0) p.counters[x.tile] = 0;
                 }
                 named_sync(1, 128);
             }
         }
+        signal_upto(p.nphase);
     }
     tc_fence_before();
     __syncthreads();
@@ -472,6 +580,14 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
         tc_fence_after();
         constexpr uint32_t cols = (2 * BN < 32) ? 32 : 2 * BN;
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
+    }
+    if (tid == 0) {  // the last CTA out re-arms the phase barriers for the next launch
+        __threadfence();
+        if (atomicAdd(p.sync + kMaxPhases, 1) == (int)gridDim.x - 1) {
+            for (int i = 0; i < kMaxPhases; ++i) p.sync[i] = 0;
+            p.sync[kMaxPhases] = 0;
+            __threadfence();
+        }
     }
 }
 
@@ -563,32 +679,40 @@ static int make_bmap(CUtensorMap *map, const void *base, int K, int rows) {
     return PGMOE_OK;
 }
 
+struct PhaseMaps {
+    CUtensorMap a, b;
+};
+
 template <int BN, int STAGES>
-static int launch(const CUtensorMap &amap, const CUtensorMap &bmap, const Params &p, cudaStream_t s) {
+static int launch(const PhaseMaps *mp, const Params &p, cudaStream_t s) {
     constexpr size_t smem = smem_bytes<BN, STAGES>();
     static_assert(smem <= 227 * 1024, "shared memory budget");
     static bool attr = false;
     if (!attr) {
-        PG_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        PG_CUDA(cudaFuncSetAttribute(block_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
         attr = true;
     }
-    PG_CUDA(launch_pdl(grouped_gemm_kernel<BN, STAGES>, dim3(kNumSMs), dim3(kThreads), smem, s, amap, bmap, p));
+    // unused phase slots repeat phase 0's maps (never dereferenced)
+    const PhaseMaps &m0 = mp[0], &m1 = p.nphase > 1 ? mp[1] : mp[0], &m2 = p.nphase > 2 ? mp[2] : mp[0];
+    PG_CUDA(launch_pdl(block_gemm_kernel<BN, STAGES>, dim3(kNumSMs), dim3(kThreads), smem, s, m0.a, m0.b, m1.a, m1.b,
+                       m2.a, m2.b, p));
     count_launch();
     return PGMOE_OK;
 }
 
 // BN: widest N tile.  Token groups wider than BN are split into N tiles
 // (each re-reads its weight tile), so BN follows the expected tokens per
-// expert: 64 covers decode batches, 256 the compute-bound stress shapes.
-static int run(const CUtensorMap &amap, const CUtensorMap &bmap, Params p, int bn, void *ws, size_t ws_bytes,
-               cudaStream_t s) {
-    PG_REQUIRE(ws_bytes > kCounterInts * 4 + 4096, PGMOE_E_CONFIG, "tcgen05 workspace too small");
+// group: 64 covers decode batches, 256 the compute-bound stress shapes.
+static int run(const PhaseMaps *mp, Params p, int bn, void *ws, size_t ws_bytes, cudaStream_t s) {
+    const size_t head = (size_t)(kCounterInts + kSyncInts) * 4;
+    PG_REQUIRE(ws_bytes > head + 4096, PGMOE_E_CONFIG, "tcgen05 workspace too small");
     p.counters = static_cast<int *>(ws);
-    p.partial = reinterpret_cast<float *>(static_cast<char *>(ws) + kCounterInts * 4);
-    p.partial_cap = (long long)((ws_bytes - kCounterInts * 4) / 4);
-    if (bn <= 64) return launch<64, 8>(amap, bmap, p, s);
-    return launch<256, 4>(amap, bmap, p, s);
+    p.sync = p.counters + kCounterInts;
+    p.partial = reinterpret_cast<float *>(static_cast<char *>(ws) + head);
+    p.partial_cap = (long long)((ws_bytes - head) / 4);
+    if (bn <= 64) return launch<64, 8>(mp, p, s);
+    return launch<256, 4>(mp, p, s);
 }
 
 static int launch_grid(long long work) {
@@ -607,39 +731,53 @@ int tc_pack_rows(const float *x, const int *perm, int n, int d, int k, uint16_t 
     return PGMOE_OK;
 }
 
-int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
-                   const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, void *ws,
-                   size_t ws_bytes, cudaStream_t s, bool xb_ready) {
+// One launch for a block's expert FFN (up, down) and — when `dense_w` is
+// given and top_k == 1 — its dense layer: phases separated by in-kernel grid
+// barriers.  `xb_ready`: the packed bf16 operand was already written (by the
+// previous block's dense epilogue).  next_xb/next_inv: see Params.
+int block_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
+             const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, bool xb_ready,
+             const void *dense_w, float *y, uint16_t *next_xb, const int *next_inv, void *ws, size_t ws_bytes,
+             cudaStream_t s) {
     PG_REQUIRE(tc_supported(d, f), PGMOE_E_CONFIG, "tcgen05 path needs d, f multiples of 128 and f >= d");
     PG_REQUIRE((reinterpret_cast<uintptr_t>(experts) & 15) == 0 && stride % 16 == 0, PGMOE_E_CONFIG,
                "expert records must be 16-byte aligned");
+    PG_REQUIRE(dense_w == nullptr || (k == 1 && mixb != nullptr), PGMOE_E_CONFIG,
+               "the fused dense phase needs top_k == 1 (mix written by the down projection)");
     const int n = T * k;
     // Records addressed through the map are < E (resident) or < n_act (slot
     // cache), both <= 1024; the extent only bounds TMA address generation.
     const int rec_extent = 1024;
-    const int bn = (n >= 2048) ? 256 : 64;
     if (!xb_ready) PG_TRY(tc_pack_rows(x, r->perm, n, d, k, xb, s));
     tc::Params p{};
     p.T = T;
     p.k = k;
     p.act = r->act; p.n_act = r->n_act; p.off = r->off; p.hist = r->hist; p.perm = r->perm; p.w_perm = r->w_perm;
     p.indexed_by_act = indexed_by_act;
-    CUtensorMap wmap, bmap;
-    PG_TRY(tc::make_wmap(&wmap, experts, d, f, rec_extent, stride));
-    PG_TRY(tc::make_bmap(&bmap, xb, d, n));
-    p.mode = tc::kUp;
-    p.M = f;
-    p.K = d;
-    p.out_bf16 = hb;
-    PG_TRY(tc::run(wmap, bmap, p, bn, ws, ws_bytes, s));
-    PG_TRY(tc::make_wmap(&wmap, static_cast<const char *>(experts) + (size_t)f * d * 2, f, d, rec_extent, stride));
-    PG_TRY(tc::make_bmap(&bmap, hb, f, n));
-    p.mode = tc::kDown;
-    p.M = d;
-    p.K = f;
-    p.out_f32 = yw;
-    p.out_bf16 = (k == 1) ? mixb : nullptr;
-    return tc::run(wmap, bmap, p, bn, ws, ws_bytes, s);
+    tc::PhaseMaps mp[3];
+    PG_TRY(tc::make_wmap(&mp[0].a, experts, d, f, rec_extent, stride));
+    PG_TRY(tc::make_bmap(&mp[0].b, xb, d, n));
+    p.ph[0] = {tc::kUp, f, d, nullptr, hb};
+    PG_TRY(tc::make_wmap(&mp[1].a, static_cast<const char *>(experts) + (size_t)f * d * 2, f, d, rec_extent, stride));
+    PG_TRY(tc::make_bmap(&mp[1].b, hb, f, n));
+    p.ph[1] = {tc::kDown, d, f, yw, (k == 1) ? mixb : nullptr};
+    p.nphase = 2;
+    if (dense_w) {
+        PG_TRY(tc::make_wmap(&mp[2].a, dense_w, d, d, 1, (size_t)d * d * 2));
+        PG_TRY(tc::make_bmap(&mp[2].b, mixb, d, T));
+        p.ph[2] = {tc::kDense, d, d, y, nullptr};
+        p.nphase = 3;
+        p.next_xb = next_xb;
+        p.next_inv = next_inv;
+    }
+    return tc::run(mp, p, (n >= 2048) ? 256 : 64, ws, ws_bytes, s);
+}
+
+int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
+                   const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, void *ws,
+                   size_t ws_bytes, cudaStream_t s, bool xb_ready) {
+    return block_tc(x, T, d, f, k, experts, stride, indexed_by_act, r, xb, hb, yw, mixb, xb_ready, nullptr, nullptr,
+                    nullptr, nullptr, ws, ws_bytes, s);
 }
 
 int dense_tc2(const float *yw, const uint16_t *mixb_ready, int T, int d, int k, const void *dense_w, float *y,
@@ -656,18 +794,16 @@ int dense_tc2(const float *yw, const uint16_t *mixb_ready, int T, int d, int k, 
         mixb = mixb_scratch;
     }
     tc::Params p{};
-    p.mode = tc::kDense;
-    p.M = d;
-    p.K = d;
     p.T = T;
     p.k = k;
-    p.out_f32 = y;
+    p.nphase = 1;
+    p.ph[0] = {tc::kDense, d, d, y, nullptr};
     p.next_xb = next_xb;
     p.next_inv = next_inv;
-    CUtensorMap wmap, bmap;
-    PG_TRY(tc::make_wmap(&wmap, dense_w, d, d, 1, (size_t)d * d * 2));
-    PG_TRY(tc::make_bmap(&bmap, mixb, d, T));
-    return tc::run(wmap, bmap, p, T >= 2048 ? 256 : 64, ws, ws_bytes, s);
+    tc::PhaseMaps mp[1];
+    PG_TRY(tc::make_wmap(&mp[0].a, dense_w, d, d, 1, (size_t)d * d * 2));
+    PG_TRY(tc::make_bmap(&mp[0].b, mixb, d, T));
+    return tc::run(mp, p, T >= 2048 ? 256 : 64, ws, ws_bytes, s);
 }
 
 // Entry points with the fp32-scratch signatures: the bf16 operands live in

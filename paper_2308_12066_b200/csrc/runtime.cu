@@ -115,6 +115,7 @@ struct pgmoe_model {
     };
     GraphEntry graphs[8];  // small LRU: callers' output buffers rotate through the allocator
     unsigned long long graph_clock = 0;
+    int64_t fused_blocks = 0;  // blocks whose dense layer ran inside the expert launch
     // host-buffer entry point
     cudaStream_t io_stream = nullptr;
     float *io_x = nullptr, *io_y = nullptr, *io_w = nullptr;
@@ -398,22 +399,40 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
         const void *experts = off ? (const void *)(m->slots + (size_t)ri * m->slot_capacity)
                                   : (const void *)bw.experts;
         if (off) PG_CUDA(cudaStreamWaitEvent(s, m->ready[ri], 0));
-        tl_begin(m, "compute", "experts", b, s);
-        PG_TRY(run_ffn(m, cur, T, experts, (off && !prefetch_all) ? 1 : 0, &rb.r, s, xb_ready));
-        tl_end(m, s);
-        if (off) {
-            PG_CUDA(cudaEventRecord(m->done[ri], s));
-            if (!m->ffn_b.empty()) PG_CUDA(cudaEventRecord(m->ffn_b[b], s));
-        }
         float *nxt = (b == nb - 1) ? y_out : m->act_buf[b & 1];
-        tl_begin(m, "compute", "non_moe", b, s);
         // Pre-gating at work: block b+1's routing is already on the device
-        // (unless b+1 carries a conventional gate), so this dense layer also
-        // writes b+1's packed up-projection operand and b+1 skips the pack.
+        // (unless b+1 carries a conventional gate), so this block's dense
+        // epilogue also writes b+1's packed up-projection operand.
         const bool fuse_next = use_tc(m) && b + 1 < nb && !has_conv_gate(c, b + 1);
-        PG_TRY(run_dense(m, T, bw.dense, nxt, s, fuse_next ? &m->routing[(b + 1) % R].r : nullptr));
+        const pgmoe_routing *next_r = fuse_next ? &m->routing[(b + 1) % R].r : nullptr;
+        const int indexed = (off && !prefetch_all) ? 1 : 0;
+        if (use_tc(m) && c.top_k == 1) {
+            // one launch: up, down(+combine), dense — phases behind grid barriers
+            tl_begin(m, "compute", "experts", b, s);
+            PG_TRY(block_tc(cur, T, c.d_model, c.d_ff, 1, experts, m->rec_bytes, indexed, &rb.r, m->xb, m->hb, m->yw,
+                            m->mixb, xb_ready, bw.dense, nxt, next_r ? m->xb : nullptr, next_r ? next_r->inv : nullptr,
+                            m->tc_ws, m->tc_ws_bytes, s));
+            tl_end(m, s);
+            if (off) {
+                PG_CUDA(cudaEventRecord(m->done[ri], s));
+                if (!m->ffn_b.empty()) PG_CUDA(cudaEventRecord(m->ffn_b[b], s));
+            }
+            tl_begin(m, "compute", "non_moe", b, s);  // fused into the launch above
+            tl_end(m, s);
+            m->fused_blocks++;
+        } else {
+            tl_begin(m, "compute", "experts", b, s);
+            PG_TRY(run_ffn(m, cur, T, experts, indexed, &rb.r, s, xb_ready));
+            tl_end(m, s);
+            if (off) {
+                PG_CUDA(cudaEventRecord(m->done[ri], s));
+                if (!m->ffn_b.empty()) PG_CUDA(cudaEventRecord(m->ffn_b[b], s));
+            }
+            tl_begin(m, "compute", "non_moe", b, s);
+            PG_TRY(run_dense(m, T, bw.dense, nxt, s, next_r));
+            tl_end(m, s);
+        }
         xb_ready = fuse_next;
-        tl_end(m, s);
         if (ids_trace) {
             PG_CUDA(cudaMemcpyAsync(ids_trace + (size_t)b * tk, rb.r.ids, tk * 4, cudaMemcpyDeviceToDevice, s));
             PG_CUDA(cudaMemcpyAsync(w_trace + (size_t)b * tk, rb.r.w, tk * 4, cudaMemcpyDeviceToDevice, s));
@@ -1011,6 +1030,7 @@ extern "C" int pgmoe_model_stats(pgmoe_model *m, pgmoe_stats *out) {
     }
     m->stats.route_fallbacks = fb;
     m->stats.route_flips = 0;
+    m->stats.fused_blocks = m->fused_blocks;
     *out = m->stats;
     return PGMOE_OK;
 }
@@ -1023,6 +1043,7 @@ extern "C" int pgmoe_model_reset_stats(pgmoe_model *m) {
     m->stats.pinned_hbm_bytes = pinned;
     m->stats.slot_capacity_bytes = slot;
     m->stats.cache_bytes = cb;
+    m->fused_blocks = 0;
     return PGMOE_OK;
 }
 
