@@ -507,6 +507,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         const int q = warp & 3;        // TMEM lane quarter this warp may access
         const int et = q * 32 + lane;  // accumulator row 0..127
         int cnt = 0, signalled = 0;    // phases [0, signalled) reported done
+        // The previous launch's last CTA re-arms the phase counters on its way
+        // out; with programmatic dependent launch this grid may already be
+        // running, so no signal may precede griddepcontrol.wait.
+        pdl_wait();
         auto signal_upto = [&](int ph_end) {
             for (; signalled < ph_end; ++signalled) {
                 __threadfence();
