@@ -255,6 +255,12 @@ PGMOE_API const char *pgmoe_last_error(void);
 PGMOE_API const char *pgmoe_version(void);
 /* Kernels this library has launched since load (benchmark evidence). */
 PGMOE_API int64_t pgmoe_launch_count(void);
+/* Debug only (no reference counterpart): install a device buffer of
+ * [rows][16] uint64 that kernels of `kind` (0 route, 1 tcgen05 block kernel)
+ * stamp with %globaltimer at fixed points, one row per CTA, consecutive
+ * launches taking consecutive rows (wrapping); nullptr disables.  Launches
+ * enqueued (or graphs captured) while installed keep writing to it. */
+PGMOE_API int pgmoe_debug_set_probe(int32_t kind, void *device_buffer, int64_t rows);
 
 #ifdef __cplusplus
 }

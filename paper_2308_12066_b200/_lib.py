@@ -66,7 +66,7 @@ EXPORTS = (
     "pgmoe_launch_count", "pgmoe_model_create_ex", "pgmoe_model_expert_records", "pgmoe_gather_rows",
     "pgmoe_unpermute_combine", "pgmoe_ep_local_routing", "pgmoe_model_config", "pgmoe_weight_file_config",
     "pgmoe_model_load_pgmoe1", "pgmoe_model_save_pgmoe1", "pgmoe_model_set_strategy", "pgmoe_model_set_cache",
-    "pgmoe_cache_replay",
+    "pgmoe_cache_replay", "pgmoe_debug_set_probe",
 )
 
 _lib = None
@@ -120,6 +120,7 @@ def load():
         "pgmoe_weight_file_config": (i32, [ctypes.c_char_p, P(Config)]),
         "pgmoe_model_load_pgmoe1": (i32, [vp, ctypes.c_char_p]),
         "pgmoe_model_save_pgmoe1": (i32, [vp, ctypes.c_char_p]),
+        "pgmoe_debug_set_probe": (i32, [i32, vp, i64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

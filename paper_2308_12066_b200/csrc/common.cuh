@@ -79,6 +79,19 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// Debug probes (tools/probe.py): per-CTA %globaltimer stamps written when a
+// probe buffer is installed with pgmoe_debug_set_probe(); null otherwise.
+constexpr int kProbeSlots = 32;
+unsigned long long *probe_buffer(int kind, int ctas);  // 0: route, 1: tcgen05 block kernel
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void probe(unsigned long long *buf, int cta, int slot) {
+    if (buf) buf[(size_t)cta * kProbeSlots + slot] = gtimer();
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

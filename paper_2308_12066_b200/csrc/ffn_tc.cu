@@ -52,6 +52,11 @@ constexpr int kMaxGroups = 1024;
 constexpr int kMaxPhases = 3;
 constexpr int kCounterInts = 8192;    // split-K tile tickets at the head of the workspace
 constexpr int kSyncInts = 16;         // phase barriers + exit ticket, after the tickets
+constexpr int kMetaInts = 512;        // per-column epilogue metadata staged in shared memory
+// split-K cost model (bytes per microsecond; microseconds)
+constexpr float kSmBytesPerUs = 150e3f;   // one SM's TMA stream when few CTAs load
+constexpr float kHbmBytesPerUs = 6.5e6f;  // whole-chip HBM stream
+constexpr float kFixUs = 3.0f;            // split-K fix-up chain
 
 enum Mode { kUp = 0, kDown = 1, kDense = 2 };
 
@@ -76,6 +81,7 @@ struct Params {
     int *sync;       // [kSyncInts] phase_done[kMaxPhases], exit ticket
     float *partial;
     long long partial_cap;  // floats
+    unsigned long long *probe;  // debug stamps [grid][kProbeSlots] or null
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -226,22 +232,97 @@ __device__ __forceinline__ Unit decode_unit(const PhaseSched *ps, int nphase, co
     return x;
 }
 
-__device__ __forceinline__ void store_out(const Params &p, const PhaseDesc &pd, const Unit &x, int n, int m,
-                                          float v) {
-    const int col = x.n0 + n;
-    if (pd.mode == kUp) {
-        pd.out_bf16[(size_t)(x.row0 + col) * pd.M + m] = bf16_bits(fmaxf(v, 0.f));  // relu, linalg.py:41-42
-    } else if (pd.mode == kDown) {
-        const int r = x.row0 + col;
-        const int dst = __ldg(p.perm + r);
-        const float y = __ldg(p.w_perm + r) * v;  // combine weight (linalg.py:45-51)
-        pd.out_f32[(size_t)dst * pd.M + m] = y;
-        if (pd.out_bf16) pd.out_bf16[(size_t)dst * pd.M + m] = bf16_bits(y);  // top-1: mix == w*y
+// Epilogue stores.  Everything a stored column needs is in registers before
+// the first store of a 16-column chunk: the per-unit constants (EpiRegs,
+// loaded once per unit) and the per-column metadata (down: destination token
+// and combine weight; dense: the next block's packed rows), which the
+// epilogue threads stage in shared memory together while the MMA runs and
+// each thread then reads for its chunk in one batch.  (Reading them between
+// stores would serialise: every st.global is a compiler memory barrier, so
+// shared-memory values would be re-read, one dependent LDS chain per
+// column — measured at ~0.2 us per column.)
+struct EpiRegs {
+    int mode, M, k;
+    bool staged;
+    float *out_f32;
+    uint16_t *out_bf16;
+    uint16_t *next_xb;
+    const int *perm, *next_inv;
+    const float *w_perm;
+};
+
+__device__ __forceinline__ EpiRegs epi_regs(const Params &p, const PhaseDesc &pd, const Unit &x) {
+    EpiRegs e;
+    e.mode = pd.mode;
+    e.M = pd.M;
+    e.k = p.k;
+    e.out_f32 = pd.out_f32;
+    e.out_bf16 = pd.out_bf16;
+    e.next_xb = pd.mode == kDense ? p.next_xb : nullptr;
+    e.perm = p.perm;
+    e.w_perm = p.w_perm;
+    e.next_inv = p.next_inv;
+    e.staged = (e.mode == kDown && x.n_valid <= kMetaInts / 2) ||
+               (e.mode == kDense && e.next_xb != nullptr && x.n_valid * e.k <= kMetaInts);
+    return e;
+}
+
+__device__ __forceinline__ void stage_meta(const EpiRegs &e, const Unit &x, int et, int *mi, float *mf) {
+    if (!e.staged) return;
+    if (e.mode == kDown) {
+        for (int c = et; c < x.n_valid; c += 128) {
+            const int r = x.row0 + x.n0 + c;
+            mi[c] = __ldg(e.perm + r);
+            mf[c] = __ldg(e.w_perm + r);
+        }
     } else {
-        pd.out_f32[(size_t)col * pd.M + m] = v;
-        if (p.next_xb) {
-            const uint16_t b = bf16_bits(v);
-            for (int s = 0; s < p.k; ++s) p.next_xb[(size_t)__ldg(p.next_inv + (size_t)col * p.k + s) * pd.M + m] = b;
+        for (int c = et; c < x.n_valid * e.k; c += 128) mi[c] = __ldg(e.next_inv + (size_t)x.n0 * e.k + c);
+    }
+}
+
+// Columns [c0, c0 + 16) of accumulator row m (only those < x.n_valid).
+__device__ __forceinline__ void store_chunk(const EpiRegs &e, const Unit &x, int c0, int m, const float (&v)[16],
+                                            const int *mi, const float *mf) {
+    const int nv = min(16, x.n_valid - c0);
+    if (e.mode == kUp) {
+        uint16_t *o = e.out_bf16 + (size_t)(x.row0 + x.n0 + c0) * e.M + m;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < nv) __stcg(o + (size_t)j * e.M, bf16_bits(fmaxf(v[j], 0.f)));  // relu, linalg.py:41-42
+    } else if (e.mode == kDown) {
+        int dst[16];
+        float w[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int r = x.row0 + x.n0 + c0 + j;
+            dst[j] = j < nv ? (e.staged ? mi[c0 + j] : __ldg(e.perm + r)) : 0;
+            w[j] = j < nv ? (e.staged ? mf[c0 + j] : __ldg(e.w_perm + r)) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (j < nv) {
+                const float y = w[j] * v[j];  // combine weight (linalg.py:45-51)
+                __stcg(e.out_f32 + (size_t)dst[j] * e.M + m, y);
+                if (e.out_bf16) __stcg(e.out_bf16 + (size_t)dst[j] * e.M + m, bf16_bits(y));  // top-1: mix == w*y
+            }
+        }
+    } else {
+        float *o = e.out_f32 + (size_t)(x.n0 + c0) * e.M + m;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < nv) __stcg(o + (size_t)j * e.M, v[j]);
+        if (e.next_xb) {
+            for (int s = 0; s < e.k; ++s) {
+                int row[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int idx = (c0 + j) * e.k + s;
+                    row[j] = j < nv ? (e.staged ? mi[idx] : __ldg(e.next_inv + (size_t)x.n0 * e.k + idx)) : 0;
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (j < nv) __stcg(e.next_xb + (size_t)row[j] * e.M + m, bf16_bits(v[j]));
+            }
         }
     }
 }
@@ -254,10 +335,25 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
 block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant__ CUtensorMap b0,
                   const __grid_constant__ CUtensorMap a1, const __grid_constant__ CUtensorMap b1,
-                  const __grid_constant__ CUtensorMap a2, const __grid_constant__ CUtensorMap b2, Params p) {
+                  const __grid_constant__ CUtensorMap a2, const __grid_constant__ CUtensorMap b2,
+                  const Params p_in) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                                            ~uintptr_t(1023));
+    // Kernel parameters live in the constant bank; the epilogue indexes the
+    // phase descriptors dynamically and, under register pressure, the
+    // compiler re-reads them per stored column (indexed LDC, slow on a miss).
+    // One copy in shared memory makes every such read an LDS.
+    __shared__ Params p_sh;
+    __shared__ PhaseSched ps[kMaxPhases];
+    __shared__ long long s_total_units;
+    static_assert(sizeof(Params) % 4 == 0 && sizeof(Params) / 4 <= kThreads, "Params copy");
+    if (threadIdx.x < sizeof(Params) / 4)
+        reinterpret_cast<int *>(&p_sh)[threadIdx.x] = reinterpret_cast<const int *>(&p_in)[threadIdx.x];
+    __syncthreads();
+    const Params &p = p_sh;
+    // 1024-byte alignment by pointer arithmetic on the shared array (an
+    // integer round trip would lose the state space and turn every shared
+    // access below into a generic one that must order against global stores)
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int kBBytes = BN * 128;
     unsigned char *sA = smem;
     unsigned char *sB = smem + STAGES * kABytes;
@@ -271,10 +367,16 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
     int *g_rec = ntp + kMaxGroups + 1;
     int *g_row0 = g_rec + kMaxGroups;
     int *g_ng = g_row0 + kMaxGroups;
+    int *meta_i = g_ng + kMaxGroups;                            // [kMetaInts]
+    float *meta_f = reinterpret_cast<float *>(meta_i + kMetaInts);  // [kMetaInts / 2]
     const CUtensorMap *amaps[3] = {&a0, &a1, &a2};
     const CUtensorMap *bmaps[3] = {&b0, &b1, &b2};
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        probe(p.probe, blockIdx.x, 0);  // entry
+        if (p.probe) p.probe[(size_t)blockIdx.x * kProbeSlots + 21] = clock64();
+    }
     bool has_expert_phase = false, has_dense = false;
     for (int i = 0; i < p.nphase; ++i) {
         has_expert_phase |= p.ph[i].mode != kDense;
@@ -283,7 +385,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
 
     // ---- schedule (identical in every CTA) --------------------------------
     Groups gr;
-    gr.n = has_expert_phase ? *p.n_act : 0;
+    gr.n = has_expert_phase ? __ldg(p.n_act) : 0;
     gr.T = p.T;
     gr.ntp = ntp;
     gr.rec = g_rec;
@@ -295,10 +397,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             const int g = g0 + lane;
             int nt = 0;
             if (g < gr.n) {
-                const int e = p.act[g];
-                const int ng = p.hist[e];
+                const int e = __ldg(p.act + g);
+                const int ng = __ldg(p.hist + e);
                 g_rec[g] = p.indexed_by_act ? g : e;
-                g_row0[g] = p.off[e];
+                g_row0[g] = __ldg(p.off + e);
                 g_ng[g] = ng;
                 nt = (ng + BN - 1) / BN;
                 mx = max(mx, (min(ng, BN) + 15) & ~15);
@@ -347,9 +449,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (tid == 0) probe(p.probe, blockIdx.x, 1);  // prologue done
     const int max_npad_expert = s_flag[1], ntiles_expert = s_flag[2];
 
-    PhaseSched ps[kMaxPhases];
+    if (tid == 0) {
     long long total_units = 0;
     for (int i = 0; i < p.nphase; ++i) {
         PhaseSched &sc = ps[i];
@@ -366,24 +469,24 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             sc.tiles = (long long)ntiles_expert * sc.m_tiles;
             max_npad = max_npad_expert;
         }
-        // Split K (a) to cover the SMs when there are fewer tiles than CTAs,
-        // (b) to even out the last wave when a split of >= 8 k-blocks per unit
-        // fills it >= 5% better.  The fix-up reads S x n partial columns per
-        // row, so wide N tiles split less.
+        // Split K only when it pays for its fix-up.  A split-K tile costs one
+        // extra dependent chain (partials out, fence + ticket, partials in:
+        // ~kFixUs) but spreads the tile's K stream over S CTAs.  Streaming
+        // time of a unit = its bytes / per-CTA bandwidth, where the per-CTA
+        // bandwidth is the single-SM TMA limit when few CTAs stream and the
+        // HBM share when all do (measured on B200 with tools/probe.py).
         const int s_cap = max(1, min(sc.kb_total, 8 * 16 / min(BN, max_npad)));
-        auto eff = [&](int c) {
-            const long long u = sc.tiles * c;
-            return (float)u / (float)(((u + gridDim.x - 1) / gridDim.x) * gridDim.x);
-        };
+        const float kb_bytes = (float)(kABytes + max_npad * 128);
         int S = 1;
-        if (sc.tiles > 0 && sc.tiles < (long long)gridDim.x) {
-            float best = eff(1);
-            for (int cand = 2; cand <= s_cap; ++cand)
-                if (eff(cand) > best + 0.02f) { best = eff(cand); S = cand; }
-        } else if (sc.tiles > 0) {
-            float best = eff(1);
-            for (int cand = 2; cand <= s_cap && sc.kb_total / cand >= 8; ++cand)
-                if (eff(cand) > best + 0.05f) { best = eff(cand); S = cand; }
+        float best = 3.4e38f;
+        for (int cand = 1; cand <= s_cap && sc.tiles > 0; ++cand) {
+            const long long units = sc.tiles * cand;
+            const int kbs = (sc.kb_total + cand - 1) / cand;
+            const long long waves = (units + gridDim.x - 1) / gridDim.x;
+            const float active = (float)min(units, (long long)gridDim.x);
+            const float bw = fminf(kSmBytesPerUs, kHbmBytesPerUs / active);
+            const float t = (float)waves * kbs * kb_bytes / bw + (cand > 1 ? kFixUs : 0.f);
+            if (t < best * 0.98f) { best = t; S = cand; }
         }
         while (S > 1 && ((long long)sc.tiles * S * BN * BM > p.partial_cap || sc.tiles > kCounterInts)) --S;
         sc.kbs = (sc.kb_total + S - 1) / S;
@@ -392,6 +495,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         sc.unit0 = total_units;
         total_units += sc.units;
     }
+    s_total_units = total_units;
+    }
+    __syncthreads();
+    const long long total_units = s_total_units;
     int *phase_done = p.sync;
 
     if (warp == 0) {
@@ -414,6 +521,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                     if (!block) return false;
                     pdl_wait();
                     pdl_trigger();
+                    probe(p.probe, blockIdx.x, 2);  // phase-0 gate (PDL) open
                     return true;
                 }
                 if (block) {
@@ -421,6 +529,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                 } else if (ld_acquire(phase_done + ph - 1) < (int)gridDim.x) {
                     return false;
                 }
+                probe(p.probe, blockIdx.x, 2 + ph);  // phase-ph gate open
                 // phase ph-1's outputs were written through the generic proxy
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 return true;
@@ -472,6 +581,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                 pdl_wait();
                 pdl_trigger();
             }
+            probe(p.probe, blockIdx.x, 11);  // last load issued
         }
     } else if (warp == 1) {
         // ================= MMA issuer (single thread) ======================
@@ -515,31 +625,40 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             for (; signalled < ph_end; ++signalled) {
                 __threadfence();
                 named_sync(1, 128);
-                if (et == 0) atomicAdd(phase_done + signalled, 1);
+                if (et == 0) {
+                    probe(p.probe, blockIdx.x, 6 + signalled);  // this CTA's phase done
+                    atomicAdd(phase_done + signalled, 1);
+                }
             }
         };
         for (long long u = blockIdx.x; u < total_units; u += gridDim.x, ++cnt) {
             const Unit x = decode_unit<BN>(ps, p.nphase, gr, u);
             signal_upto(x.ph);
-            const PhaseDesc &pd = p.ph[x.ph];
-            const PhaseSched &sc = ps[x.ph];
+            const EpiRegs e = epi_regs(p, p.ph[x.ph], x);
+            const int S = ps[x.ph].S;
             const int acc = cnt & 1;
+            if (e.staged) {
+                named_sync(1, 128);  // the previous unit's readers are done
+                stage_meta(e, x, et, meta_i, meta_f);
+                named_sync(1, 128);
+            }
             mbar_wait(&tfull[acc], (cnt >> 1) & 1);
             tc_fence_after();
+            if (et == 0) probe(p.probe, blockIdx.x, cnt == 0 ? 5 : 12);  // first / last accumulator ready
             const int m = x.m_tile * BM + et;
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-            if (sc.S == 1) {
+            if (S == 1) {
                 for (int c0 = 0; c0 < x.n_valid; c0 += 16) {
                     float v[16];
                     tmem_ld16(taddr + c0, v);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (c0 + j < x.n_valid) store_out(p, pd, x, c0 + j, m, v[j]);
+                    if (et == 0 && c0 < 64) probe(p.probe, blockIdx.x, 23 + c0 / 8);  // chunk loaded from TMEM
+                    store_chunk(e, x, c0, m, v, meta_i, meta_f);
+                    if (et == 0 && c0 < 64) probe(p.probe, blockIdx.x, 24 + c0 / 8);  // chunk stored
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[acc]);
             } else {
-                float *part = p.partial + ((size_t)x.tile * sc.S + x.s) * (BN * BM);
+                float *part = p.partial + ((size_t)x.tile * S + x.s) * (BN * BM);
                 for (int c0 = 0; c0 < x.n_valid; c0 += 16) {
                     float v[16];
                     tmem_ld16(taddr + c0, v);
@@ -549,32 +668,46 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[acc]);  // accumulator free: the rest works from global
+                if (et == 0) probe(p.probe, blockIdx.x, 13);  // partials stored (last unit)
                 __threadfence();
                 named_sync(1, 128);
-                if (et == 0) s_flag[0] = (atomicAdd(p.counters + x.tile, 1) == sc.S - 1);
+                if (et == 0) s_flag[0] = (atomicAdd(p.counters + x.tile, 1) == S - 1);
                 named_sync(1, 128);
                 if (s_flag[0]) {
                     __threadfence();
-                    const float *base = p.partial + (size_t)x.tile * sc.S * (BN * BM) + et;
-                    for (int n0 = 0; n0 < x.n_valid; n0 += 4) {
-                        float a4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-                        for (int s = 0; s < sc.S; ++s) {  // split order: deterministic
-                            float v4[4];
+                    if (et == 0) probe(p.probe, blockIdx.x, 14);  // fix-up start (last unit)
+                    const float *base = p.partial + (size_t)x.tile * S * (BN * BM) + et;
+                    // 32 partial loads in flight per thread: 16 columns x 2
+                    // splits at a time, summed in split order (deterministic)
+                    for (int n0 = 0; n0 < x.n_valid; n0 += 16) {
+                        float a[16];
 #pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                v4[j] = (n0 + j < x.n_valid) ? __ldcg(base + ((size_t)s * BN + n0 + j) * BM) : 0.f;
+                        for (int j = 0; j < 16; ++j) a[j] = 0.f;
+                        for (int s0 = 0; s0 < S; s0 += 2) {
+                            float v[2][16];
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) a4[j] += v4[j];
+                            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                                for (int j = 0; j < 16; ++j)
+                                    v[h][j] = (s0 + h < S && n0 + j < x.n_valid)
+                                                  ? __ldcg(base + ((size_t)(s0 + h) * BN + n0 + j) * BM)
+                                                  : 0.f;
+#pragma unroll
+                            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                                for (int j = 0; j < 16; ++j)
+                                    if (s0 + h < S) a[j] += v[h][j];
                         }
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            if (n0 + j < x.n_valid) store_out(p, pd, x, n0 + j, m, a4[j]);
+                        if (et == 0 && n0 < 32) probe(p.probe, blockIdx.x, 16 + n0 / 8);  // chunk loaded
+                        store_chunk(e, x, n0, m, a, meta_i, meta_f);
+                        if (et == 0 && n0 < 32) probe(p.probe, blockIdx.x, 17 + n0 / 8);  // chunk stored
                     }
+                    if (et == 0) probe(p.probe, blockIdx.x, 20);
                     if (et == 0) p.counters[x.tile] = 0;
                 }
                 named_sync(1, 128);
             }
+            if (et == 0) probe(p.probe, blockIdx.x, 15);  // last unit finished
         }
         signal_upto(p.nphase);
     }
@@ -586,6 +719,8 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
     }
     if (tid == 0) {  // the last CTA out re-arms the phase barriers for the next launch
+        probe(p.probe, blockIdx.x, 9);  // exit
+        if (p.probe) p.probe[(size_t)blockIdx.x * kProbeSlots + 22] = clock64();
         __threadfence();
         if (atomicAdd(p.sync + kMaxPhases, 1) == (int)gridDim.x - 1) {
             for (int i = 0; i < kMaxPhases; ++i) p.sync[i] = 0;
@@ -638,7 +773,8 @@ __global__ void sum_slots_bf16_kernel(const float *__restrict__ yw, int T, int d
 
 template <int BN, int STAGES>
 constexpr size_t smem_bytes() {
-    return 1024 + (size_t)STAGES * (kABytes + BN * 128) + (2 * STAGES + 4) * 8 + 32 + (4 * kMaxGroups + 1) * 4;
+    return 1024 + (size_t)STAGES * (kABytes + BN * 128) + (2 * STAGES + 4) * 8 + 32 + (4 * kMaxGroups + 1) * 4 +
+           (kMetaInts + kMetaInts / 2) * 4;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -715,6 +851,7 @@ static int run(const PhaseMaps *mp, Params p, int bn, void *ws, size_t ws_bytes,
     p.sync = p.counters + kCounterInts;
     p.partial = reinterpret_cast<float *>(static_cast<char *>(ws) + head);
     p.partial_cap = (long long)((ws_bytes - head) / 4);
+    p.probe = probe_buffer(1, kNumSMs);
     if (bn <= 64) return launch<64, 8>(mp, p, s);
     return launch<256, 4>(mp, p, s);
 }

@@ -47,6 +47,8 @@ struct RouteParams {
     int *tile_counter; // workspace: [tiles] K splits finished per token tile
     double *plogit;    // workspace: [splits][T][E]
     float *pcmax;      // workspace: [tiles][splits][E] column max |G| of each K slice
+    double *pxsum;     // workspace: [splits][T] sum |x_i| of each K slice
+    unsigned long long *probe;  // debug stamps [tiles*splits][kProbeSlots] or null
 };
 
 __device__ __forceinline__ bool better(double fa, int ia, double fb, int ib) {
@@ -128,29 +130,47 @@ __device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, 
     const double gam = (double)d * u / (1.0 - (double)d * u);
     const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
     const double bpad = 1e-300;  // products are exact in fp64: no underflow below ~1e-90
-    // sum_i |x_i G_ij| <= (sum_i |x_i|) * max_i |G_ij|
+    // sum_i |x_i G_ij| <= (sum_i |x_i|) * max_i |G_ij|; the split CTAs
+    // wrote sum |x_i| of their slices.  All split partials are loaded in one
+    // batch (16 in flight per thread), then summed in split order.
     if (warp < ntok) {
         double xs = 0.0;
-#pragma unroll 8
-        for (int i = lane; i < d; i += 32) xs += fabs((double)__ldg(p.x + (size_t)(tok0 + warp) * d + i));
+        for (int z = lane; z < p.splits; z += 32) xs += __ldcg(p.pxsum + (size_t)z * p.T + tok0 + warp);
         xs = warp_sumd(xs);
-        if (lane == 0) s_xsum[warp] = xs * (1.0 + 2.0 * gam);  // rounding of the fp64 |x| sum
+        if (lane == 0) s_xsum[warp] = xs * (1.0 + 2.0 * gam);  // rounding of the fp64 |x| sums
     }
-    __syncthreads();
     for (int q = tid; q < ntok * E; q += kSelectThreads) {
         const int t = q / E, j = q - t * E;
         double sum = 0.0;
         float cm = 0.f;
-#pragma unroll 4
-        for (int z = 0; z < p.splits; ++z) {  // fixed order: deterministic
-            sum += __ldcg(p.plogit + ((size_t)z * p.T + tok0 + t) * E + j);
-            cm = fmaxf(cm, __ldcg(p.pcmax + ((size_t)tile * p.splits + z) * E + j));
+        for (int z0 = 0; z0 < p.splits; z0 += 16) {
+            double pl[16];
+            float pc[16];
+#pragma unroll
+            for (int z = 0; z < 16; ++z) {
+                pl[z] = (z0 + z < p.splits) ? __ldcg(p.plogit + ((size_t)(z0 + z) * p.T + tok0 + t) * E + j) : 0.0;
+                pc[z] = (z0 + z < p.splits) ? __ldcg(p.pcmax + ((size_t)tile * p.splits + z0 + z) * E + j) : 0.f;
+            }
+#pragma unroll
+            for (int z = 0; z < 16; ++z) {  // fixed order: deterministic
+                if (z0 + z < p.splits) {
+                    sum += pl[z];
+                    cm = fmaxf(cm, pc[z]);
+                }
+            }
         }
         double *lgt = reinterpret_cast<double *>(smem_raw) + (size_t)t * 2 * E;
         lgt[j] = sum;
-        lgt[E + j] = bscale * s_xsum[t] * (double)cm + bpad;
+        lgt[E + j] = (double)cm;
     }
     __syncthreads();
+    for (int q = tid; q < ntok * E; q += kSelectThreads) {
+        const int t = q / E, j = q - t * E;
+        double *lgt = reinterpret_cast<double *>(smem_raw) + (size_t)t * 2 * E;
+        lgt[E + j] = bscale * s_xsum[t] * lgt[E + j] + bpad;
+    }
+    __syncthreads();
+    if (tid == 0) probe(p.probe, blockIdx.y * gridDim.x + blockIdx.x, 7);  // partials reduced
     const int tok = tok0 + warp;
     if (warp < ntok) {  // tok < p.T follows
         double *lg = logit;
@@ -214,6 +234,7 @@ __device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, 
                 }
                 if (lane == 0) atomicAdd(p.out.status + 1, 1);
             }
+            if (lane == 0 && warp == 0) probe(p.probe, blockIdx.y * gridDim.x + blockIdx.x, 8);  // ranked
             // softmax over all E (linalg.py:54-59), max-subtracted
             double m = -INFINITY;
             for (int j = lane; j < E; j += 32) m = fmax(m, lg[j]);
@@ -319,9 +340,17 @@ __device__ void permute_all(const RouteParams &p, unsigned char *smem_raw) {
 // one step of the reference's serial sum.
 template <typename GT, int TOK, bool VECLOAD>
 __global__ void __launch_bounds__(kLogitThreads)
-route_kernel(RouteParams p) {
+route_kernel(const RouteParams p_in) {
     constexpr int V = Vec<GT>::N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // parameters copied to shared memory once: the select / permute tails
+    // re-read them often, and LDS beats indexed constant-bank reads
+    __shared__ RouteParams p_sh;
+    static_assert(sizeof(RouteParams) % 4 == 0 && sizeof(RouteParams) / 4 <= kLogitThreads, "params copy");
+    if (threadIdx.x < sizeof(RouteParams) / 4)
+        reinterpret_cast<int *>(&p_sh)[threadIdx.x] = reinterpret_cast<const int *>(&p_in)[threadIdx.x];
+    __syncthreads();
+    const RouteParams &p = p_sh;
     const int d = p.d, E = p.E;
     const GT *G = static_cast<const GT *>(p.G);
     const int tile = blockIdx.x;
@@ -339,13 +368,25 @@ route_kernel(RouteParams p) {
     double *red = reinterpret_cast<double *>(smem_raw);                   // reuse: [RG][TOK][E]
     float *redm = reinterpret_cast<float *>(red + (size_t)RG * TOK * E);  // [RG][E]
 
+    const int cta = split * gridDim.x + tile;
+    if (tid == 0) probe(p.probe, cta, 0);
     pdl_wait();  // x is produced by the previous kernel in the stream
     pdl_trigger();
+    if (tid == 0) probe(p.probe, cta, 1);
     for (int i = tid; i < TOK * kn; i += kLogitThreads) {
         const int t = i / kn;
         xd[i] = (t < ntok) ? (double)__ldg(p.x + (size_t)(t0 + t) * d + k0 + (i - t * kn)) : 0.0;
     }
     __syncthreads();
+    {   // sum |x_i| over this K slice, one warp per token (bounds the logit error)
+        const int warp = tid >> 5, lane = tid & 31;
+        if (warp < ntok) {
+            double xs = 0.0;
+            for (int i = lane; i < kn; i += 32) xs += fabs(xd[warp * kn + i]);
+            xs = warp_sumd(xs);
+            if (lane == 0) p.pxsum[(size_t)split * p.T + t0 + warp] = xs;
+        }
+    }
 
     double acc[TOK][V];
     float cmax[V];
@@ -418,17 +459,20 @@ route_kernel(RouteParams p) {
     __shared__ int s_last;
     __syncthreads();
     if (tid == 0) {
+        probe(p.probe, cta, 2);  // partial logits written
         __threadfence();
         s_last = (atomicAdd(p.tile_counter + tile, 1) == p.splits - 1);
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    if (tid == 0) probe(p.probe, cta, 3);  // select start
     select_tile<GT>(p, tile, t0, ntok, smem_raw);
 
     // ---- phase 3: the last token tile permutes ----------------------------
     __syncthreads();
     if (tid == 0) {
+        probe(p.probe, cta, 4);  // select done
         p.tile_counter[tile] = 0;
         __threadfence();
         s_last = (atomicAdd(p.counter, 1) == (int)gridDim.x - 1);
@@ -436,8 +480,12 @@ route_kernel(RouteParams p) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    if (tid == 0) probe(p.probe, cta, 5);  // permute start
     permute_all(p, smem_raw);
-    if (tid == 0) *p.counter = 0;
+    if (tid == 0) {
+        *p.counter = 0;
+        probe(p.probe, cta, 6);  // permute done
+    }
 }
 
 static int pick_tok(int T) {
@@ -509,9 +557,9 @@ extern "C" size_t pgmoe_route_workspace_bytes(int32_t T, int32_t E) {
     for (int t = 1; t <= std::max(T, 1); ++t) {
         const int tok = pick_tok(t), sp = pick_splits(t, 1 << 20, tok);
         const size_t tiles = (t + tok - 1) / tok;
-        worst = std::max(worst, (size_t)sp * t * 8 + tiles * sp * 4);
+        worst = std::max(worst, ((size_t)sp * t * 8 + tiles * sp * 4) * std::max(E, 1) + 256 + (size_t)sp * t * 8);
     }
-    return ws_head() + worst * std::max(E, 1) + 256;
+    return ws_head() + worst + 256;
 }
 
 extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const void *gate_w,
@@ -546,6 +594,9 @@ extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const vo
     const size_t n = (size_t)p.splits * T * E;
     p.plogit = reinterpret_cast<double *>(ws + ws_head());
     p.pcmax = reinterpret_cast<float *>(ws + ws_head() + n * 8);
+    const size_t ncm = (size_t)((T + p.tok - 1) / p.tok) * p.splits * E;
+    p.pxsum = reinterpret_cast<double *>(ws + ws_head() + ((n * 8 + ncm * 4 + 255) & ~(size_t)255));
+    p.probe = probe_buffer(0, ((T + p.tok - 1) / p.tok) * p.splits);
     if (wdtype == PGMOE_BF16) return route_dispatch<uint16_t>(p, s);
     if (wdtype == PGMOE_F32) return route_dispatch<float>(p, s);
     set_error("unknown weight dtype %d", wdtype);

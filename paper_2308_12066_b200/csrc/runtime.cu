@@ -28,6 +28,18 @@ namespace pgmoe {
 static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// Debug probes: each launch of kind k takes the next `ctas` rows of the
+// installed buffer (wrapping at its capacity), so one decoder iteration
+// leaves every launch's stamps side by side.
+static unsigned long long *g_probe[2] = {nullptr, nullptr};
+static long long g_probe_rows[2] = {0, 0}, g_probe_next[2] = {0, 0};
+unsigned long long *probe_buffer(int kind, int ctas) {
+    if (kind < 0 || kind >= 2 || !g_probe[kind]) return nullptr;
+    if (g_probe_next[kind] + ctas > g_probe_rows[kind]) g_probe_next[kind] = 0;
+    unsigned long long *b = g_probe[kind] + (size_t)g_probe_next[kind] * kProbeSlots;
+    g_probe_next[kind] += ctas;
+    return b;
+}
 
 void set_error(const char *fmt, ...) {
     char buf[1024];
@@ -450,6 +462,13 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
 extern "C" const char *pgmoe_last_error(void) { return g_last_error.c_str(); }
 extern "C" const char *pgmoe_version(void) { return "pgmoe-b200 0.1.0 (sm_100a)"; }
 extern "C" int64_t pgmoe_launch_count(void) { return g_launches.load(); }
+extern "C" int pgmoe_debug_set_probe(int32_t kind, void *device_buffer, int64_t rows) {
+    PG_REQUIRE(kind >= 0 && kind < 2, PGMOE_E_CONFIG, "probe kind %d", kind);
+    g_probe[kind] = static_cast<unsigned long long *>(device_buffer);
+    g_probe_rows[kind] = device_buffer ? rows : 0;
+    g_probe_next[kind] = 0;
+    return PGMOE_OK;
+}
 
 extern "C" int pgmoe_expert_forward(const float *x, int32_t T, int32_t d, int32_t f, int32_t k,
                                     const void *experts, size_t expert_stride, int32_t wdtype,
