@@ -280,51 +280,67 @@ __device__ __forceinline__ void stage_meta(const EpiRegs &e, const Unit &x, int 
     }
 }
 
-// Columns [c0, c0 + 16) of accumulator row m (only those < x.n_valid).
-__device__ __forceinline__ void store_chunk(const EpiRegs &e, const Unit &x, int c0, int m, const float (&v)[16],
-                                            const int *mi, const float *mf) {
+// Columns [c0, c0 + 16) of the accumulator rows this warp owns (m0w + lane),
+// only those < x.n_valid.  The warp transposes its 32 x 16 slice through a
+// 2 KB shared staging tile so that every global store is a 16-byte vector of
+// consecutive output rows (one thread per (column, row group)): a scalar
+// st.global per column per thread costs ~40 cycles of LSU issue per warp.
+__device__ __forceinline__ void store_chunk(const EpiRegs &e, const Unit &x, int c0, int m0w, int lane,
+                                            const float (&v)[16], const int *mi, const float *mf, float *stg) {
     const int nv = min(16, x.n_valid - c0);
-    if (e.mode == kUp) {
-        uint16_t *o = e.out_bf16 + (size_t)(x.row0 + x.n0 + c0) * e.M + m;
+    if (e.mode == kDown) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (j < nv) __stcg(o + (size_t)j * e.M, bf16_bits(fmaxf(v[j], 0.f)));  // relu, linalg.py:41-42
-    } else if (e.mode == kDown) {
-        int dst[16];
-        float w[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int r = x.row0 + x.n0 + c0 + j;
-            dst[j] = j < nv ? (e.staged ? mi[c0 + j] : __ldg(e.perm + r)) : 0;
-            w[j] = j < nv ? (e.staged ? mf[c0 + j] : __ldg(e.w_perm + r)) : 0.f;
+        for (int j = 0; j < 16; ++j) {  // combine weight (linalg.py:45-51), one per column
+            const float w = j < nv ? (e.staged ? mf[c0 + j] : __ldg(e.w_perm + x.row0 + x.n0 + c0 + j)) : 0.f;
+            stg[j * 32 + lane] = w * v[j];
         }
+    } else if (e.mode == kUp) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if (j < nv) {
-                const float y = w[j] * v[j];  // combine weight (linalg.py:45-51)
-                __stcg(e.out_f32 + (size_t)dst[j] * e.M + m, y);
-                if (e.out_bf16) __stcg(e.out_bf16 + (size_t)dst[j] * e.M + m, bf16_bits(y));  // top-1: mix == w*y
-            }
-        }
+        for (int j = 0; j < 16; ++j) stg[j * 32 + lane] = fmaxf(v[j], 0.f);  // relu, linalg.py:41-42
     } else {
-        float *o = e.out_f32 + (size_t)(x.n0 + c0) * e.M + m;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (j < nv) __stcg(o + (size_t)j * e.M, v[j]);
-        if (e.next_xb) {
-            for (int s = 0; s < e.k; ++s) {
-                int row[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int idx = (c0 + j) * e.k + s;
-                    row[j] = j < nv ? (e.staged ? mi[idx] : __ldg(e.next_inv + (size_t)x.n0 * e.k + idx)) : 0;
-                }
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (j < nv) __stcg(e.next_xb + (size_t)row[j] * e.M + m, bf16_bits(v[j]));
-            }
+        for (int j = 0; j < 16; ++j) stg[j * 32 + lane] = v[j];
+    }
+    __syncwarp();
+    // fp32 rows: down -> yw[perm[r]], dense -> y[token]; 8 float4 per column
+    if (e.mode != kUp) {
+        for (int i = lane; i < nv * 8; i += 32) {
+            const int col = i >> 3, g = i & 7;
+            const int row = e.mode == kDown
+                                ? (e.staged ? mi[c0 + col] : __ldg(e.perm + x.row0 + x.n0 + c0 + col))
+                                : x.n0 + c0 + col;
+            const float4 val = *reinterpret_cast<const float4 *>(stg + col * 32 + g * 4);
+            __stcg(reinterpret_cast<float4 *>(e.out_f32 + (size_t)row * e.M + m0w + g * 4), val);
         }
     }
+    // bf16 rows: up -> hb[r], down (top-1) -> mixb[perm[r]], dense -> the next
+    // block's packed rows next_xb[next_inv[t*k+s]]; 4 x 16 bytes per column
+    uint16_t *ob = e.mode == kDense ? e.next_xb : e.out_bf16;
+    if (ob != nullptr) {
+        const int slots = e.mode == kDense ? e.k : 1;
+        for (int i = lane; i < nv * 4 * slots; i += 32) {
+            const int s = i / (nv * 4), rem = i - s * (nv * 4);
+            const int col = rem >> 2, g = rem & 3;
+            int row;
+            if (e.mode == kUp) {
+                row = x.row0 + x.n0 + c0 + col;
+            } else if (e.mode == kDown) {
+                row = e.staged ? mi[c0 + col] : __ldg(e.perm + x.row0 + x.n0 + c0 + col);
+            } else {
+                const int idx = (c0 + col) * e.k + s;
+                row = e.staged ? mi[idx] : __ldg(e.next_inv + (size_t)x.n0 * e.k + idx);
+            }
+            const float4 a = *reinterpret_cast<const float4 *>(stg + col * 32 + g * 8);
+            const float4 b = *reinterpret_cast<const float4 *>(stg + col * 32 + g * 8 + 4);
+            uint4 o;
+            o.x = bf16_bits(a.x) | ((uint32_t)bf16_bits(a.y) << 16);
+            o.y = bf16_bits(a.z) | ((uint32_t)bf16_bits(a.w) << 16);
+            o.z = bf16_bits(b.x) | ((uint32_t)bf16_bits(b.y) << 16);
+            o.w = bf16_bits(b.z) | ((uint32_t)bf16_bits(b.w) << 16);
+            __stcg(reinterpret_cast<uint4 *>(ob + (size_t)row * e.M + m0w + g * 8), o);
+        }
+    }
+    __syncwarp();  // the staging tile is rewritten by the next chunk
 }
 
 struct DeferredB {
@@ -369,6 +385,9 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
     int *g_ng = g_row0 + kMaxGroups;
     int *meta_i = g_ng + kMaxGroups;                            // [kMetaInts]
     float *meta_f = reinterpret_cast<float *>(meta_i + kMetaInts);  // [kMetaInts / 2]
+    unsigned char *stage_raw = reinterpret_cast<unsigned char *>(meta_f + kMetaInts / 2);
+    float *stage_out = reinterpret_cast<float *>(stage_raw + ((16u - (smem_u32(stage_raw) & 15u)) & 15u));
+    // ^ [4 warps][16 cols][32 rows], 16-byte aligned for the vector reads
     const CUtensorMap *amaps[3] = {&a0, &a1, &a2};
     const CUtensorMap *bmaps[3] = {&b0, &b1, &b2};
 
@@ -652,8 +671,11 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                     float v[16];
                     tmem_ld16(taddr + c0, v);
                     if (et == 0 && c0 < 64) probe(p.probe, blockIdx.x, 23 + c0 / 8);  // chunk loaded from TMEM
-                    store_chunk(e, x, c0, m, v, meta_i, meta_f);
+                    const long long ck0 = clock64();
+                    store_chunk(e, x, c0, x.m_tile * BM + q * 32, lane, v, meta_i, meta_f, stage_out + q * 512);
+                    const long long ck1 = clock64();
                     if (et == 0 && c0 < 64) probe(p.probe, blockIdx.x, 24 + c0 / 8);  // chunk stored
+                    if (et == 0 && c0 == 0 && p.probe) p.probe[(size_t)blockIdx.x * kProbeSlots + 31] = ck1 - ck0;
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[acc]);
@@ -699,7 +721,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                                     if (s0 + h < S) a[j] += v[h][j];
                         }
                         if (et == 0 && n0 < 32) probe(p.probe, blockIdx.x, 16 + n0 / 8);  // chunk loaded
-                        store_chunk(e, x, n0, m, a, meta_i, meta_f);
+                        store_chunk(e, x, n0, x.m_tile * BM + q * 32, lane, a, meta_i, meta_f, stage_out + q * 512);
                         if (et == 0 && n0 < 32) probe(p.probe, blockIdx.x, 17 + n0 / 8);  // chunk stored
                     }
                     if (et == 0) probe(p.probe, blockIdx.x, 20);
@@ -774,7 +796,7 @@ __global__ void sum_slots_bf16_kernel(const float *__restrict__ yw, int T, int d
 template <int BN, int STAGES>
 constexpr size_t smem_bytes() {
     return 1024 + (size_t)STAGES * (kABytes + BN * 128) + (2 * STAGES + 4) * 8 + 32 + (4 * kMaxGroups + 1) * 4 +
-           (kMetaInts + kMetaInts / 2) * 4;
+           (kMetaInts + kMetaInts / 2) * 4 + 16 + 4 * 512 * 4;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

@@ -116,7 +116,7 @@ def main():
                 v = rows[:, s]
                 if (v > 0).any():
                     c = int(np.argmax(v))
-                    res["launches"].append({"cta": c, "phase_slot": s,
+                    res["launches"].append({"cta": c, "phase_slot": s, "store_chunk0_cycles": int(rows[c, 31]),
                                             "row": {BLOCK_SLOTS[k]: round(float((rows[c, k] - t0) / 1e3), 2)
                                                     for k in BLOCK_SLOTS if rows[c, k] > 0}})
     # effective SM clock over each block kernel CTA: d(clock64) / d(globaltimer)
