@@ -22,9 +22,10 @@
 // boxes until the barrier opens (the same trick hides the programmatic-
 // dependent-launch wait of phase 0).
 //
-// Warp roles (192 threads, one CTA per SM, grid = #SMs so all CTAs are
+// Warp roles (224 threads, one CTA per SM, grid = #SMs so all CTAs are
 // co-resident for the barrier):
-//   warp 0      : TMA producer (one elected lane)
+//   warp 0      : weight TMA producer + unit scheduler (one lane)
+//   warp 6      : gated activation TMA producer (one lane)
 //   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2-5   : epilogue — tcgen05.ld the fp32 accumulator, ReLU / combine
 //                 weight / scatter, or the split-K fix-up; signals phases
@@ -43,7 +44,7 @@ namespace pgmoe {
 
 namespace tc {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;
 constexpr int BM = 128;               // UMMA M (weight rows per tile)
 constexpr int BK = 64;                // bf16 elements per 128-byte swizzle row
 constexpr int kABytes = BM * BK * 2;  // 16 KB
@@ -51,7 +52,8 @@ constexpr int kBRowsPerBox = 16;      // activation rows per TMA box (2 KB)
 constexpr int kMaxGroups = 1024;
 constexpr int kMaxPhases = 3;
 constexpr int kCounterInts = 8192;    // split-K tile tickets at the head of the workspace
-constexpr int kSyncInts = 16;         // phase barriers + exit ticket, after the tickets
+constexpr int kSyncInts = 16 + kMaxGroups;  // phase barriers, exit ticket, unit counter; per-group up tiles done
+constexpr int kUnitQ = 16;            // producer -> MMA / epilogue unit queue (shared memory ring)
 constexpr int kMetaInts = 512;        // per-column epilogue metadata staged in shared memory
 // split-K cost model (bytes per microsecond; microseconds)
 constexpr float kSmBytesPerUs = 150e3f;   // one SM's TMA stream when few CTAs load
@@ -78,7 +80,7 @@ struct Params {
     uint16_t *next_xb;
     const int *next_inv;
     int *counters;   // [kCounterInts] split-K tickets
-    int *sync;       // [kSyncInts] phase_done[kMaxPhases], exit ticket
+    int *sync;       // [kSyncInts] phase_done[kMaxPhases], exit ticket, unit counter, grp_done[kMaxGroups]
     float *partial;
     long long partial_cap;  // floats
     unsigned long long *probe;  // debug stamps [grid][kProbeSlots] or null
@@ -176,6 +178,8 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
 
 struct PhaseSched {
     int mode, M, K, m_tiles, kb_total, kbs, S;
+    int ctr0;             // first split-K ticket of this phase (phases may overlap)
+    long long part0;      // first partial-tile float of this phase
     long long tiles, units, unit0;
 };
 
@@ -343,9 +347,6 @@ __device__ __forceinline__ void store_chunk(const EpiRegs &e, const Unit &x, int
     __syncwarp();  // the staging tile is rewritten by the next chunk
 }
 
-struct DeferredB {
-    int stage, kb, row, npad;
-};
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -377,7 +378,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *uq_full = tempty + 2;       // [kUnitQ]
+    uint64_t *uq_empty = uq_full + kUnitQ;  // [kUnitQ]
+    long long *unit_q = reinterpret_cast<long long *>(uq_empty + kUnitQ);  // [kUnitQ]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(unit_q + kUnitQ);
     int *s_flag = reinterpret_cast<int *>(tmem_slot + 1);
     int *ntp = s_flag + 4;
     int *g_rec = ntp + kMaxGroups + 1;
@@ -456,6 +460,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 128);
         }
+        for (int i = 0; i < kUnitQ; ++i) {
+            mbar_init(&uq_full[i], 1);   // producer
+            mbar_init(&uq_empty[i], 3);  // MMA lane 0, activation producer, one epilogue thread
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid == 96) {
@@ -472,7 +480,8 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
     const int max_npad_expert = s_flag[1], ntiles_expert = s_flag[2];
 
     if (tid == 0) {
-    long long total_units = 0;
+    long long total_units = 0, part_used = 0;
+    int ctr_used = 0;
     for (int i = 0; i < p.nphase; ++i) {
         PhaseSched &sc = ps[i];
         sc.mode = p.ph[i].mode;
@@ -507,9 +516,18 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             const float t = (float)waves * kbs * kb_bytes / bw + (cand > 1 ? kFixUs : 0.f);
             if (t < best * 0.98f) { best = t; S = cand; }
         }
-        while (S > 1 && ((long long)sc.tiles * S * BN * BM > p.partial_cap || sc.tiles > kCounterInts)) --S;
+        // phases can run concurrently (per-expert gating), so each phase's
+        // tickets and partial tiles live in their own ranges
+        while (S > 1 && (part_used + (long long)sc.tiles * S * BN * BM > p.partial_cap ||
+                         ctr_used + sc.tiles > kCounterInts)) --S;
         sc.kbs = (sc.kb_total + S - 1) / S;
         sc.S = (sc.kb_total + sc.kbs - 1) / sc.kbs;
+        sc.ctr0 = ctr_used;
+        sc.part0 = part_used;
+        if (sc.S > 1) {
+            ctr_used += (int)sc.tiles;
+            part_used += sc.tiles * sc.S * BN * BM;
+        }
         sc.units = sc.tiles * sc.S;
         sc.unit0 = total_units;
         total_units += sc.units;
@@ -518,95 +536,133 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
     }
     __syncthreads();
     const long long total_units = s_total_units;
-    int *phase_done = p.sync;
+    int *phase_done = p.sync;                    // [kMaxPhases]
+    int *unit_ctr = p.sync + kMaxPhases + 1;     // dynamic unit counter
+    int *grp_done = p.sync + 16;                 // [kMaxGroups] up tiles finished per expert group
+    // Down-projection units of group g wait only for g's own up tiles (not for
+    // the whole up phase), so the two expert phases overlap at their boundary.
+    const bool group_gated = p.nphase >= 2 && ps[0].mode == kUp && ps[1].mode == kDown;
 
     if (warp == 0) {
-        // ================= TMA producer ====================================
-        // Weight tiles never depend on earlier work: they are issued as soon
-        // as a stage is free.  A phase's activation boxes wait for its gate —
-        // griddepcontrol.wait (PDL) for phase 0, the grid barrier on the
-        // previous phase otherwise — and are deferred (at most STAGES) until
-        // then, so the gate's latency overlaps weight streaming.
+        // ================= weight producer (one thread) ====================
+        // Units are handed out dynamically (the first one static, then an
+        // atomic counter once the previous launch is complete) and published
+        // to the other roles through a shared ring.  This thread streams the
+        // weight tiles: they never depend on earlier work, so it runs up to
+        // STAGES ahead of the MMA and arms each stage for the weight AND the
+        // activation bytes.  The activation boxes come from the gated
+        // producer (warp 6), so a gate wait never stalls the weight stream.
         if (lane == 0) {
             uint64_t policy;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-            int stage = 0;
-            uint32_t phase = 0;
-            int open_ph = -1;  // gates of phases <= open_ph are open
-            DeferredB dq[STAGES];
-            int nd = 0;
-            auto open_gate = [&](int ph, bool block) -> bool {
-                if (ph == 0) {
-                    if (!block) return false;
-                    pdl_wait();
-                    pdl_trigger();
-                    probe(p.probe, blockIdx.x, 2);  // phase-0 gate (PDL) open
-                    return true;
-                }
-                if (block) {
-                    while (ld_acquire(phase_done + ph - 1) < (int)gridDim.x) __nanosleep(64);
-                } else if (ld_acquire(phase_done + ph - 1) < (int)gridDim.x) {
-                    return false;
-                }
-                probe(p.probe, blockIdx.x, 2 + ph);  // phase-ph gate open
-                // phase ph-1's outputs were written through the generic proxy
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                return true;
-            };
-            auto flush = [&](int ph) {
-                for (int q = 0; q < nd; ++q)
-                    for (int j = 0; j < dq[q].npad; j += kBRowsPerBox)
-                        tma_load_2d(sB + dq[q].stage * kBBytes + j * 128, bmaps[ph], &full[dq[q].stage],
-                                    dq[q].kb * BK, dq[q].row + j);
-                nd = 0;
-            };
-            for (long long u = blockIdx.x; u < total_units; u += gridDim.x) {
+            int stage = 0, qi = 0;
+            uint32_t phase = 0, qphase = 0;
+            bool pdl_done = false;
+            long long cyc_empty = 0, cyc_atom = 0, n_units = 0;
+            long long u = blockIdx.x;
+            while (u < total_units) {
                 const Unit x = decode_unit<BN>(ps, p.nphase, gr, u);
-                while (open_ph < x.ph - 1) {  // an earlier gate must open first
-                    open_gate(open_ph + 1, true);
-                    flush(open_ph + 1);
-                    ++open_ph;
-                }
-                const int brow = x.row0 + x.n0;
+                mbar_wait(&uq_empty[qi], qphase ^ 1);
+                unit_q[qi] = u;
+                mbar_arrive(&uq_full[qi]);
+                if (++qi == kUnitQ) { qi = 0; qphase ^= 1; }
+                // fetch the next unit early: the atomic's latency overlaps this unit
+                int nxt = -1;
+                if (pdl_done) nxt = atomicAdd(unit_ctr, 1);
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                    const long long c1 = clock64();
                     mbar_wait(&empty[stage], phase ^ 1);
+                    cyc_empty += clock64() - c1;
                     mbar_expect_tx(&full[stage], kABytes + x.n_pad * 128);
                     tma_load_3d(sA + stage * kABytes, amaps[x.ph], &full[stage], kb * BK, x.m_tile * BM, x.rec,
                                 policy);
-                    if (open_ph < x.ph && open_gate(x.ph, false)) {
-                        flush(x.ph);
-                        open_ph = x.ph;
-                    }
-                    if (open_ph >= x.ph) {
-                        for (int j = 0; j < x.n_pad; j += kBRowsPerBox)
-                            tma_load_2d(sB + stage * kBBytes + j * 128, bmaps[x.ph], &full[stage], kb * BK,
-                                        brow + j);
-                    } else {
-                        dq[nd++] = {stage, kb, brow, x.n_pad};
-                        if (nd == STAGES) {  // every stage waits on the gate now
-                            open_gate(x.ph, true);
-                            flush(x.ph);
-                            open_ph = x.ph;
-                        }
-                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
+                if (!pdl_done) {  // the unit counter is re-armed by the previous launch
+                    pdl_wait();
+                    pdl_trigger();
+                    pdl_done = true;
+                    probe(p.probe, blockIdx.x, 2);  // PDL gate open
+                    const long long c3 = clock64();
+                    nxt = atomicAdd(unit_ctr, 1);
+                    cyc_atom += clock64() - c3;
+                }
+                u = (long long)gridDim.x + nxt;
+                ++n_units;
             }
-            if (nd > 0) {
-                open_gate(open_ph + 1, true);
-                flush(open_ph + 1);
-            }
-            if (open_ph < 0) {  // no phase-0 work here: still honour PDL before exiting
+            if (!pdl_done) {  // no work here: still honour PDL before exiting
                 pdl_wait();
                 pdl_trigger();
             }
-            probe(p.probe, blockIdx.x, 11);  // last load issued
+            mbar_wait(&uq_empty[qi], qphase ^ 1);
+            unit_q[qi] = -1;
+            mbar_arrive(&uq_full[qi]);
+            probe(p.probe, blockIdx.x, 11);  // last weight load issued
+            if (p.probe) {
+                unsigned long long *pr = p.probe + (size_t)blockIdx.x * kProbeSlots;
+                pr[17] = cyc_empty; pr[18] = cyc_atom; pr[19] = n_units;
+            }
+        }
+    } else if (warp == 6) {
+        // ================= activation producer (one thread) ================
+        // Follows the unit ring; before a unit's activation boxes it waits for
+        // the unit's gate: griddepcontrol.wait (PDL) for phase 0, the unit's
+        // expert's up tiles for a down unit (so the expert phases overlap),
+        // the whole previous phase for the dense phase.  Its boxes complete
+        // the stage the weight producer armed for both (the transaction count
+        // may briefly run ahead of the arming).
+        if (lane == 0) {
+            int stage = 0, qi = 0;
+            uint32_t phase = 0, qphase = 0;
+            long long cyc_gate = 0;
+            pdl_wait();  // the activations of phase 0 come from the previous kernel
+            int open_group = -1, open_phase = 0;
+            for (;;) {
+                mbar_wait(&uq_full[qi], qphase);
+                const long long u = unit_q[qi];
+                mbar_arrive(&uq_empty[qi]);
+                if (++qi == kUnitQ) { qi = 0; qphase ^= 1; }
+                if (u < 0) break;
+                const Unit x = decode_unit<BN>(ps, p.nphase, gr, u);
+                const long long c0 = clock64();
+                if (x.ph > 0) {
+                    if (group_gated && x.ph == 1) {
+                        if (x.g != open_group) {
+                            const int need = (gr.ntp[x.g + 1] - gr.ntp[x.g]) * ps[0].m_tiles;
+                            while (ld_acquire(grp_done + x.g) < need) __nanosleep(32);
+                            open_group = x.g;
+                            asm volatile("fence.proxy.async.global;" ::: "memory");
+                        }
+                    } else if (x.ph > open_phase) {
+                        while (ld_acquire(phase_done + x.ph - 1) < (int)gridDim.x) __nanosleep(32);
+                        open_phase = x.ph;
+                        probe(p.probe, blockIdx.x, 2 + x.ph);  // phase gate open
+                        // the previous phase's rows were written through the generic proxy
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
+                }
+                cyc_gate += clock64() - c0;
+                const int brow = x.row0 + x.n0;
+                for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    for (int j = 0; j < x.n_pad; j += kBRowsPerBox)
+                        tma_load_2d(sB + stage * kBBytes + j * 128, bmaps[x.ph], &full[stage], kb * BK, brow + j);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+            if (p.probe) p.probe[(size_t)blockIdx.x * kProbeSlots + 16] = cyc_gate;
         }
     } else if (warp == 1) {
         // ================= MMA issuer (single thread) ======================
-        int stage = 0, cnt = 0;
-        uint32_t phase = 0;
-        for (long long u = blockIdx.x; u < total_units; u += gridDim.x, ++cnt) {
+        int stage = 0, cnt = 0, qi = 0;
+        uint32_t phase = 0, qphase = 0;
+        for (;; ++cnt) {
+            mbar_wait(&uq_full[qi], qphase);
+            const long long u = unit_q[qi];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&uq_empty[qi]);
+            if (++qi == kUnitQ) { qi = 0; qphase ^= 1; }
+            if (u < 0) break;
             const Unit x = decode_unit<BN>(ps, p.nphase, gr, u);
             const int acc = cnt & 1;
             mbar_wait(&tempty[acc], ((cnt >> 1) & 1) ^ 1);
@@ -635,10 +691,11 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         // ================= epilogue: TMEM -> registers -> global ===========
         const int q = warp & 3;        // TMEM lane quarter this warp may access
         const int et = q * 32 + lane;  // accumulator row 0..127
-        int cnt = 0, signalled = 0;    // phases [0, signalled) reported done
-        // The previous launch's last CTA re-arms the phase counters on its way
-        // out; with programmatic dependent launch this grid may already be
-        // running, so no signal may precede griddepcontrol.wait.
+        int cnt = 0, signalled = 0, qi = 0;  // phases [0, signalled) reported done
+        uint32_t qphase = 0;
+        // The previous launch's last CTA re-arms the counters on its way out;
+        // with programmatic dependent launch this grid may already be running,
+        // so no signal may precede griddepcontrol.wait.
         pdl_wait();
         auto signal_upto = [&](int ph_end) {
             for (; signalled < ph_end; ++signalled) {
@@ -650,7 +707,20 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                 }
             }
         };
-        for (long long u = blockIdx.x; u < total_units; u += gridDim.x, ++cnt) {
+        // an up tile's hidden rows are complete: release its expert's down units
+        auto tile_done = [&](const Unit &x) {
+            if (!group_gated || x.ph != 0) return;
+            __threadfence();
+            named_sync(1, 128);
+            if (et == 0) atomicAdd(grp_done + x.g, 1);
+        };
+        for (;; ++cnt) {
+            mbar_wait(&uq_full[qi], qphase);
+            const long long u = unit_q[qi];
+            named_sync(1, 128);  // every epilogue thread has read the slot
+            if (et == 0) mbar_arrive(&uq_empty[qi]);
+            if (++qi == kUnitQ) { qi = 0; qphase ^= 1; }
+            if (u < 0) break;
             const Unit x = decode_unit<BN>(ps, p.nphase, gr, u);
             signal_upto(x.ph);
             const EpiRegs e = epi_regs(p, p.ph[x.ph], x);
@@ -664,23 +734,19 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             mbar_wait(&tfull[acc], (cnt >> 1) & 1);
             tc_fence_after();
             if (et == 0) probe(p.probe, blockIdx.x, cnt == 0 ? 5 : 12);  // first / last accumulator ready
-            const int m = x.m_tile * BM + et;
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
             if (S == 1) {
                 for (int c0 = 0; c0 < x.n_valid; c0 += 16) {
                     float v[16];
                     tmem_ld16(taddr + c0, v);
-                    if (et == 0 && c0 < 64) probe(p.probe, blockIdx.x, 23 + c0 / 8);  // chunk loaded from TMEM
-                    const long long ck0 = clock64();
                     store_chunk(e, x, c0, x.m_tile * BM + q * 32, lane, v, meta_i, meta_f, stage_out + q * 512);
-                    const long long ck1 = clock64();
-                    if (et == 0 && c0 < 64) probe(p.probe, blockIdx.x, 24 + c0 / 8);  // chunk stored
-                    if (et == 0 && c0 == 0 && p.probe) p.probe[(size_t)blockIdx.x * kProbeSlots + 31] = ck1 - ck0;
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[acc]);
+                tile_done(x);
             } else {
-                float *part = p.partial + ((size_t)x.tile * S + x.s) * (BN * BM);
+                const PhaseSched &sc = ps[x.ph];
+                float *part = p.partial + sc.part0 + ((size_t)x.tile * S + x.s) * (BN * BM);
                 for (int c0 = 0; c0 < x.n_valid; c0 += 16) {
                     float v[16];
                     tmem_ld16(taddr + c0, v);
@@ -693,12 +759,13 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                 if (et == 0) probe(p.probe, blockIdx.x, 13);  // partials stored (last unit)
                 __threadfence();
                 named_sync(1, 128);
-                if (et == 0) s_flag[0] = (atomicAdd(p.counters + x.tile, 1) == S - 1);
+                int *ticket = p.counters + sc.ctr0 + x.tile;
+                if (et == 0) s_flag[0] = (atomicAdd(ticket, 1) == S - 1);
                 named_sync(1, 128);
                 if (s_flag[0]) {
                     __threadfence();
                     if (et == 0) probe(p.probe, blockIdx.x, 14);  // fix-up start (last unit)
-                    const float *base = p.partial + (size_t)x.tile * S * (BN * BM) + et;
+                    const float *base = p.partial + sc.part0 + (size_t)x.tile * S * (BN * BM) + et;
                     // 32 partial loads in flight per thread: 16 columns x 2
                     // splits at a time, summed in split order (deterministic)
                     for (int n0 = 0; n0 < x.n_valid; n0 += 16) {
@@ -720,12 +787,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                                 for (int j = 0; j < 16; ++j)
                                     if (s0 + h < S) a[j] += v[h][j];
                         }
-                        if (et == 0 && n0 < 32) probe(p.probe, blockIdx.x, 16 + n0 / 8);  // chunk loaded
                         store_chunk(e, x, n0, x.m_tile * BM + q * 32, lane, a, meta_i, meta_f, stage_out + q * 512);
-                        if (et == 0 && n0 < 32) probe(p.probe, blockIdx.x, 17 + n0 / 8);  // chunk stored
                     }
-                    if (et == 0) probe(p.probe, blockIdx.x, 20);
-                    if (et == 0) p.counters[x.tile] = 0;
+                    if (et == 0) *ticket = 0;
+                    tile_done(x);
                 }
                 named_sync(1, 128);
             }
@@ -740,15 +805,22 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         constexpr uint32_t cols = (2 * BN < 32) ? 32 : 2 * BN;
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
     }
-    if (tid == 0) {  // the last CTA out re-arms the phase barriers for the next launch
+    // the last CTA out re-arms the counters for the next launch
+    if (tid == 0) {
         probe(p.probe, blockIdx.x, 9);  // exit
         if (p.probe) p.probe[(size_t)blockIdx.x * kProbeSlots + 22] = clock64();
         __threadfence();
-        if (atomicAdd(p.sync + kMaxPhases, 1) == (int)gridDim.x - 1) {
-            for (int i = 0; i < kMaxPhases; ++i) p.sync[i] = 0;
+        s_flag[3] = (atomicAdd(p.sync + kMaxPhases, 1) == (int)gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_flag[3]) {
+        for (int i = tid; i < gr.n; i += kThreads) grp_done[i] = 0;
+        if (tid == 0) {
+            for (int i = 0; i < kMaxPhases; ++i) phase_done[i] = 0;
             p.sync[kMaxPhases] = 0;
-            __threadfence();
+            *unit_ctr = 0;
         }
+        __threadfence();
     }
 }
 
@@ -795,7 +867,8 @@ __global__ void sum_slots_bf16_kernel(const float *__restrict__ yw, int T, int d
 
 template <int BN, int STAGES>
 constexpr size_t smem_bytes() {
-    return 1024 + (size_t)STAGES * (kABytes + BN * 128) + (2 * STAGES + 4) * 8 + 32 + (4 * kMaxGroups + 1) * 4 +
+    return 1024 + (size_t)STAGES * (kABytes + BN * 128) + (2 * STAGES + 4 + 3 * kUnitQ) * 8 + 32 +
+           (4 * kMaxGroups + 1) * 4 +
            (kMetaInts + kMetaInts / 2) * 4 + 16 + 4 * 512 * 4;
 }
 

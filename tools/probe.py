@@ -31,7 +31,7 @@ PRESETS = {
 ROUTE_SLOTS = {0: "entry", 1: "pdl", 2: "logits", 3: "sel0", 7: "selred", 8: "ranked", 4: "sel1", 5: "perm0",
                6: "perm1"}
 BLOCK_SLOTS = {0: "entry", 1: "prolog", 2: "gate0", 3: "gate1", 4: "gate2", 5: "acc0", 6: "ph0", 7: "ph1",
-               8: "ph2", 11: "lastld", 12: "accN", 13: "partN", 14: "fixN", 16: "c0ld", 17: "c0st", 18: "c1ld", 19: "c1st", 20: "fixend", 23: "t0ld", 24: "t0st", 25: "t1ld", 26: "t1st", 27: "t2ld", 28: "t2st",
+               8: "ph2", 11: "lastld", 12: "accN", 13: "partN", 14: "fixN", 23: "t0ld", 24: "t0st", 25: "t1ld", 26: "t1st", 27: "t2ld", 28: "t2st",
                29: "t3ld", 30: "t3st", 15: "endN",
                9: "exit"}
 ROWS = 1 << 15
@@ -126,6 +126,11 @@ def main():
         if ok.any():
             mhz.append(float(np.median((b[ok, 22] - b[ok, 21]) / (b[ok, 9] - b[ok, 0]) * 1e3)))
     res["sm_mhz_in_block_kernel"] = [round(v) for v in mhz[:4]]
+    # producer cycle counters of block 1's launch: gate waits / empty-stage waits / unit atomics / units
+    b = bl[1]
+    res["producer_us"] = {k: [round(float(np.percentile(b[:, s] / 1.86e3, q)), 1) for q in (0, 50, 100)]
+                          for k, s in (("gate", 16), ("empty", 17), ("atomic", 18))}
+    res["units_per_cta"] = [int(b[:, 19].min()), float(np.median(b[:, 19])), int(b[:, 19].max())]
     print(json.dumps(res))
 
 
