@@ -158,6 +158,7 @@ typedef struct {
     int64_t cache_hits, cache_misses;
     int64_t d2d_bytes;            /* cache <-> working-slot copies */
     int64_t fused_blocks;         /* blocks whose dense layer ran inside the expert-FFN launch */
+    int64_t fused_routes;         /* pre-gates computed inside the block launch (resident) */
 } pgmoe_stats;
 
 /* init_model (core.py:266) + placement (tiers.py:134-157).  max_tokens
@@ -219,6 +220,11 @@ PGMOE_API int pgmoe_cache_replay(int32_t policy, int32_t capacity_records, const
 
 /* Kernel family for K2/K3 (AUTO: tcgen05 for bf16, SIMT for fp32). */
 PGMOE_API int pgmoe_model_set_kernel(pgmoe_model *m, int32_t kernel);
+/* Resident top-1 decoding computes each block's pre-gate (gate_forward of
+ * the next block's decision, core.py:327-329) inside that block's tcgen05
+ * launch, overlapped with its expert GEMMs (default on).  0 restores the
+ * separate K1 launch; routing and outputs are identical either way. */
+PGMOE_API int pgmoe_model_set_fused_route(pgmoe_model *m, int32_t enabled);
 
 /* decoder_iteration (core.py:342-383) for T tokens, device buffers.
  * x_in / y_out: fp32 [T][d] device.  ids_trace / w_trace (optional, device):

@@ -53,7 +53,8 @@ class Stats(ctypes.Structure):
                 ("route_fallbacks", ctypes.c_int64), ("route_flips", ctypes.c_int64),
                 ("h2d_seconds", ctypes.c_double), ("last_step_seconds", ctypes.c_double),
                 ("cache_bytes", ctypes.c_int64), ("cache_hits", ctypes.c_int64), ("cache_misses", ctypes.c_int64),
-                ("d2d_bytes", ctypes.c_int64), ("fused_blocks", ctypes.c_int64)]
+                ("d2d_bytes", ctypes.c_int64), ("fused_blocks", ctypes.c_int64),
+                ("fused_routes", ctypes.c_int64)]
 
 
 EXPORTS = (
@@ -66,7 +67,7 @@ EXPORTS = (
     "pgmoe_launch_count", "pgmoe_model_create_ex", "pgmoe_model_expert_records", "pgmoe_gather_rows",
     "pgmoe_unpermute_combine", "pgmoe_ep_local_routing", "pgmoe_model_config", "pgmoe_weight_file_config",
     "pgmoe_model_load_pgmoe1", "pgmoe_model_save_pgmoe1", "pgmoe_model_set_strategy", "pgmoe_model_set_cache",
-    "pgmoe_cache_replay", "pgmoe_debug_set_probe",
+    "pgmoe_cache_replay", "pgmoe_debug_set_probe", "pgmoe_model_set_fused_route",
 )
 
 _lib = None
@@ -121,6 +122,7 @@ def load():
         "pgmoe_model_load_pgmoe1": (i32, [vp, ctypes.c_char_p]),
         "pgmoe_model_save_pgmoe1": (i32, [vp, ctypes.c_char_p]),
         "pgmoe_debug_set_probe": (i32, [i32, vp, i64]),
+        "pgmoe_model_set_fused_route": (i32, [vp, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -342,6 +342,10 @@ class DeviceModel:
     def set_kernel(self, kernel: str) -> None:
         _lib.check(self._L.pgmoe_model_set_kernel(self._h, _KERNEL[kernel]))
 
+    def set_fused_route(self, enabled: bool) -> None:
+        """Resident top-1: compute each pre-gate inside the block launch (default)."""
+        _lib.check(self._L.pgmoe_model_set_fused_route(self._h, 1 if enabled else 0))
+
     # -- weights (BlockParams `loaded` hook, core.py:185-211) --
     def _mat_shape(self, name):
         c = self.config

@@ -36,20 +36,22 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "route_common.cuh"
 
 namespace pgmoe {
 
 namespace tc {
 
-constexpr int kThreads = 224;
+constexpr int kThreads = 288;
 constexpr int BM = 128;               // UMMA M (weight rows per tile)
 constexpr int BK = 64;                // bf16 elements per 128-byte swizzle row
 constexpr int kABytes = BM * BK * 2;  // 16 KB
 constexpr int kBRowsPerBox = 16;      // activation rows per TMA box (2 KB)
-constexpr int kMaxGroups = 1024;
+constexpr int kMaxGroups = 512;        // active experts per launch (smem schedule arrays)
 constexpr int kMaxPhases = 3;
 constexpr int kCounterInts = 8192;    // split-K tile tickets at the head of the workspace
 constexpr int kSyncInts = 16 + kMaxGroups;  // phase barriers, exit ticket, unit counter; per-group up tiles done
@@ -84,6 +86,8 @@ struct Params {
     float *partial;
     long long partial_cap;  // floats
     unsigned long long *probe;  // debug stamps [grid][kProbeSlots] or null
+    FusedRoute route;           // the next block's routing, computed by warps 7-8 (resident)
+    int max_inflight;           // weight stages the producer keeps in flight (<= STAGES)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -361,6 +365,8 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
     // One copy in shared memory makes every such read an LDS.
     __shared__ Params p_sh;
     __shared__ PhaseSched ps[kMaxPhases];
+    __shared__ float r_xs[kRouterTok * kRouterMaxKn];  // routing role: x slice / permutation scratch
+    __shared__ int r_flag;
     __shared__ long long s_total_units;
     static_assert(sizeof(Params) % 4 == 0 && sizeof(Params) / 4 <= kThreads, "Params copy");
     if (threadIdx.x < sizeof(Params) / 4)
@@ -559,6 +565,12 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             uint32_t phase = 0, qphase = 0;
             bool pdl_done = false;
             long long cyc_empty = 0, cyc_atom = 0, n_units = 0;
+            // Bytes in flight set the memory system's queueing delay for every
+            // other access of the kernel (latency = in-flight / bandwidth once
+            // HBM saturates), so streaming phases keep only as many stages
+            // in flight as the bandwidth needs.
+            const int lim = max(1, min(p.max_inflight, STAGES));
+            long long kbi = 0;  // weight k-blocks issued by this CTA
             long long u = blockIdx.x;
             while (u < total_units) {
                 const Unit x = decode_unit<BN>(ps, p.nphase, gr, u);
@@ -569,8 +581,12 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                 // fetch the next unit early: the atomic's latency overlaps this unit
                 int nxt = -1;
                 if (pdl_done) nxt = atomicAdd(unit_ctr, 1);
-                for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                for (int kb = x.kb0; kb < x.kb1; ++kb, ++kbi) {
                     const long long c1 = clock64();
+                    if (lim < STAGES && kbi >= lim) {  // k-block kbi - lim consumed
+                        const long long o = kbi - lim;
+                        mbar_wait(&empty[o % STAGES], (uint32_t)((o / STAGES) & 1));
+                    }
                     mbar_wait(&empty[stage], phase ^ 1);
                     cyc_empty += clock64() - c1;
                     mbar_expect_tx(&full[stage], kABytes + x.n_pad * 128);
@@ -580,7 +596,9 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                 }
                 if (!pdl_done) {  // the unit counter is re-armed by the previous launch
                     pdl_wait();
-                    pdl_trigger();
+                    // with fused routing the next launch reads this launch's
+                    // routing output: the routing role triggers it instead
+                    if (!p.route.active) pdl_trigger();
                     pdl_done = true;
                     probe(p.probe, blockIdx.x, 2);  // PDL gate open
                     const long long c3 = clock64();
@@ -592,7 +610,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             }
             if (!pdl_done) {  // no work here: still honour PDL before exiting
                 pdl_wait();
-                pdl_trigger();
+                if (!p.route.active) pdl_trigger();
             }
             mbar_wait(&uq_empty[qi], qphase ^ 1);
             unit_q[qi] = -1;
@@ -635,6 +653,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                         }
                     } else if (x.ph > open_phase) {
                         while (ld_acquire(phase_done + x.ph - 1) < (int)gridDim.x) __nanosleep(32);
+                        // the dense epilogue packs the next block's operand in
+                        // its routing order: that routing must be complete
+                        if (p.route.active && ps[x.ph].mode == kDense)
+                            while (ld_acquire(p.route.done) == 0) __nanosleep(32);
                         open_phase = x.ph;
                         probe(p.probe, blockIdx.x, 2 + x.ph);  // phase gate open
                         // the previous phase's rows were written through the generic proxy
@@ -651,6 +673,21 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                 }
             }
             if (p.probe) p.probe[(size_t)blockIdx.x * kProbeSlots + 16] = cyc_gate;
+        }
+    } else if (warp >= 7) {
+        // ================= routing role (warps 7-8) ========================
+        // The next block's pre-gated routing (route_common.cuh), overlapped
+        // with this block's expert GEMMs; once it is complete the next launch
+        // (which schedules from it) may start.
+        if (p.route.active) {
+            pdl_wait();  // the block input comes from the previous kernel
+            if (tid == 7 * 32) probe(p.probe, blockIdx.x, 25);  // routing role past PDL
+            router_run(p.route, tid - 7 * 32, r_xs, &r_flag, p.probe);
+            if (tid == 7 * 32) {
+                while (ld_acquire(p.route.done) == 0) __nanosleep(64);
+                pdl_trigger();
+                probe(p.probe, blockIdx.x, 30);  // dependents triggered
+            }
         }
     } else if (warp == 1) {
         // ================= MMA issuer (single thread) ======================
@@ -692,6 +729,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         const int q = warp & 3;        // TMEM lane quarter this warp may access
         const int et = q * 32 + lane;  // accumulator row 0..127
         int cnt = 0, signalled = 0, qi = 0;  // phases [0, signalled) reported done
+        bool route_seen = false;
         uint32_t qphase = 0;
         // The previous launch's last CTA re-arms the counters on its way out;
         // with programmatic dependent launch this grid may already be running,
@@ -726,6 +764,12 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             const EpiRegs e = epi_regs(p, p.ph[x.ph], x);
             const int S = ps[x.ph].S;
             const int acc = cnt & 1;
+            if (e.mode == kDense && p.route.active && !route_seen) {  // next_inv comes from the routing role
+                if (et == 0)
+                    while (ld_acquire(p.route.done) == 0) __nanosleep(32);
+                named_sync(1, 128);
+                route_seen = true;
+            }
             if (e.staged) {
                 named_sync(1, 128);  // the previous unit's readers are done
                 stage_meta(e, x, et, meta_i, meta_f);
@@ -817,6 +861,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         for (int i = tid; i < gr.n; i += kThreads) grp_done[i] = 0;
         if (tid == 0) {
             for (int i = 0; i < kMaxPhases; ++i) phase_done[i] = 0;
+            if (p.route.active) *p.route.done = 0;
             p.sync[kMaxPhases] = 0;
             *unit_ctr = 0;
         }
@@ -947,6 +992,8 @@ static int run(const PhaseMaps *mp, Params p, int bn, void *ws, size_t ws_bytes,
     p.partial = reinterpret_cast<float *>(static_cast<char *>(ws) + head);
     p.partial_cap = (long long)((ws_bytes - head) / 4);
     p.probe = probe_buffer(1, kNumSMs);
+    if (p.max_inflight <= 0) p.max_inflight = 8;
+    { const char *e = getenv("PGMOE_INFLIGHT"); if (e) p.max_inflight = atoi(e); }
     if (bn <= 64) return launch<64, 8>(mp, p, s);
     return launch<256, 4>(mp, p, s);
 }
@@ -974,7 +1021,7 @@ int tc_pack_rows(const float *x, const int *perm, int n, int d, int k, uint16_t 
 int block_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
              const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, bool xb_ready,
              const void *dense_w, float *y, uint16_t *next_xb, const int *next_inv, void *ws, size_t ws_bytes,
-             cudaStream_t s) {
+             cudaStream_t s, const FusedRoute *route) {
     PG_REQUIRE(tc_supported(d, f), PGMOE_E_CONFIG, "tcgen05 path needs d, f multiples of 128 and f >= d");
     PG_REQUIRE((reinterpret_cast<uintptr_t>(experts) & 15) == 0 && stride % 16 == 0, PGMOE_E_CONFIG,
                "expert records must be 16-byte aligned");
@@ -1005,6 +1052,16 @@ int block_tc(const float *x, int T, int d, int f, int k, const void *experts, si
         p.nphase = 3;
         p.next_xb = next_xb;
         p.next_inv = next_inv;
+    }
+    if (route && route->active) {
+        PG_REQUIRE(dense_w != nullptr && fused_route_supported(route->E), PGMOE_E_CONFIG,
+                   "fused routing needs the dense phase and E in {64, 128, 256}");
+        p.route = *route;
+        // The routing role's loads queue behind the weight stream; when its
+        // work rivals the GEMMs' (small experts, many tokens) a shallower
+        // weight pipeline (lower queueing delay) finishes the block sooner
+        // (tools/gpu_inflight_sweep.sh: Base-64 T=256 -8%; Large-128 needs 8).
+        if (route->E <= 64 && n >= 64 && (size_t)d * f <= (size_t)768 * 3072) p.max_inflight = 4;
     }
     return tc::run(mp, p, (n >= 2048) ? 256 : 64, ws, ws_bytes, s);
 }

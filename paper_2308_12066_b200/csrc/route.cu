@@ -27,6 +27,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "route_common.cuh"
 
 namespace pgmoe {
 
@@ -50,72 +51,6 @@ struct RouteParams {
     double *pxsum;     // workspace: [splits][T] sum |x_i| of each K slice
     unsigned long long *probe;  // debug stamps [tiles*splits][kProbeSlots] or null
 };
-
-__device__ __forceinline__ bool better(double fa, int ia, double fb, int ib) {
-    // reference sort key (-logit, id): larger logit first, ties -> lower id
-    return fa > fb || (fa == fb && ia < ib);
-}
-
-__device__ __forceinline__ void warp_argmax(double &f, int &id) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        double of = __shfl_xor_sync(0xffffffffu, f, o);
-        int oi = __shfl_xor_sync(0xffffffffu, id, o);
-        if (oi >= 0 && (id < 0 || better(of, oi, f, id))) {
-            f = of;
-            id = oi;
-        }
-    }
-}
-
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-
-__device__ __forceinline__ double warp_sumd(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-
-// Gate row loads of V adjacent experts as exact doubles (+ |g| for the
-// column max that bounds the logit error).
-template <typename GT> struct Vec;
-template <> struct Vec<uint16_t> {
-    static constexpr int N = 4;
-    __device__ __forceinline__ static void load(const uint16_t *p, double (&d)[4], float (&a)[4]) {
-        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
-        const float f[4] = {__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
-                            __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u)};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            d[i] = f[i];
-            a[i] = fabsf(f[i]);
-        }
-    }
-    __device__ __forceinline__ static double one(const uint16_t *p) { return bf16_to_f32(__ldg(p)); }
-};
-template <> struct Vec<float> {
-    static constexpr int N = 4;
-    __device__ __forceinline__ static void load(const float *p, double (&d)[4], float (&a)[4]) {
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
-        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
-        a[0] = fabsf(v.x); a[1] = fabsf(v.y); a[2] = fabsf(v.z); a[3] = fabsf(v.w);
-    }
-    __device__ __forceinline__ static double one(const float *p) { return __ldg(p); }
-};
-template <typename GT> __device__ __forceinline__ double gval(const GT *G, size_t i) { return Vec<GT>::one(G + i); }
-
-// Serial fp64 logit in the reference order (linalg.py:35-37): out += x_i*G_ij.
-template <typename GT>
-__device__ double serial_logit(const float *x, const GT *G, int d, int E, int j) {
-    double acc = 0.0;
-    for (int i = 0; i < d; ++i) acc = __dadd_rn(acc, __dmul_rn((double)x[i], gval(G, (size_t)i * E + j)));
-    return acc;
-}
 
 // Phase 2: tokens [tok0, tok0+ntok) of tile `tile`, all splits present.
 template <typename GT>

@@ -1,0 +1,476 @@
+// route_common.cuh — certified-routing helpers shared by K1 (route.cu) and
+// the routing role fused into the tcgen05 block kernel (ffn_tc.cu).
+// Reference: gate_forward, core.py:284-305; matvec_columns, linalg.py:25-38.
+#pragma once
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace pgmoe {
+
+__device__ __forceinline__ bool better(double fa, int ia, double fb, int ib) {
+    // reference sort key (-logit, id): larger logit first, ties -> lower id
+    return fa > fb || (fa == fb && ia < ib);
+}
+
+__device__ __forceinline__ void warp_argmax(double &f, int &id) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        double of = __shfl_xor_sync(0xffffffffu, f, o);
+        int oi = __shfl_xor_sync(0xffffffffu, id, o);
+        if (oi >= 0 && (id < 0 || better(of, oi, f, id))) {
+            f = of;
+            id = oi;
+        }
+    }
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ double warp_sumd(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+
+// Gate row loads of V adjacent experts as exact doubles (+ |g| for the
+// column max that bounds the logit error).
+template <typename GT> struct Vec;
+template <> struct Vec<uint16_t> {
+    static constexpr int N = 4;
+    using Raw = uint2;
+    __device__ __forceinline__ static Raw ld(const uint16_t *p) { return __ldg(reinterpret_cast<const uint2 *>(p)); }
+    __device__ __forceinline__ static void cvt(Raw v, double (&d)[4], float (&a)[4]) {
+        const float f[4] = {__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                            __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u)};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            d[i] = f[i];
+            a[i] = fabsf(f[i]);
+        }
+    }
+    __device__ __forceinline__ static void load(const uint16_t *p, double (&d)[4], float (&a)[4]) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+        const float f[4] = {__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                            __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u)};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            d[i] = f[i];
+            a[i] = fabsf(f[i]);
+        }
+    }
+    __device__ __forceinline__ static double one(const uint16_t *p) { return bf16_to_f32(__ldg(p)); }
+};
+template <> struct Vec<float> {
+    static constexpr int N = 4;
+    using Raw = float4;
+    __device__ __forceinline__ static Raw ld(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
+    __device__ __forceinline__ static void cvt(Raw v, double (&d)[4], float (&a)[4]) {
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+        a[0] = fabsf(v.x); a[1] = fabsf(v.y); a[2] = fabsf(v.z); a[3] = fabsf(v.w);
+    }
+    __device__ __forceinline__ static void load(const float *p, double (&d)[4], float (&a)[4]) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+        a[0] = fabsf(v.x); a[1] = fabsf(v.y); a[2] = fabsf(v.z); a[3] = fabsf(v.w);
+    }
+    __device__ __forceinline__ static double one(const float *p) { return __ldg(p); }
+};
+template <typename GT> __device__ __forceinline__ double gval(const GT *G, size_t i) { return Vec<GT>::one(G + i); }
+
+// Serial fp64 logit in the reference order (linalg.py:35-37): out += x_i*G_ij.
+template <typename GT>
+__device__ double serial_logit(const float *x, const GT *G, int d, int E, int j) {
+    double acc = 0.0;
+    for (int i = 0; i < d; ++i) acc = __dadd_rn(acc, __dmul_rn((double)x[i], gval(G, (size_t)i * E + j)));
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// Routing role fused into the tcgen05 block kernel (resident placement).
+// The pre-gate of block b depends only on block b's INPUT, so the routing of
+// block b+1 is computed by two extra warps per CTA while the expert GEMMs of
+// block b stream their weights; only the dense epilogue (which packs block
+// b+1's operand in b+1's routing order) and the next launch wait for it.
+// Same arithmetic contract as route.cu: exact fp64 products, certified
+// ranking with serial reference-order recompute, reference softmax.
+// Work: units (token tile of kRouterTok tokens) x (K split) spread over the
+// grid; the last split of a tile selects (one warp per token); the last
+// tile builds histogram, scan, stable permutation and active list.
+constexpr int kRouterThreads = 64;
+constexpr int kRouterWarps = 2;
+constexpr int kRouterTok = 8;
+constexpr int kRouterMaxKn = 128;  // gate rows per split (x slice in shared memory)
+// route workspace: [counter @0 | done @64 | tile counters @256 (8192 ints) | partials]
+constexpr size_t kFusedRouteHead = 256 + 8192 * 4;
+
+struct FusedRoute {
+    int active;          // 0: this launch routes nothing
+    int gt_bf16;         // gate dtype: 1 bf16, 0 fp32
+    int d, E, T, k, splits, tiles;
+    const float *x;      // block input [T][d]
+    const void *G;       // pre-gate [d][E]
+    pgmoe_routing out;
+    int *counter;        // token tiles finished (reset by the last)
+    int *tile_counter;   // [tiles] splits finished (reset by each tile's last)
+    int *done;           // 1 once the permutation is written (re-armed at kernel exit)
+    double *plogit;      // [splits][T][E]
+    float *pcmax;        // [tiles][splits][E]
+    double *pxsum;       // [splits][T]
+};
+
+// Splits for a fused routing of T tokens: one unit per SM where possible,
+// at most kRouterMaxKn gate rows per split.
+inline int fused_route_splits(int T, int d, int grid) {
+    const int tiles = (T + kRouterTok - 1) / kRouterTok;
+    int s = std::max(1, grid / std::max(1, tiles));
+    s = std::min(s, std::max(1, d / 64));
+    s = std::min(s, 16);
+    s = std::max(s, (d + kRouterMaxKn - 1) / kRouterMaxKn);
+    return s;
+}
+inline size_t fused_route_ws_bytes(int T, int d, int E, int grid) {
+    const int s = fused_route_splits(T, d, grid);
+    const size_t tiles = (T + kRouterTok - 1) / kRouterTok;
+    return (size_t)s * T * E * 8 + 256 + tiles * s * E * 4 + 256 + (size_t)s * T * 8 + 256;
+}
+
+__device__ __forceinline__ void router_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kRouterThreads)); }
+
+// Partial fp64 logits of one (tile, split) unit.  NJ = E / 32: each thread
+// owns 4 adjacent experts x NJ tokens (64 threads cover 8 tokens x E).
+template <typename GT, int NJ>
+__device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs) {
+    const int E = r.E, T = r.T, d = r.d;
+    const int tile = unit / r.splits, split = unit - tile * r.splits;
+    const int t0 = tile * kRouterTok, ntok = min(kRouterTok, T - t0);
+    const int k0 = (int)((long)d * split / r.splits), k1 = (int)((long)d * (split + 1) / r.splits);
+    const int kn = k1 - k0;
+    for (int i0 = rt; i0 < kRouterTok * kn; i0 += 8 * kRouterThreads) {  // 8 loads in flight
+        float v[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int i = i0 + b * kRouterThreads, t = i / kn;
+            v[b] = (i < kRouterTok * kn && t < ntok) ? __ldg(r.x + (size_t)(t0 + t) * d + k0 + (i - t * kn)) : 0.f;
+        }
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if (i0 + b * kRouterThreads < kRouterTok * kn) xs[i0 + b * kRouterThreads] = v[b];
+    }
+    router_sync();
+    const int lane = rt & 31, w = rt >> 5;
+    for (int t = w; t < ntok; t += kRouterWarps) {  // sum |x_i| over the slice (bounds the error)
+        double sx = 0.0;
+        for (int i = lane; i < kn; i += 32) sx += fabs((double)xs[t * kn + i]);
+        sx = warp_sumd(sx);
+        if (lane == 0) r.pxsum[(size_t)split * T + t0 + t] = sx;
+    }
+    constexpr int CG = 8 * NJ;  // E / 4 column groups
+    const int cg = rt % CG, tg = rt / CG;
+    double acc[NJ][4];
+    float cm[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int tt = 0; tt < NJ; ++tt)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[tt][v] = 0.0;
+    const GT *G = static_cast<const GT *>(r.G) + (size_t)k0 * E + cg * 4;
+    // 16 gate rows in flight per thread (raw, converted on use): this role
+    // runs next to the expert GEMMs' full-bandwidth weight stream, so every
+    // load sees the loaded memory latency (in-flight bytes / bandwidth)
+    using Raw = typename Vec<GT>::Raw;
+    constexpr int RB = sizeof(Raw) <= 8 ? 16 : 8;
+    for (int i0 = 0; i0 < kn; i0 += RB) {
+        Raw raw[RB];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) raw[b] = Vec<GT>::ld(G + (size_t)min(i0 + b, kn - 1) * E);
+#pragma unroll
+        for (int b = 0; b < RB; ++b) {
+            if (i0 + b < kn) {
+                double g[4];
+                float a[4];
+                Vec<GT>::cvt(raw[b], g, a);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) cm[v] = fmaxf(cm[v], a[v]);
+#pragma unroll
+                for (int tt = 0; tt < NJ; ++tt) {
+                    const double xv = xs[(tg * NJ + tt) * kn + i0 + b];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[tt][v] = fma(xv, g[v], acc[tt][v]);  // exact product, one rounding
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int tt = 0; tt < NJ; ++tt) {
+        const int t = tg * NJ + tt;
+        if (t < ntok)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) r.plogit[((size_t)split * T + t0 + t) * E + cg * 4 + v] = acc[tt][v];
+    }
+    if (tg == 0)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) r.pcmax[((size_t)tile * r.splits + split) * E + cg * 4 + v] = cm[v];
+    router_sync();  // the x slice is rewritten by the next unit
+}
+
+// One token's certified selection + softmax, by one warp (select_tile's
+// per-token logic with the E logits in registers, NJ per lane).
+template <typename GT, int NJ>
+__device__ void router_select_token(const FusedRoute &r, int tile, int tok, int lane) {
+    const int E = r.E, T = r.T, S = r.splits, k = r.k, d = r.d;
+    const double u = 1.1102230246251565e-16;  // 2^-53
+    const double gam = (double)d * u / (1.0 - (double)d * u);
+    const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
+    const double bpad = 1e-300;
+    double sx = 0.0;
+    for (int z = lane; z < S; z += 32) sx += __ldcg(r.pxsum + (size_t)z * T + tok);
+    sx = warp_sumd(sx) * (1.0 + 2.0 * gam);
+    double lg[NJ], bd[NJ];
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) {
+        const int j = lane + 32 * jj;
+        double sum = 0.0;
+        float cm = 0.f;
+        for (int z0 = 0; z0 < S; z0 += 16) {  // all splits' partials in flight, then summed in split order
+            double pl[16];
+            float pc[16];
+#pragma unroll
+            for (int z = 0; z < 16; ++z) {
+                pl[z] = z0 + z < S ? __ldcg(r.plogit + ((size_t)(z0 + z) * T + tok) * E + j) : 0.0;
+                pc[z] = z0 + z < S ? __ldcg(r.pcmax + ((size_t)tile * S + z0 + z) * E + j) : 0.f;
+            }
+#pragma unroll
+            for (int z = 0; z < 16; ++z)
+                if (z0 + z < S) {
+                    sum += pl[z];
+                    cm = fmaxf(cm, pc[z]);
+                }
+        }
+        lg[jj] = sum;
+        bd[jj] = bscale * sx * (double)cm + bpad;
+    }
+    auto pick = [&](const double (&a)[NJ], int bi) -> double {  // a[bi >> 5] of lane bi & 31
+        double mine = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+            if (jj == (bi >> 5)) mine = a[jj];
+        return __shfl_sync(0xffffffffu, mine, bi & 31);
+    };
+    bool finite = true;
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) finite &= (bool)isfinite(lg[jj]);
+    finite = __all_sync(0xffffffffu, finite);
+    if (!finite) {  // core.py:297
+        if (lane == 0) atomicCAS(r.out.status, 0, (int)PGMOE_E_GATE_OVERFLOW);
+        for (int s = lane; s < k; s += 32) {
+            r.out.ids[(size_t)tok * k + s] = 0;
+            r.out.w[(size_t)tok * k + s] = 0.f;
+        }
+        return;
+    }
+    int sel[8];
+    uint32_t taken = 0;
+    bool certified = true;
+    double minlow = INFINITY;
+    for (int s = 0; s < k; ++s) {
+        double bf = -INFINITY;
+        int bi = -1;
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+            if (!(taken >> jj & 1u) && (bi < 0 || better(lg[jj], lane + 32 * jj, bf, bi))) {
+                bf = lg[jj];
+                bi = lane + 32 * jj;
+            }
+        warp_argmax(bf, bi);
+        sel[s] = bi;
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+        const double low = bf - pick(bd, bi);
+        minlow = fmin(minlow, low);
+        double up = -INFINITY;
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+            if (!(taken >> jj & 1u)) up = fmax(up, lg[jj] + bd[jj]);
+        up = warp_max(up);
+        certified &= (low > up);
+    }
+    if (!certified) {  // recompute the candidates in the reference's serial order
+        uint32_t cand = 0;
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+            if (lg[jj] + bd[jj] >= minlow) cand |= 1u << jj;
+        const GT *G = static_cast<const GT *>(r.G);
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+            if (cand >> jj & 1u) lg[jj] = serial_logit<GT>(r.x + (size_t)tok * d, G, d, E, lane + 32 * jj);
+        for (int s = 0; s < k; ++s) {
+            double bf = -INFINITY;
+            int bi = -1;
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj)
+                if ((cand >> jj & 1u) && (bi < 0 || better(lg[jj], lane + 32 * jj, bf, bi))) {
+                    bf = lg[jj];
+                    bi = lane + 32 * jj;
+                }
+            warp_argmax(bf, bi);
+            sel[s] = bi;
+            if ((bi & 31) == lane) cand &= ~(1u << (bi >> 5));
+        }
+        if (lane == 0) atomicAdd(r.out.status + 1, 1);
+    }
+    // softmax over all E (linalg.py:54-59), max-subtracted; same order as route.cu
+    double m = -INFINITY;
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) m = fmax(m, lg[jj]);
+    m = warp_max(m);
+    double z = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) z += exp(lg[jj] - m);
+    z = warp_sumd(z);
+    for (int s = 0; s < k; ++s) {
+        const double pr = exp(pick(lg, sel[s]) - m) / z;
+        if (lane == 0) {
+            if (!(pr > 0.0)) atomicCAS(r.out.status, 0, (int)PGMOE_E_GATE_UNDERFLOW);
+            r.out.ids[(size_t)tok * k + s] = sel[s];
+            r.out.w[(size_t)tok * k + s] = __double2float_rn(pr);
+        }
+    }
+}
+
+// Histogram, exclusive scan, stable permutation, active list (permute_all
+// of route.cu with the router's two warps).  sm: >= 3 * E ints.
+static __device__ __noinline__ void router_permute(const FusedRoute &r, int rt, int *sm) {
+    const int E = r.E, k = r.k, lane = rt & 31, w = rt >> 5;
+    const int N = r.T * k;
+    int *whist = sm;                        // [kRouterWarps][E] -> cursors
+    int *tot = whist + kRouterWarps * E;    // [E]
+    for (int i = rt; i < kRouterWarps * E; i += kRouterThreads) whist[i] = 0;
+    router_sync();
+    const int seg = (N + kRouterWarps - 1) / kRouterWarps;
+    const int r0 = w * seg, r1 = min(N, r0 + seg);
+    for (int i = r0 + lane; i < r1; i += 32) atomicAdd(&whist[w * E + __ldcg(r.out.ids + i)], 1);
+    router_sync();
+    for (int e = rt; e < E; e += kRouterThreads) {
+        int s = 0;
+        for (int ww = 0; ww < kRouterWarps; ++ww) s += whist[ww * E + e];
+        tot[e] = s;
+    }
+    router_sync();
+    if (w == 0) {
+        int run = 0, nact = 0;
+        for (int e0 = 0; e0 < E; e0 += 32) {
+            const int e = e0 + lane;
+            const int h = e < E ? tot[e] : 0;
+            int incl = h;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const unsigned am = __ballot_sync(0xffffffffu, h > 0);
+            if (e < E) {
+                const int ex = run + incl - h;
+                r.out.hist[e] = h;
+                r.out.off[e] = ex;
+                tot[e] = ex;
+                if (h > 0) r.out.act[nact + __popc(am & ((1u << lane) - 1u))] = e;
+            }
+            run += __shfl_sync(0xffffffffu, incl, 31);
+            nact += __popc(am);
+        }
+        if (lane == 0) {
+            r.out.off[E] = run;
+            *r.out.n_act = nact;
+        }
+    }
+    router_sync();
+    for (int e = rt; e < E; e += kRouterThreads) {
+        int base = tot[e];
+        for (int ww = 0; ww < kRouterWarps; ++ww) {
+            const int c = whist[ww * E + e];
+            whist[ww * E + e] = base;
+            base += c;
+        }
+    }
+    router_sync();
+    const unsigned ltmask = (1u << lane) - 1u;
+    for (int c0 = r0; c0 < r1; c0 += 32) {
+        const int i = c0 + lane;
+        const bool valid = i < r1;
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            const int e = __ldcg(r.out.ids + i);
+            const unsigned grp = __match_any_sync(vm, e);
+            const int rank = __popc(grp & ltmask);
+            const int pos = whist[w * E + e] + rank;
+            r.out.perm[pos] = i;
+            if (r.out.inv) r.out.inv[i] = pos;
+            r.out.w_perm[pos] = __ldcg(r.out.w + i);
+            __syncwarp(vm);
+            if (rank == __popc(grp) - 1) whist[w * E + e] += __popc(grp);
+        }
+        __syncwarp();
+    }
+}
+
+// The whole routing role (64 threads, rt = 0..63) for one CTA.
+template <typename GT, int NJ>
+__device__ void router_role(const FusedRoute &r, int rt, float *xs, int *s_flag, unsigned long long *pr) {
+    const int lane = rt & 31, w = rt >> 5;
+    const int units = r.tiles * r.splits;
+    for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+        router_logits<GT, NJ>(r, unit, rt, xs);
+        if (rt == 0) probe(pr, blockIdx.x, 26);  // partial logits written
+        const int tile = unit / r.splits;
+        __threadfence();
+        router_sync();
+        if (rt == 0) *s_flag = (atomicAdd(r.tile_counter + tile, 1) == r.splits - 1);
+        router_sync();
+        if (!*s_flag) continue;
+        __threadfence();
+        const int t0 = tile * kRouterTok, ntok = min(kRouterTok, r.T - t0);
+        if (rt == 0) probe(pr, blockIdx.x, 27);  // tile select start
+        for (int t = w; t < ntok; t += kRouterWarps) router_select_token<GT, NJ>(r, tile, t0 + t, lane);
+        __threadfence();
+        router_sync();
+        if (rt == 0) probe(pr, blockIdx.x, 28);  // tile selected
+        if (rt == 0) {
+            r.tile_counter[tile] = 0;
+            *s_flag = (atomicAdd(r.counter, 1) == r.tiles - 1);
+        }
+        router_sync();
+        if (!*s_flag) continue;
+        __threadfence();
+        router_permute(r, rt, reinterpret_cast<int *>(xs));
+        __threadfence();
+        router_sync();
+        if (rt == 0) probe(pr, blockIdx.x, 29);  // permutation written
+        if (rt == 0) {
+            *r.counter = 0;
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(r.done), "r"(1) : "memory");
+        }
+    }
+}
+
+template <int NJ>
+__device__ __forceinline__ void router_dispatch_gt(const FusedRoute &r, int rt, float *xs, int *s_flag,
+                                                   unsigned long long *pr) {
+    if (r.gt_bf16) router_role<uint16_t, NJ>(r, rt, xs, s_flag, pr);
+    else router_role<float, NJ>(r, rt, xs, s_flag, pr);
+}
+__device__ __forceinline__ void router_run(const FusedRoute &r, int rt, float *xs, int *s_flag,
+                                           unsigned long long *pr) {
+    switch (r.E) {
+        case 64: router_dispatch_gt<2>(r, rt, xs, s_flag, pr); break;
+        case 128: router_dispatch_gt<4>(r, rt, xs, s_flag, pr); break;
+        case 256: router_dispatch_gt<8>(r, rt, xs, s_flag, pr); break;
+        default: break;  // the host only fuses E in {64, 128, 256}
+    }
+}
+inline bool fused_route_supported(int E) { return E == 64 || E == 128 || E == 256; }
+
+}  // namespace pgmoe

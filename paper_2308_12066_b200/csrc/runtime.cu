@@ -22,6 +22,7 @@
 #include "expert_cache.h"
 #include "kernels.h"
 #include "rng.h"
+#include "route_common.cuh"
 
 namespace pgmoe {
 
@@ -128,6 +129,8 @@ struct pgmoe_model {
     GraphEntry graphs[8];  // small LRU: callers' output buffers rotate through the allocator
     unsigned long long graph_clock = 0;
     int64_t fused_blocks = 0;  // blocks whose dense layer ran inside the expert launch
+    int64_t fused_routes = 0;  // pre-gates computed inside the block launch
+    bool fuse_route = true;    // resident: route inside the block launch (pgmoe_model_set_fused_route)
     // host-buffer entry point
     cudaStream_t io_stream = nullptr;
     float *io_x = nullptr, *io_y = nullptr, *io_w = nullptr;
@@ -357,6 +360,36 @@ static int route_into(pgmoe_model *m, const float *x, int T, const void *G, int 
     return PGMOE_OK;
 }
 
+// The pre-gate of block b, computed inside block b's tcgen05 launch (route
+// workspace layout: counter @0, done flag @64, tile counters @256, partials
+// after kFusedRouteHead).
+static FusedRoute fused_route_args(pgmoe_model *m, const float *x, int T, const void *G, const pgmoe_routing &out) {
+    const auto &c = m->cfg;
+    FusedRoute r{};
+    r.active = 1;
+    r.gt_bf16 = m->wdtype == PGMOE_BF16;
+    r.d = c.d_model;
+    r.E = c.num_experts;
+    r.T = T;
+    r.k = c.top_k;
+    r.splits = fused_route_splits(T, c.d_model, kNumSMs);
+    r.tiles = (T + kRouterTok - 1) / kRouterTok;
+    r.x = x;
+    r.G = G;
+    r.out = out;
+    char *ws = static_cast<char *>(m->route_ws);
+    r.counter = reinterpret_cast<int *>(ws);
+    r.done = reinterpret_cast<int *>(ws + 64);
+    r.tile_counter = reinterpret_cast<int *>(ws + 256);
+    char *q = ws + kFusedRouteHead;
+    r.plogit = reinterpret_cast<double *>(q);
+    q += ((size_t)r.splits * T * c.num_experts * 8 + 255) & ~(size_t)255;
+    r.pcmax = reinterpret_cast<float *>(q);
+    q += ((size_t)r.tiles * r.splits * c.num_experts * 4 + 255) & ~(size_t)255;
+    r.pxsum = reinterpret_cast<double *>(q);
+    return r;
+}
+
 int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, int32_t *ids_trace,
                       float *w_trace, cudaStream_t s) {
     const auto &c = m->cfg;
@@ -384,6 +417,11 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
     const int strat = off ? m->strategy : PGMOE_PRE_GATED;
     const bool prefetch_all = off && strat == PGMOE_PREFETCH_ALL;
     bool xb_ready = false;
+    // Resident top-1 blocks compute their pre-gate inside the block launch
+    // (it depends only on the block input); offloaded blocks keep the
+    // separate K1 launch because the host needs the active list at once.
+    const bool fuse_route = !off && use_tc(m) && c.top_k == 1 && L == 1 && m->fuse_route &&
+                            fused_route_supported(c.num_experts) && T <= (1 << 16);
     const float *cur = x_in;
     for (int b = 0; b < nb; ++b) {
         const BlockW &bw = m->blocks[b];
@@ -397,9 +435,14 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
             PG_TRY(route_into(m, cur, T, bw.gate, ri, off && !prefetch_all, s, "gate", b));
             if (off && strat == PGMOE_PRE_GATED) PG_TRY(issue_fetch(m, b, ri));  // exposed serial fetch
         }
+        FusedRoute fr{};
         if (has_pre_gate(c, b)) {
             const int tr = (b + L) % R;
-            PG_TRY(route_into(m, cur, T, bw.pre_gate, tr, off && !prefetch_all, s, "pre_gate", b));
+            if (fuse_route) {
+                fr = fused_route_args(m, cur, T, bw.pre_gate, m->routing[tr].r);
+            } else {
+                PG_TRY(route_into(m, cur, T, bw.pre_gate, tr, off && !prefetch_all, s, "pre_gate", b));
+            }
             if (off && strat == PGMOE_PRE_GATED) pending_fetch = b + L;
         }
         if (off && strat == PGMOE_ON_DEMAND) {  // fetch starts once compute reaches block b
@@ -423,7 +466,8 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
             tl_begin(m, "compute", "experts", b, s);
             PG_TRY(block_tc(cur, T, c.d_model, c.d_ff, 1, experts, m->rec_bytes, indexed, &rb.r, m->xb, m->hb, m->yw,
                             m->mixb, xb_ready, bw.dense, nxt, next_r ? m->xb : nullptr, next_r ? next_r->inv : nullptr,
-                            m->tc_ws, m->tc_ws_bytes, s));
+                            m->tc_ws, m->tc_ws_bytes, s, fr.active ? &fr : nullptr));
+            if (fr.active) m->fused_routes++;
             tl_end(m, s);
             if (off) {
                 PG_CUDA(cudaEventRecord(m->done[ri], s));
@@ -603,7 +647,9 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
         if ((st = alloc_routing(m->routing[i], max_tokens, c.num_experts, (int)k)) != PGMOE_OK) return fail(st);
         cudaEventCreateWithFlags(&m->routed[i], cudaEventDisableTiming);
     }
-    const size_t rws = pgmoe_route_workspace_bytes(max_tokens, c.num_experts);
+    size_t rws = pgmoe_route_workspace_bytes(max_tokens, c.num_experts);
+    for (int t = 1; t <= max_tokens; ++t)  // the routing role fused into the block kernel (resident)
+        rws = std::max(rws, kFusedRouteHead + fused_route_ws_bytes(t, d, c.num_experts, kNumSMs));
     if (cudaMalloc(&m->route_ws, rws) != cudaSuccess || cudaMemset(m->route_ws, 0, rws) != cudaSuccess)
         return fail(PGMOE_E_OOM);
     const size_t T = max_tokens;
@@ -744,9 +790,26 @@ extern "C" int pgmoe_cache_replay(int32_t policy, int32_t capacity_records, cons
     return PGMOE_OK;
 }
 
+// Captured decoder graphs bake the launch sequence: drop them when it changes.
+static void drop_graphs(pgmoe_model *m) {
+    cudaDeviceSynchronize();
+    for (auto &g : m->graphs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g = pgmoe_model::GraphEntry{};
+    }
+}
+
 extern "C" int pgmoe_model_set_kernel(pgmoe_model *m, int32_t kernel) {
     PG_REQUIRE(kernel >= PGMOE_KERNEL_AUTO && kernel <= PGMOE_KERNEL_TCGEN05, PGMOE_E_CONFIG, "bad kernel %d", kernel);
+    if (m->kernel != kernel) drop_graphs(m);
     m->kernel = kernel;
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_model_set_fused_route(pgmoe_model *m, int32_t enabled) {
+    PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
+    if (m->fuse_route != (enabled != 0)) drop_graphs(m);
+    m->fuse_route = enabled != 0;
     return PGMOE_OK;
 }
 
@@ -1050,6 +1113,7 @@ extern "C" int pgmoe_model_stats(pgmoe_model *m, pgmoe_stats *out) {
     m->stats.route_fallbacks = fb;
     m->stats.route_flips = 0;
     m->stats.fused_blocks = m->fused_blocks;
+    m->stats.fused_routes = m->fused_routes;
     *out = m->stats;
     return PGMOE_OK;
 }
@@ -1063,6 +1127,7 @@ extern "C" int pgmoe_model_reset_stats(pgmoe_model *m) {
     m->stats.slot_capacity_bytes = slot;
     m->stats.cache_bytes = cb;
     m->fused_blocks = 0;
+    m->fused_routes = 0;
     return PGMOE_OK;
 }
 

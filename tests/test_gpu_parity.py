@@ -291,6 +291,43 @@ def test_offloaded_equals_resident_and_ledger(dtype):
     off.close()
 
 
+@pytest.mark.parametrize("E,T", [(64, 1), (64, 40), (128, 300), (256, 17)])
+def test_fused_routing_equals_separate_launch_and_offloaded(E, T):
+    """Resident top-1 decoding computes each pre-gate inside the block's
+    tcgen05 launch (route_common.cuh).  Routing ids, weights and block
+    outputs must equal the separate-K1 schedule and the offloaded one bitwise,
+    including tokens whose ranking needs the serial-fp64 recompute (exact
+    ties planted in block 0's pre-gate)."""
+    dims = og.Dims(256, 512, 5, E, 1, seed=7)
+    x0 = torch.from_numpy(tokens(256, T)).cuda()
+    fused = _device_model(dims, "bf16", "resident", max_tokens=T)
+    sep = _device_model(dims, "bf16", "resident", max_tokens=T)
+    sep.set_fused_route(False)
+    off = _device_model(dims, "bf16", "offloaded", max_tokens=T)
+    g = fused.get_matrix("pre_gate", 0)
+    g[:, 1] = g[:, 0]  # exact ties between experts 0, 1 and 2
+    g[:, 2] = g[:, 0]
+    for m in (fused, sep, off):
+        m.set_matrix("pre_gate", 0, -1, g)
+    outs = []
+    for m in (fused, sep, off):
+        m.reset_stats()
+        for _ in range(2):  # the second call replays the captured graph (resident)
+            y, ids, w = m.decoder_iteration(x0, trace=True)
+        torch.cuda.synchronize()
+        outs.append((y.clone(), ids.clone(), w.clone()))
+    nf = fused.stats()["fused_routes"]  # counted per host pass (a graph capture is one pass)
+    assert nf > 0 and nf % (dims.num_blocks - 1) == 0
+    assert sep.stats()["fused_routes"] == 0
+    for y, ids, w in outs[1:]:
+        assert torch.equal(outs[0][1], ids) and torch.equal(outs[0][2], w)
+        assert torch.equal(outs[0][0], y)
+    st_f, st_s = fused.stats(), sep.stats()
+    assert st_f["route_fallbacks"] == st_s["route_fallbacks"]
+    for m in (fused, sep, off):
+        m.close()
+
+
 def test_timeline_schema_and_causality():
     dims = og.Dims(128, 256, 4, 8, 1)
     m = _device_model(dims, "bf16", "offloaded", max_tokens=8)

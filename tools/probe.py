@@ -31,9 +31,8 @@ PRESETS = {
 ROUTE_SLOTS = {0: "entry", 1: "pdl", 2: "logits", 3: "sel0", 7: "selred", 8: "ranked", 4: "sel1", 5: "perm0",
                6: "perm1"}
 BLOCK_SLOTS = {0: "entry", 1: "prolog", 2: "gate0", 3: "gate1", 4: "gate2", 5: "acc0", 6: "ph0", 7: "ph1",
-               8: "ph2", 11: "lastld", 12: "accN", 13: "partN", 14: "fixN", 23: "t0ld", 24: "t0st", 25: "t1ld", 26: "t1st", 27: "t2ld", 28: "t2st",
-               29: "t3ld", 30: "t3st", 15: "endN",
-               9: "exit"}
+               8: "ph2", 11: "lastld", 12: "accN", 13: "partN", 14: "fixN", 15: "endN",
+               25: "r_pdl", 26: "r_logits", 27: "r_sel0", 28: "r_sel1", 29: "r_perm", 30: "r_trig", 9: "exit"}
 ROWS = 1 << 15
 
 
@@ -63,10 +62,13 @@ def main():
     ap.add_argument("--tokens", type=int, default=1)
     ap.add_argument("--blocks", type=int, default=4, help="blocks of the iteration to print")
     ap.add_argument("--cta-detail", action="store_true")
+    ap.add_argument("--no-fused-route", action="store_true", help="resident: separate K1 launches")
     args = ap.parse_args()
     L = _lib.load()
     cfg = P.ModelConfig(top_k=1, activation_level=1, seed=0, **PRESETS[args.preset])
     m = P.DeviceModel(cfg, dtype="bf16", placement=args.placement, max_tokens=args.tokens)
+    if args.no_fused_route:
+        m.set_fused_route(False)
     x = torch.from_numpy(token_batch(0, cfg.d_model, args.tokens)).cuda()
     y = torch.empty_like(x)
     pr = torch.zeros((ROWS, 32), dtype=torch.int64, device="cuda")
@@ -89,17 +91,20 @@ def main():
     ra = pr.cpu().numpy().astype(np.int64)
     ba = pb.cpu().numpy().astype(np.int64)
     nr = int((ra[:, 0] > 0).sum())
-    route_ctas = nr // nb  # nb route launches per iteration
-    rl = [ra[i * route_ctas:(i + 1) * route_ctas] for i in range(nb)]
+    fused = m.stats()["fused_routes"] > 0
+    n_route = 1 if fused else nb  # block 0's gate (+ every pre-gate unless fused into the block launch)
+    route_ctas = nr // n_route
+    rl = [ra[i * route_ctas:(i + 1) * route_ctas] for i in range(n_route)]
     bl = [ba[i * 148:(i + 1) * 148] for i in range(nb)]
     t0 = min(r[:, 0][r[:, 0] > 0].min() for r in rl + bl)
     res = {"preset": args.preset, "placement": args.placement, "T": T, "route_ctas": route_ctas,
            "iteration_us": round(float((max(b[:, 9].max() for b in bl) - t0) / 1e3), 2), "launches": []}
     order = [("route", 0, rl[0])]
     for b in range(nb):
-        if b + 1 < nb:
+        if b + 1 < nb and not fused:
             order.append(("route", b, rl[b + 1]))
         order.append(("block", b, bl[b]))
+    res["fused_route"] = fused
     for kind, b, rows in order:
         if b >= args.blocks and b < nb - 1:
             continue
@@ -116,7 +121,7 @@ def main():
                 v = rows[:, s]
                 if (v > 0).any():
                     c = int(np.argmax(v))
-                    res["launches"].append({"cta": c, "phase_slot": s, "store_chunk0_cycles": int(rows[c, 31]),
+                    res["launches"].append({"cta": c, "phase_slot": s, 
                                             "row": {BLOCK_SLOTS[k]: round(float((rows[c, k] - t0) / 1e3), 2)
                                                     for k in BLOCK_SLOTS if rows[c, k] > 0}})
     # effective SM clock over each block kernel CTA: d(clock64) / d(globaltimer)

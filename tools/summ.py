@@ -23,6 +23,7 @@ if os.path.exists(p):
         for e in x["launches"]:
             if "kind" in e:
                 keys = ["pdl", "logits", "sel0", "selred", "ranked", "sel1", "perm1"] if e["kind"] == "route" else \
-                    ["entry", "gate0", "ph0", "gate1", "ph1", "gate2", "ph2", "exit"]
+                    ["entry", "gate0", "ph0", "gate1", "ph1", "r_pdl", "r_logits", "r_sel0", "r_sel1", "r_perm",
+                     "gate2", "ph2", "exit"]
                 print("   ", e["kind"], e["block"], " ".join(f"{k}={e[k][2] if k not in ('entry',) else e[k][0]}"
                                                          for k in keys if k in e))
