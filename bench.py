@@ -117,14 +117,25 @@ def measure_pcie_gbs(torch, nbytes=1 << 30) -> float:
     return gbs
 
 
-def ncu_traffic(kernel_label: str):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    summary (profiles/*_ncu_summary.json), or None."""
+def workload_name(preset: str, placement: str, tokens: int) -> str:
+    """BASELINE.json configs index of a single-GPU workload."""
+    idx = {("base8", "offloaded"): 0, ("base8", "resident"): 0, ("base64", "resident"): 1,
+           ("base128", "offloaded"): 2, ("large128", "offloaded"): 3}.get((preset, placement))
+    tag = f" (BASELINE configs[{idx}])" if idx is not None else ""
+    return f"Switch-{preset} {placement} pre-gated T={tokens}{tag}"
+
+
+def ncu_traffic(kernel_label: str, workload: str):
+    """Per-launch DRAM bytes (read + write) of the dominant kernel from the
+    committed ncu summary of THIS workload (profiles/*ncu_summary*.json
+    carrying the same `workload`), or None."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_summary*.json")), reverse=True):
         try:
             with open(path) as fh:
                 s = json.load(fh)
+            if s.get("workload") != workload:
+                continue
             k = s.get("kernels", {}).get(kernel_label)
             if k and k.get("dram_bytes_per_launch"):
                 return k["dram_bytes_per_launch"]
@@ -266,6 +277,9 @@ def run_ours(args, rank: int, world: int):
     fused = st.get("fused_blocks", 0) > 0
     if fused:  # the dense layer runs inside the same launch: its weights and activations
         ffn_bytes += prof_steps * nb * (d * d * sw + T * d * (2 + 4))
+    routed_in_launch = st.get("fused_routes", 0) > 0
+    if routed_in_launch:  # resident: the next block's pre-gate (gate weights + block input) too
+        ffn_bytes += prof_steps * (nb - 1) * (d * E * sw + T * d * 4)
     ffn_gbs = ffn_bytes / ffn_s / 1e9 if ffn_s > 0 else None
     h2d_s = sum(e["end_s"] - e["start_s"] for e in fetch)
     pcie_gbs = measure_pcie_gbs(torch)
@@ -313,7 +327,7 @@ def run_ours(args, rank: int, world: int):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (reference RNG weights/tokens, SURVEY §8(d))",
-        "config": {"workload": f"Switch-{args.preset} {args.placement} pre-gated (BASELINE configs[3])",
+        "config": {"workload": workload_name(args.preset, args.placement, T),
                    "preset": args.preset, "placement": args.placement, "tokens_per_rank": T,
                    "global_batch": T * world, "num_blocks": nb, "d_model": d, "d_ff": f, "num_experts": E,
                    "top_k": 1, "activation_level": 1, "parallelism": f"sequences x{world} (replicas)",
@@ -323,10 +337,12 @@ def run_ours(args, rank: int, world: int):
         "block_roofline": {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / block_ms, 4),
                            "bound": "pcie" if pcie_b and pcie_b / (pcie_gbs * 1e9) >= hbm_b / (hbm_peak * 1e9) else "hbm",
                            "n_act_avg": round(nact_avg, 2)},
-        "roofline": {"bound": "hbm", "kernel": "K2 up+down" + (" + K3 dense, one launch" if fused else ""),
+        "roofline": {"bound": "hbm", "kernel": "K2 up+down" + (" + K3 dense" if fused else "") +
+                     (" + next block's K1 routing" if routed_in_launch else "") + (", one launch" if fused else ""),
                      "achieved": round(ffn_gbs, 1) if ffn_gbs else None, "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(ffn_gbs / hbm_peak, 4) if ffn_gbs else None,
-                     "traffic": ncu_traffic("ffn"), "peak_kind": peak_kind,
+                     "traffic": ncu_traffic("ffn", workload_name(args.preset, args.placement, T)),
+                     "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": round(ffn_bytes / max(1, len(ffn))),
                      "avg_launch_us": round(ffn_s / max(1, len(ffn)) * 1e6, 2)},
         "migration": {"h2d_gbs": round(h2d_gbs, 2) if h2d_gbs else None, "pcie_measured_gbs": round(pcie_gbs, 2),

@@ -105,7 +105,7 @@ __device__ double serial_logit(const float *x, const GT *G, int d, int E, int j)
 constexpr int kRouterThreads = 64;
 constexpr int kRouterWarps = 2;
 constexpr int kRouterTok = 8;
-constexpr int kRouterMaxKn = 128;  // gate rows per split (x slice in shared memory)
+constexpr int kRouterMaxKn = 256;  // gate rows per split (x slice in shared memory)
 // route workspace: [counter @0 | done @64 | tile counters @256 (8192 ints) | partials]
 constexpr size_t kFusedRouteHead = 256 + 8192 * 4;
 
