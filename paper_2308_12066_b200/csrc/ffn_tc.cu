@@ -365,7 +365,8 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
     // One copy in shared memory makes every such read an LDS.
     __shared__ Params p_sh;
     __shared__ PhaseSched ps[kMaxPhases];
-    __shared__ float r_xs[kRouterTok * kRouterMaxKn];  // routing role: x slice / permutation scratch
+    __shared__ __align__(16) float r_xs[kRouterSmemFloats];  // routing role: x slice, reduction, permutation
+    static_assert(kRouterSmemFloats >= kRouterTok * kRouterMaxKn, "routing x slice");
     __shared__ int r_flag;
     __shared__ long long s_total_units;
     static_assert(sizeof(Params) % 4 == 0 && sizeof(Params) / 4 <= kThreads, "Params copy");

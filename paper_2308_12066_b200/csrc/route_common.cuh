@@ -143,7 +143,14 @@ inline size_t fused_route_ws_bytes(int T, int d, int E, int grid) {
 __device__ __forceinline__ void router_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kRouterThreads)); }
 
 // Partial fp64 logits of one (tile, split) unit.  NJ = E / 32: each thread
-// owns 4 adjacent experts x NJ tokens (64 threads cover 8 tokens x E).
+// owns 4 adjacent experts x NJ tokens (64 threads cover 8 tokens x E).  When
+// the tile holds <= NJ tokens (small batches) the token groups take row
+// slices instead and are summed in shared memory in a fixed order, so each
+// thread has a quarter (E=64) or half (E=128) of the rows to load: at small T
+// every gate load waits behind the block's weight prefetch, and the number
+// of dependent load rounds is the routing role's critical path.
+constexpr int kRouterSmemFloats = 3328;  // x slice + row-split reduction (13 KB)
+
 template <typename GT, int NJ>
 __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs) {
     const int E = r.E, T = r.T, d = r.d;
@@ -151,16 +158,20 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs) 
     const int t0 = tile * kRouterTok, ntok = min(kRouterTok, T - t0);
     const int k0 = (int)((long)d * split / r.splits), k1 = (int)((long)d * (split + 1) / r.splits);
     const int kn = k1 - k0;
-    for (int i0 = rt; i0 < kRouterTok * kn; i0 += 8 * kRouterThreads) {  // 8 loads in flight
+    constexpr int CG = 8 * NJ;                 // E / 4 column groups
+    constexpr int TG = kRouterThreads / CG;    // token (or row) groups
+    const bool rowsplit = TG > 1 && ntok <= NJ;
+    const int tslots = rowsplit ? NJ : kRouterTok;
+    for (int i0 = rt; i0 < tslots * kn; i0 += 8 * kRouterThreads) {  // 8 loads in flight
         float v[8];
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
             const int i = i0 + b * kRouterThreads, t = i / kn;
-            v[b] = (i < kRouterTok * kn && t < ntok) ? __ldg(r.x + (size_t)(t0 + t) * d + k0 + (i - t * kn)) : 0.f;
+            v[b] = (i < tslots * kn && t < ntok) ? __ldg(r.x + (size_t)(t0 + t) * d + k0 + (i - t * kn)) : 0.f;
         }
 #pragma unroll
         for (int b = 0; b < 8; ++b)
-            if (i0 + b * kRouterThreads < kRouterTok * kn) xs[i0 + b * kRouterThreads] = v[b];
+            if (i0 + b * kRouterThreads < tslots * kn) xs[i0 + b * kRouterThreads] = v[b];
     }
     router_sync();
     const int lane = rt & 31, w = rt >> 5;
@@ -170,8 +181,10 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs) 
         sx = warp_sumd(sx);
         if (lane == 0) r.pxsum[(size_t)split * T + t0 + t] = sx;
     }
-    constexpr int CG = 8 * NJ;  // E / 4 column groups
     const int cg = rt % CG, tg = rt / CG;
+    const int tbase = rowsplit ? 0 : tg * NJ;
+    const int rstart = rowsplit ? tg : 0, rstep = rowsplit ? TG : 1;
+    const int nrows = rowsplit ? (kn - tg + TG - 1) / TG : kn;
     double acc[NJ][4];
     float cm[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -180,17 +193,19 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs) 
         for (int v = 0; v < 4; ++v) acc[tt][v] = 0.0;
     const GT *G = static_cast<const GT *>(r.G) + (size_t)k0 * E + cg * 4;
     // 16 gate rows in flight per thread (raw, converted on use): this role
-    // runs next to the expert GEMMs' full-bandwidth weight stream, so every
-    // load sees the loaded memory latency (in-flight bytes / bandwidth)
+    // runs next to the expert GEMMs' weight stream, so every load sees the
+    // loaded memory latency (in-flight bytes / bandwidth)
     using Raw = typename Vec<GT>::Raw;
     constexpr int RB = sizeof(Raw) <= 8 ? 16 : 8;
-    for (int i0 = 0; i0 < kn; i0 += RB) {
+    for (int n0 = 0; n0 < nrows; n0 += RB) {
         Raw raw[RB];
 #pragma unroll
-        for (int b = 0; b < RB; ++b) raw[b] = Vec<GT>::ld(G + (size_t)min(i0 + b, kn - 1) * E);
+        for (int b = 0; b < RB; ++b)
+            raw[b] = Vec<GT>::ld(G + (size_t)(rstart + min(n0 + b, nrows - 1) * rstep) * E);
 #pragma unroll
         for (int b = 0; b < RB; ++b) {
-            if (i0 + b < kn) {
+            if (n0 + b < nrows) {
+                const int i = rstart + (n0 + b) * rstep;
                 double g[4];
                 float a[4];
                 Vec<GT>::cvt(raw[b], g, a);
@@ -198,61 +213,135 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs) 
                 for (int v = 0; v < 4; ++v) cm[v] = fmaxf(cm[v], a[v]);
 #pragma unroll
                 for (int tt = 0; tt < NJ; ++tt) {
-                    const double xv = xs[(tg * NJ + tt) * kn + i0 + b];
+                    const double xv = xs[(tbase + tt) * kn + i];
 #pragma unroll
                     for (int v = 0; v < 4; ++v) acc[tt][v] = fma(xv, g[v], acc[tt][v]);  // exact product, one rounding
                 }
             }
         }
     }
+    if (!rowsplit) {
 #pragma unroll
-    for (int tt = 0; tt < NJ; ++tt) {
-        const int t = tg * NJ + tt;
-        if (t < ntok)
+        for (int tt = 0; tt < NJ; ++tt) {
+            const int t = tbase + tt;
+            if (t < ntok)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) r.plogit[((size_t)split * T + t0 + t) * E + cg * 4 + v] = acc[tt][v];
+                for (int v = 0; v < 4; ++v) r.plogit[((size_t)split * T + t0 + t) * E + cg * 4 + v] = acc[tt][v];
+        }
+        if (tg == 0)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) r.pcmax[((size_t)tile * r.splits + split) * E + cg * 4 + v] = cm[v];
+    } else {
+        // [TG][NJ][E] partial sums and [TG][E] column maxima after the x slice
+        double *red = reinterpret_cast<double *>(xs + ((tslots * kn + 1) & ~1));
+        float *cmr = reinterpret_cast<float *>(red + TG * NJ * E);
+#pragma unroll
+        for (int tt = 0; tt < NJ; ++tt)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) red[(tg * NJ + tt) * E + cg * 4 + v] = acc[tt][v];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) cmr[tg * E + cg * 4 + v] = cm[v];
+        router_sync();
+        for (int q = rt; q < ntok * E; q += kRouterThreads) {
+            const int tt = q / E, j = q - tt * E;
+            double sum = 0.0;
+#pragma unroll
+            for (int g = 0; g < TG; ++g) sum += red[(g * NJ + tt) * E + j];  // fixed order: deterministic
+            r.plogit[((size_t)split * T + t0 + tt) * E + j] = sum;
+        }
+        for (int j = rt; j < E; j += kRouterThreads) {
+            float m = 0.f;
+#pragma unroll
+            for (int g = 0; g < TG; ++g) m = fmaxf(m, cmr[g * E + j]);
+            r.pcmax[((size_t)tile * r.splits + split) * E + j] = m;
+        }
     }
-    if (tg == 0)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) r.pcmax[((size_t)tile * r.splits + split) * E + cg * 4 + v] = cm[v];
     router_sync();  // the x slice is rewritten by the next unit
 }
 
+// Sum the K-split partials of a tile's tokens (all 64 threads, loads of two
+// (token, expert) entries = up to 64 partials in flight per thread, summed in
+// split order) into shared memory: lgs[t][j] (fp64 logit), cms[t][j] (column
+// max |G|), sxs[t] (sum |x|).  The per-token selection then works from
+// shared memory, so the tile costs one or two dependent load rounds rather
+// than one per 32 experts per token.
+struct TileSums {
+    double *lgs;  // [ntok][E]
+    float *cms;   // [ntok][E]
+    double *sxs;  // [kRouterTok]
+};
+__device__ __forceinline__ TileSums tile_sums_layout(float *xs, int E) {
+    TileSums ts;
+    ts.sxs = reinterpret_cast<double *>(xs);
+    ts.lgs = ts.sxs + kRouterTok;
+    ts.cms = reinterpret_cast<float *>(ts.lgs + kRouterTok * E);
+    return ts;
+}
+static __device__ __noinline__ void router_reduce_tile(const FusedRoute &r, int tile, int t0, int ntok, int rt, const TileSums &ts) {
+    const int E = r.E, T = r.T, S = r.splits;
+    const int lane = rt & 31, w = rt >> 5;
+    for (int t = w; t < ntok; t += kRouterWarps) {
+        double sx = 0.0;
+        for (int z = lane; z < S; z += 32) sx += __ldcg(r.pxsum + (size_t)z * T + t0 + t);
+        sx = warp_sumd(sx);
+        if (lane == 0) ts.sxs[t] = sx;
+    }
+    const int n = ntok * E;
+    for (int q0 = rt; q0 < n; q0 += 2 * kRouterThreads) {
+        double pl[2][16];
+        float pc[2][16];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = q0 + h * kRouterThreads;
+            const int t = q / E, j = q - t * E;
+#pragma unroll
+            for (int z = 0; z < 16; ++z) {
+                const bool ok = q < n && z < S;
+                pl[h][z] = ok ? __ldcg(r.plogit + ((size_t)z * T + t0 + t) * E + j) : 0.0;
+                pc[h][z] = ok ? __ldcg(r.pcmax + ((size_t)tile * S + z) * E + j) : 0.f;
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = q0 + h * kRouterThreads;
+            if (q >= n) continue;
+            double sum = 0.0;
+            float cm = 0.f;
+#pragma unroll
+            for (int z = 0; z < 16; ++z)  // split order: deterministic
+                if (z < S) {
+                    sum += pl[h][z];
+                    cm = fmaxf(cm, pc[h][z]);
+                }
+            for (int z = 16; z < S; ++z) {  // S > 16 (not produced by fused_route_splits)
+                sum += __ldcg(r.plogit + ((size_t)z * T + t0 + q / E) * E + (q % E));
+                cm = fmaxf(cm, __ldcg(r.pcmax + ((size_t)tile * S + z) * E + (q % E)));
+            }
+            ts.lgs[q] = sum;
+            ts.cms[q] = cm;
+        }
+    }
+    router_sync();
+}
+
 // One token's certified selection + softmax, by one warp (select_tile's
-// per-token logic with the E logits in registers, NJ per lane).
+// per-token logic with the E logits in registers, NJ per lane).  `t`: the
+// token's index in the tile (shared sums), `tok`: its global index.
 template <typename GT, int NJ>
-__device__ void router_select_token(const FusedRoute &r, int tile, int tok, int lane) {
-    const int E = r.E, T = r.T, S = r.splits, k = r.k, d = r.d;
+__device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int t, int tok, int lane,
+                                    int *s_ids, float *s_w) {
+    const int E = r.E, k = r.k, d = r.d;
     const double u = 1.1102230246251565e-16;  // 2^-53
     const double gam = (double)d * u / (1.0 - (double)d * u);
     const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
     const double bpad = 1e-300;
-    double sx = 0.0;
-    for (int z = lane; z < S; z += 32) sx += __ldcg(r.pxsum + (size_t)z * T + tok);
-    sx = warp_sumd(sx) * (1.0 + 2.0 * gam);
+    const double sx = ts.sxs[t] * (1.0 + 2.0 * gam);
     double lg[NJ], bd[NJ];
 #pragma unroll
     for (int jj = 0; jj < NJ; ++jj) {
         const int j = lane + 32 * jj;
-        double sum = 0.0;
-        float cm = 0.f;
-        for (int z0 = 0; z0 < S; z0 += 16) {  // all splits' partials in flight, then summed in split order
-            double pl[16];
-            float pc[16];
-#pragma unroll
-            for (int z = 0; z < 16; ++z) {
-                pl[z] = z0 + z < S ? __ldcg(r.plogit + ((size_t)(z0 + z) * T + tok) * E + j) : 0.0;
-                pc[z] = z0 + z < S ? __ldcg(r.pcmax + ((size_t)tile * S + z0 + z) * E + j) : 0.f;
-            }
-#pragma unroll
-            for (int z = 0; z < 16; ++z)
-                if (z0 + z < S) {
-                    sum += pl[z];
-                    cm = fmaxf(cm, pc[z]);
-                }
-        }
-        lg[jj] = sum;
-        bd[jj] = bscale * sx * (double)cm + bpad;
+        lg[jj] = ts.lgs[t * E + j];
+        bd[jj] = bscale * sx * (double)ts.cms[t * E + j] + bpad;
     }
     auto pick = [&](const double (&a)[NJ], int bi) -> double {  // a[bi >> 5] of lane bi & 31
         double mine = 0.0;
@@ -270,6 +359,8 @@ __device__ void router_select_token(const FusedRoute &r, int tile, int tok, int 
         for (int s = lane; s < k; s += 32) {
             r.out.ids[(size_t)tok * k + s] = 0;
             r.out.w[(size_t)tok * k + s] = 0.f;
+            s_ids[t * k + s] = 0;
+            s_w[t * k + s] = 0.f;
         }
         return;
     }
@@ -337,13 +428,16 @@ __device__ void router_select_token(const FusedRoute &r, int tile, int tok, int 
             if (!(pr > 0.0)) atomicCAS(r.out.status, 0, (int)PGMOE_E_GATE_UNDERFLOW);
             r.out.ids[(size_t)tok * k + s] = sel[s];
             r.out.w[(size_t)tok * k + s] = __double2float_rn(pr);
+            s_ids[t * k + s] = sel[s];
+            s_w[t * k + s] = __double2float_rn(pr);
         }
     }
 }
 
 // Histogram, exclusive scan, stable permutation, active list (permute_all
 // of route.cu with the router's two warps).  sm: >= 3 * E ints.
-static __device__ __noinline__ void router_permute(const FusedRoute &r, int rt, int *sm) {
+static __device__ __noinline__ void router_permute(const FusedRoute &r, int rt, int *sm, const int *ids_src,
+                                                   const float *w_src) {
     const int E = r.E, k = r.k, lane = rt & 31, w = rt >> 5;
     const int N = r.T * k;
     int *whist = sm;                        // [kRouterWarps][E] -> cursors
@@ -352,7 +446,7 @@ static __device__ __noinline__ void router_permute(const FusedRoute &r, int rt, 
     router_sync();
     const int seg = (N + kRouterWarps - 1) / kRouterWarps;
     const int r0 = w * seg, r1 = min(N, r0 + seg);
-    for (int i = r0 + lane; i < r1; i += 32) atomicAdd(&whist[w * E + __ldcg(r.out.ids + i)], 1);
+    for (int i = r0 + lane; i < r1; i += 32) atomicAdd(&whist[w * E + ids_src[i]], 1);
     router_sync();
     for (int e = rt; e < E; e += kRouterThreads) {
         int s = 0;
@@ -403,13 +497,13 @@ static __device__ __noinline__ void router_permute(const FusedRoute &r, int rt, 
         const bool valid = i < r1;
         const unsigned vm = __ballot_sync(0xffffffffu, valid);
         if (valid) {
-            const int e = __ldcg(r.out.ids + i);
+            const int e = ids_src[i];
             const unsigned grp = __match_any_sync(vm, e);
             const int rank = __popc(grp & ltmask);
             const int pos = whist[w * E + e] + rank;
             r.out.perm[pos] = i;
             if (r.out.inv) r.out.inv[i] = pos;
-            r.out.w_perm[pos] = __ldcg(r.out.w + i);
+            r.out.w_perm[pos] = w_src[i];
             __syncwarp(vm);
             if (rank == __popc(grp) - 1) whist[w * E + e] += __popc(grp);
         }
@@ -434,23 +528,39 @@ __device__ void router_role(const FusedRoute &r, int rt, float *xs, int *s_flag,
         __threadfence();
         const int t0 = tile * kRouterTok, ntok = min(kRouterTok, r.T - t0);
         if (rt == 0) probe(pr, blockIdx.x, 27);  // tile select start
-        for (int t = w; t < ntok; t += kRouterWarps) router_select_token<GT, NJ>(r, tile, t0 + t, lane);
+        const TileSums ts = tile_sums_layout(xs, r.E);
+        // the tile's ids / weights also stay in shared memory (the end of the
+        // scratch, clear of the sums and of the permutation's histograms)
+        int *s_ids = reinterpret_cast<int *>(xs + kRouterSmemFloats - 2 * kRouterTok * 8);
+        float *s_w = xs + kRouterSmemFloats - kRouterTok * 8;
+        // token chunks whose sums fit the scratch (E=256: 4 tokens at a time)
+        constexpr int kChunk = (kRouterSmemFloats - 2 * kRouterTok * 8 - 2 * kRouterTok) / (NJ * 32 * 3);
+        constexpr int CH = kChunk < kRouterTok ? kChunk : kRouterTok;
+        static_assert(CH >= 1, "routing scratch too small");
+        for (int c0 = 0; c0 < ntok; c0 += CH) {
+            const int nc = min(CH, ntok - c0);
+            router_reduce_tile(r, tile, t0 + c0, nc, rt, ts);
+            for (int t = w; t < nc; t += kRouterWarps)
+                router_select_token<GT, NJ>(r, ts, t, t0 + c0 + t, lane, s_ids + c0 * r.k, s_w + c0 * r.k);
+            router_sync();  // the sums are rewritten by the next chunk
+        }
         __threadfence();
         router_sync();
         if (rt == 0) probe(pr, blockIdx.x, 28);  // tile selected
+        const bool single = r.tiles == 1;  // this CTA holds every token's decision: no global ticket
         if (rt == 0) {
             r.tile_counter[tile] = 0;
-            *s_flag = (atomicAdd(r.counter, 1) == r.tiles - 1);
+            *s_flag = single ? 1 : (atomicAdd(r.counter, 1) == r.tiles - 1);
         }
         router_sync();
         if (!*s_flag) continue;
-        __threadfence();
-        router_permute(r, rt, reinterpret_cast<int *>(xs));
+        if (!single) __threadfence();
+        router_permute(r, rt, reinterpret_cast<int *>(xs), single ? s_ids : r.out.ids, single ? s_w : r.out.w);
         __threadfence();
         router_sync();
         if (rt == 0) probe(pr, blockIdx.x, 29);  // permutation written
         if (rt == 0) {
-            *r.counter = 0;
+            if (!single) *r.counter = 0;
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(r.done), "r"(1) : "memory");
         }
     }
