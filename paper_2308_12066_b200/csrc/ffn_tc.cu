@@ -88,6 +88,14 @@ struct Params {
     unsigned long long *probe;  // debug stamps [grid][kProbeSlots] or null
     FusedRoute route;           // the next block's routing, computed by warps 7-8 (resident)
     int max_inflight;           // weight stages the producer keeps in flight (<= STAGES)
+    // Chained launches (resident decoder): instead of waiting for the previous
+    // launch to COMPLETE (griddepcontrol.wait, ~4-6 us after its last CTA),
+    // phase 0 and the routing role wait for its dense phase to be written:
+    // *epoch >= epoch_wait.  This launch sets *epoch = epoch_set once its own
+    // dense phase is complete.  Counters / partials alternate between two
+    // parity buffers, so a launch never touches what its predecessor re-arms.
+    int *epoch;                 // null: not chained
+    int epoch_wait, epoch_set;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -572,6 +580,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             // in flight as the bandwidth needs.
             const int lim = max(1, min(p.max_inflight, STAGES));
             long long kbi = 0;  // weight k-blocks issued by this CTA
+            // chained: the unit counter lives in this launch's parity buffer,
+            // re-armed two launches ago, so units are fetched without waiting
+            const bool chained = p.epoch != nullptr;
+            if (chained) pdl_done = true;
             long long u = blockIdx.x;
             while (u < total_units) {
                 const Unit x = decode_unit<BN>(ps, p.nphase, gr, u);
@@ -609,7 +621,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                 u = (long long)gridDim.x + nxt;
                 ++n_units;
             }
-            if (!pdl_done) {  // no work here: still honour PDL before exiting
+            if (!pdl_done || (chained && !p.route.active)) {  // still honour PDL before exiting
                 pdl_wait();
                 if (!p.route.active) pdl_trigger();
             }
@@ -634,7 +646,13 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             int stage = 0, qi = 0;
             uint32_t phase = 0, qphase = 0;
             long long cyc_gate = 0;
-            pdl_wait();  // the activations of phase 0 come from the previous kernel
+            // the activations of phase 0 come from the previous launch
+            if (p.epoch) {
+                while (ld_acquire(p.epoch) < p.epoch_wait) __nanosleep(32);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            } else {
+                pdl_wait();
+            }
             int open_group = -1, open_phase = 0;
             for (;;) {
                 mbar_wait(&uq_full[qi], qphase);
@@ -681,11 +699,22 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         // with this block's expert GEMMs; once it is complete the next launch
         // (which schedules from it) may start.
         if (p.route.active) {
-            pdl_wait();  // the block input comes from the previous kernel
-            if (tid == 7 * 32) probe(p.probe, blockIdx.x, 25);  // routing role past PDL
+            if (p.epoch) {  // the block input is the previous launch's dense output
+                if (tid == 7 * 32)
+                    while (ld_acquire(p.epoch) < p.epoch_wait) __nanosleep(32);
+                router_sync();
+            } else {
+                pdl_wait();
+            }
+            if (tid == 7 * 32) probe(p.probe, blockIdx.x, 25);  // routing role past its gate
             router_run(p.route, tid - 7 * 32, r_xs, &r_flag, p.probe);
             if (tid == 7 * 32) {
                 while (ld_acquire(p.route.done) == 0) __nanosleep(64);
+                // the next launch may start once it can schedule from this
+                // routing — and (chained: parity buffers) once the previous
+                // launch has completed, so that launch k+2 never meets launch
+                // k's re-arm
+                pdl_wait();
                 pdl_trigger();
                 probe(p.probe, blockIdx.x, 30);  // dependents triggered
             }
@@ -734,15 +763,22 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         uint32_t qphase = 0;
         // The previous launch's last CTA re-arms the counters on its way out;
         // with programmatic dependent launch this grid may already be running,
-        // so no signal may precede griddepcontrol.wait.
-        pdl_wait();
+        // so no signal may precede griddepcontrol.wait (chained launches use
+        // the other parity's counters instead).
+        if (!p.epoch) pdl_wait();
         auto signal_upto = [&](int ph_end) {
             for (; signalled < ph_end; ++signalled) {
                 __threadfence();
                 named_sync(1, 128);
                 if (et == 0) {
                     probe(p.probe, blockIdx.x, 6 + signalled);  // this CTA's phase done
-                    atomicAdd(phase_done + signalled, 1);
+                    const int old = atomicAdd(phase_done + signalled, 1);
+                    if (p.epoch && signalled == p.nphase - 1 && old == (int)gridDim.x - 1) {
+                        // every CTA's last-phase rows are written: release the next launch
+                        __threadfence();
+                        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.epoch), "r"(p.epoch_set)
+                                     : "memory");
+                    }
                 }
             }
         };
@@ -985,13 +1021,15 @@ static int launch(const PhaseMaps *mp, const Params &p, cudaStream_t s) {
 // BN: widest N tile.  Token groups wider than BN are split into N tiles
 // (each re-reads its weight tile), so BN follows the expected tokens per
 // group: 64 covers decode batches, 256 the compute-bound stress shapes.
-static int run(const PhaseMaps *mp, Params p, int bn, void *ws, size_t ws_bytes, cudaStream_t s) {
+// Workspace: [parity 0: tickets | sync][parity 1: tickets | sync][partials 0][partials 1]
+static int run(const PhaseMaps *mp, Params p, int bn, void *ws, size_t ws_bytes, cudaStream_t s, int parity = 0) {
     const size_t head = (size_t)(kCounterInts + kSyncInts) * 4;
-    PG_REQUIRE(ws_bytes > head + 4096, PGMOE_E_CONFIG, "tcgen05 workspace too small");
-    p.counters = static_cast<int *>(ws);
+    PG_REQUIRE(ws_bytes > 2 * head + 8192, PGMOE_E_CONFIG, "tcgen05 workspace too small");
+    const size_t half = ((ws_bytes - 2 * head) / 2) & ~(size_t)255;
+    p.counters = reinterpret_cast<int *>(static_cast<char *>(ws) + (size_t)parity * head);
     p.sync = p.counters + kCounterInts;
-    p.partial = reinterpret_cast<float *>(static_cast<char *>(ws) + head);
-    p.partial_cap = (long long)((ws_bytes - head) / 4);
+    p.partial = reinterpret_cast<float *>(static_cast<char *>(ws) + 2 * head + (size_t)parity * half);
+    p.partial_cap = (long long)(half / 4);
     p.probe = probe_buffer(1, kNumSMs);
     if (p.max_inflight <= 0) p.max_inflight = 8;
     { const char *e = getenv("PGMOE_INFLIGHT"); if (e) p.max_inflight = atoi(e); }
@@ -1022,7 +1060,7 @@ int tc_pack_rows(const float *x, const int *perm, int n, int d, int k, uint16_t 
 int block_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
              const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, bool xb_ready,
              const void *dense_w, float *y, uint16_t *next_xb, const int *next_inv, void *ws, size_t ws_bytes,
-             cudaStream_t s, const FusedRoute *route) {
+             cudaStream_t s, const FusedRoute *route, const LaunchChain *chain) {
     PG_REQUIRE(tc_supported(d, f), PGMOE_E_CONFIG, "tcgen05 path needs d, f multiples of 128 and f >= d");
     PG_REQUIRE((reinterpret_cast<uintptr_t>(experts) & 15) == 0 && stride % 16 == 0, PGMOE_E_CONFIG,
                "expert records must be 16-byte aligned");
@@ -1064,7 +1102,15 @@ int block_tc(const float *x, int T, int d, int f, int k, const void *experts, si
         // (tools/gpu_inflight_sweep.sh: Base-64 T=256 -8%; Large-128 needs 8).
         if (route->E <= 64 && n >= 64 && (size_t)d * f <= (size_t)768 * 3072) p.max_inflight = 4;
     }
-    return tc::run(mp, p, (n >= 2048) ? 256 : 64, ws, ws_bytes, s);
+    int parity = 0;
+    if (chain && chain->epoch) {
+        PG_REQUIRE(dense_w != nullptr, PGMOE_E_CONFIG, "chained launches end with the dense phase");
+        p.epoch = chain->epoch;
+        p.epoch_wait = chain->epoch_wait;
+        p.epoch_set = chain->epoch_set;
+        parity = chain->parity & 1;
+    }
+    return tc::run(mp, p, (n >= 2048) ? 256 : 64, ws, ws_bytes, s, parity);
 }
 
 int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,

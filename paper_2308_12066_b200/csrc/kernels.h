@@ -29,10 +29,17 @@ int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *exper
 // One launch for up + down (+ the dense layer when dense_w != nullptr and
 // top_k == 1), phases separated by in-kernel grid barriers.
 struct FusedRoute;
+// Chained resident launches (see tc::Params::epoch).
+struct LaunchChain {
+    int *epoch;       // device counter, zeroed at the start of each decoder iteration
+    int epoch_wait;   // 0: wait for the previous launch to complete (PDL)
+    int epoch_set;
+    int parity;       // alternates between consecutive block launches
+};
 int block_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
              const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, bool xb_ready,
              const void *dense_w, float *y, uint16_t *next_xb, const int *next_inv, void *ws, size_t ws_bytes,
-             cudaStream_t s, const FusedRoute *route = nullptr);
+             cudaStream_t s, const FusedRoute *route = nullptr, const LaunchChain *chain = nullptr);
 // next_xb / next_inv (optional): scatter y as the next block's packed bf16
 // up-projection operand (the next block's routing is already known).
 int dense_tc2(const float *yw, const uint16_t *mixb_ready, int T, int d, int k, const void *dense_w, float *y,

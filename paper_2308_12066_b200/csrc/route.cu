@@ -306,7 +306,9 @@ route_kernel(const RouteParams p_in) {
     const int cta = split * gridDim.x + tile;
     if (tid == 0) probe(p.probe, cta, 0);
     pdl_wait();  // x is produced by the previous kernel in the stream
-    pdl_trigger();
+    // No early trigger: the next launch (a block launch) reads this routing in
+    // its prologue, so dependents start only when every CTA has exited or —
+    // the permuting CTA — triggered after its last write.
     if (tid == 0) probe(p.probe, cta, 1);
     for (int i = tid; i < TOK * kn; i += kLogitThreads) {
         const int t = i / kn;
@@ -421,6 +423,9 @@ route_kernel(const RouteParams p_in) {
         *p.counter = 0;
         probe(p.probe, cta, 6);  // permute done
     }
+    __threadfence();
+    __syncthreads();
+    pdl_trigger();
 }
 
 static int pick_tok(int T) {

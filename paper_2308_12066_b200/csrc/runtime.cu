@@ -131,6 +131,12 @@ struct pgmoe_model {
     int64_t fused_blocks = 0;  // blocks whose dense layer ran inside the expert launch
     int64_t fused_routes = 0;  // pre-gates computed inside the block launch
     bool fuse_route = true;    // resident: route inside the block launch (pgmoe_model_set_fused_route)
+    // fused: launches chained on the previous dense phase instead of its
+    // completion (PGMOE_CHAIN=1).  Measured: saves the ~4.5 us completion
+    // latency but pays ~3-4 us of atomic + fence + poll, net -1 % at T=256
+    // and +2 % at T=1 (tools/gpu_ab_chain.sh), so off by default.
+    bool chain_launches = false;
+    int *epoch = nullptr;        // device counter of chained launches
     // host-buffer entry point
     cudaStream_t io_stream = nullptr;
     float *io_x = nullptr, *io_y = nullptr, *io_w = nullptr;
@@ -363,7 +369,8 @@ static int route_into(pgmoe_model *m, const float *x, int T, const void *G, int 
 // The pre-gate of block b, computed inside block b's tcgen05 launch (route
 // workspace layout: counter @0, done flag @64, tile counters @256, partials
 // after kFusedRouteHead).
-static FusedRoute fused_route_args(pgmoe_model *m, const float *x, int T, const void *G, const pgmoe_routing &out) {
+static FusedRoute fused_route_args(pgmoe_model *m, const float *x, int T, const void *G, const pgmoe_routing &out,
+                                   int parity) {
     const auto &c = m->cfg;
     FusedRoute r{};
     r.active = 1;
@@ -379,7 +386,7 @@ static FusedRoute fused_route_args(pgmoe_model *m, const float *x, int T, const 
     r.out = out;
     char *ws = static_cast<char *>(m->route_ws);
     r.counter = reinterpret_cast<int *>(ws);
-    r.done = reinterpret_cast<int *>(ws + 64);
+    r.done = reinterpret_cast<int *>(ws + 64 + 4 * (parity & 1));  // re-armed at its launch's exit
     r.tile_counter = reinterpret_cast<int *>(ws + 256);
     char *q = ws + kFusedRouteHead;
     r.plogit = reinterpret_cast<double *>(q);
@@ -423,6 +430,11 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
     const bool fuse_route = !off && use_tc(m) && c.top_k == 1 && L == 1 && m->fuse_route &&
                             fused_route_supported(c.num_experts) && T <= (1 << 16);
     const float *cur = x_in;
+    // Chained block launches (fused routing): each launch waits for its
+    // predecessor's dense phase through a device counter instead of for its
+    // completion; the counter restarts every iteration.
+    const bool chain = fuse_route && m->chain_launches;
+    if (chain) PG_CUDA(cudaMemsetAsync(m->epoch, 0, sizeof(int), s));
     for (int b = 0; b < nb; ++b) {
         const BlockW &bw = m->blocks[b];
         const int ri = b % R;
@@ -439,7 +451,7 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
         if (has_pre_gate(c, b)) {
             const int tr = (b + L) % R;
             if (fuse_route) {
-                fr = fused_route_args(m, cur, T, bw.pre_gate, m->routing[tr].r);
+                fr = fused_route_args(m, cur, T, bw.pre_gate, m->routing[tr].r, b & 1);
             } else {
                 PG_TRY(route_into(m, cur, T, bw.pre_gate, tr, off && !prefetch_all, s, "pre_gate", b));
             }
@@ -461,12 +473,14 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
         const bool fuse_next = use_tc(m) && b + 1 < nb && !has_conv_gate(c, b + 1);
         const pgmoe_routing *next_r = fuse_next ? &m->routing[(b + 1) % R].r : nullptr;
         const int indexed = (off && !prefetch_all) ? 1 : 0;
+        LaunchChain lc{m->epoch, b > 0 ? b : 0, b + 1, b & 1};
         if (use_tc(m) && c.top_k == 1) {
             // one launch: up, down(+combine), dense — phases behind grid barriers
             tl_begin(m, "compute", "experts", b, s);
             PG_TRY(block_tc(cur, T, c.d_model, c.d_ff, 1, experts, m->rec_bytes, indexed, &rb.r, m->xb, m->hb, m->yw,
                             m->mixb, xb_ready, bw.dense, nxt, next_r ? m->xb : nullptr, next_r ? next_r->inv : nullptr,
-                            m->tc_ws, m->tc_ws_bytes, s, fr.active ? &fr : nullptr));
+                            m->tc_ws, m->tc_ws_bytes, s, fr.active ? &fr : nullptr,
+                            chain ? &lc : nullptr));
             if (fr.active) m->fused_routes++;
             tl_end(m, s);
             if (off) {
@@ -664,6 +678,9 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
     m->tc_ws_bytes = 64ull << 20;
     if (cudaMalloc(&m->tc_ws, m->tc_ws_bytes) != cudaSuccess || cudaMemset(m->tc_ws, 0, m->tc_ws_bytes) != cudaSuccess)
         return fail(PGMOE_E_OOM);
+    if (cudaMalloc(&m->epoch, 256) != cudaSuccess || cudaMemset(m->epoch, 0, 256) != cudaSuccess)
+        return fail(PGMOE_E_OOM);
+    if (const char *e = getenv("PGMOE_CHAIN")) m->chain_launches = (e[0] == '1');
     cudaEventCreate(&m->t0);
     m->stats.pinned_hbm_bytes = (int64_t)pinned;
     m->stats.slot_capacity_bytes = (int64_t)m->slot_capacity;
@@ -704,6 +721,7 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     cudaFree(m->slots);
     cudaFree(m->route_ws);
     cudaFree(m->tc_ws);
+    cudaFree(m->epoch);
     cudaFree(m->act_buf[0]);
     cudaFree(m->act_buf[1]);
     cudaFree(m->h);

@@ -328,6 +328,27 @@ def test_fused_routing_equals_separate_launch_and_offloaded(E, T):
         m.close()
 
 
+def test_chained_block_launches_equal_pdl_chain(monkeypatch):
+    """PGMOE_CHAIN=1: each resident block launch waits for its predecessor's
+    dense phase through a device counter (parity-buffered counters) instead
+    of its completion; outputs and routing must be identical."""
+    dims = og.Dims(256, 512, 6, 128, 1, seed=9)
+    x0 = torch.from_numpy(tokens(256, 48)).cuda()
+    base = _device_model(dims, "bf16", "resident", max_tokens=48)
+    monkeypatch.setenv("PGMOE_CHAIN", "1")
+    chained = _device_model(dims, "bf16", "resident", max_tokens=48)
+    outs = []
+    for m in (base, chained):
+        for _ in range(3):
+            y, ids, w = m.decoder_iteration(x0, trace=True)
+        torch.cuda.synchronize()
+        outs.append((y.clone(), ids.clone(), w.clone()))
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    base.close()
+    chained.close()
+
+
 def test_timeline_schema_and_causality():
     dims = og.Dims(128, 256, 4, 8, 1)
     m = _device_model(dims, "bf16", "offloaded", max_tokens=8)

@@ -15,7 +15,7 @@ for it in range(4):
 b = pb.cpu().numpy()
 t0 = b[148:296, 0][b[148:296, 0] > 0].min()
 rows = b[148:296]
-for c in list(range(0, 16)) + [100, 147]:
+for c in list(range(0, 14)) + [24, 60, 100, 147]:
     r = rows[c]
-    print(c, " ".join(f"{n}={(r[s]-t0)/1e3:.2f}" for s, n in [(0,'entry'),(1,'prolog'),(2,'gate0'),(25,'r_pdl'),(26,'r_log'),(27,'sel0'),(28,'sel1'),(29,'perm'),(30,'trig'),(9,'exit')] if r[s] > 0))
+    print(c, " ".join(f"{n}={(r[s]-t0)/1e3:.2f}" for s, n in [(0,'entry'),(1,'prolog'),(2,'gate0'),(25,'r_pdl'),(26,'r_log'),(27,'sel0'),(23,'sums'),(24,'stored'),(28,'sel1'),(29,'perm'),(30,'trig'),(6,'ph0'),(7,'ph1'),(4,'gate2'),(8,'ph2'),(9,'exit')] if r[s] > 0))
 PY
