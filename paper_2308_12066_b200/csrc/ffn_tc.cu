@@ -190,6 +190,7 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
 
 struct PhaseSched {
     int mode, M, K, m_tiles, kb_total, kbs, S;
+    int nw;               // token columns per tile (BN; narrower for the dense phase)
     int ctr0;             // first split-K ticket of this phase (phases may overlap)
     long long part0;      // first partial-tile float of this phase
     long long tiles, units, unit0;
@@ -221,7 +222,7 @@ __device__ __forceinline__ Unit decode_unit(const PhaseSched *ps, int nphase, co
         x.g = 0;
         const int n_tile = x.tile / sc.m_tiles;
         x.m_tile = x.tile - n_tile * sc.m_tiles;
-        x.n0 = n_tile * BN;
+        x.n0 = n_tile * sc.nw;
         ng = gr.T;
         x.row0 = 0;
         x.rec = 0;
@@ -241,7 +242,7 @@ __device__ __forceinline__ Unit decode_unit(const PhaseSched *ps, int nphase, co
         x.row0 = gr.row0[lo];
         x.rec = gr.rec[lo];
     }
-    x.n_valid = min(BN, ng - x.n0);
+    x.n_valid = min(sc.nw, ng - x.n0);
     x.n_pad = max(16, (x.n_valid + 15) & ~15);
     x.kb0 = x.s * sc.kbs;
     x.kb1 = min(sc.kb_total, x.kb0 + sc.kbs);
@@ -506,10 +507,15 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         sc.kb_total = sc.K / BK;
         int max_npad;
         if (sc.mode == kDense) {
-            sc.tiles = (long long)((p.T + BN - 1) / BN) * sc.m_tiles;
-            max_npad = max(16, (min(p.T, BN) + 15) & ~15);
+            // The dense phase has few tiles (T / BN x d / 128) and a serial
+            // epilogue per tile: 32-token tiles double the CTAs sharing it
+            // (the 1-2 MB weight tile is re-read from L2, not HBM)
+            sc.nw = (BN >= 64 && p.T > 32) ? 32 : BN;
+            sc.tiles = (long long)((p.T + sc.nw - 1) / sc.nw) * sc.m_tiles;
+            max_npad = max(16, (min(p.T, sc.nw) + 15) & ~15);
         } else {
             sc.tiles = (long long)ntiles_expert * sc.m_tiles;
+            sc.nw = BN;
             max_npad = max_npad_expert;
         }
         // Split K only when it pays for its fix-up.  A split-K tile costs one
