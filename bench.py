@@ -206,7 +206,7 @@ def run_ours(args, rank: int, world: int):
     cfg = P.ModelConfig(top_k=1, activation_level=1, seed=0, **pr)
     T = args.tokens
     t_setup = time.perf_counter()
-    model = P.DeviceModel(cfg, dtype="bf16", placement=args.placement, max_tokens=T, kernel=args.kernel)
+    model = P.DeviceModel(cfg, dtype=args.dtype, placement=args.placement, max_tokens=T, kernel=args.kernel)
     setup_s = time.perf_counter() - t_setup
     # each rank owns its own T sequences (weak scaling over sequences)
     x_host = torch.from_numpy(token_batch(0, cfg.d_model, T, offset=rank * T)).pin_memory()
@@ -258,7 +258,7 @@ def run_ours(args, rank: int, world: int):
 
     # ---- per-kernel roofline from the CUDA events on the compute stream ---
     hbm_peak, tc_peak, peak_kind = peaks()
-    sw = 2
+    sw = 2 if args.dtype == "bf16" else 4
     d, f, E, nb = cfg.d_model, cfg.d_ff, cfg.num_experts, cfg.num_blocks
     rec = 2 * d * f * sw
     ffn = [e for e in tl if e["label"] == "experts"]
@@ -325,9 +325,10 @@ def run_ours(args, rank: int, world: int):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "bf16",
+        "dtype": args.dtype,
         "data": "synthetic (reference RNG weights/tokens, SURVEY §8(d))",
-        "config": {"workload": workload_name(args.preset, args.placement, T),
+        "config": {"workload": workload_name(args.preset, args.placement, T) +
+                               (" f32 weights" if args.dtype == "f32" else ""),
                    "preset": args.preset, "placement": args.placement, "tokens_per_rank": T,
                    "global_batch": T * world, "num_blocks": nb, "d_model": d, "d_ff": f, "num_experts": E,
                    "top_k": 1, "activation_level": 1, "parallelism": f"sequences x{world} (replicas)",
@@ -341,7 +342,8 @@ def run_ours(args, rank: int, world: int):
                      (" + next block's K1 routing" if routed_in_launch else "") + (", one launch" if fused else ""),
                      "achieved": round(ffn_gbs, 1) if ffn_gbs else None, "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(ffn_gbs / hbm_peak, 4) if ffn_gbs else None,
-                     "traffic": ncu_traffic("ffn", workload_name(args.preset, args.placement, T)),
+                     "traffic": ncu_traffic("ffn", workload_name(args.preset, args.placement, T) +
+                                            (" f32 weights" if args.dtype == "f32" else "")),
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": round(ffn_bytes / max(1, len(ffn))),
                      "avg_launch_us": round(ffn_s / max(1, len(ffn)) * 1e6, 2)},
@@ -365,7 +367,7 @@ def run_ours(args, rank: int, world: int):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nth = os.cpu_count() or 1
         sample = args.cpu_sample or nth
-        times = cpu_reference_run(args.preset, "bf16", sample, 1, 0, nth)
+        times = cpu_reference_run(args.preset, args.dtype, sample, 1, 0, nth)
         out["cpu_baseline"] = {"value": round(sample / times[0], 4), "unit": "tokens/s", "cores": nth,
                                "kind": "port",
                                "sample": f"{sample} tokens x 1 decoder iteration ({nb} blocks), oracle C "
@@ -488,6 +490,8 @@ def main():
     ap.add_argument("--preset", choices=sorted(PRESETS), default="large128")
     ap.add_argument("--placement", choices=["offloaded", "resident"], default="offloaded")
     ap.add_argument("--kernel", choices=["auto", "simt", "tcgen05"], default="auto")
+    ap.add_argument("--dtype", choices=["bf16", "f32"], default="bf16",
+                    help="weight dtype (f32: BASELINE configs[0]-style fp32 weights on the SIMT kernels)")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", choices=["auto", "single", "ep"], default="auto",
