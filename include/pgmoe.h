@@ -129,6 +129,30 @@ PGMOE_API int pgmoe_unpermute_combine(const float *back, const int32_t *perm, co
 PGMOE_API int pgmoe_ep_local_routing(const int32_t *recv_cnt, int32_t P, int32_t El, const pgmoe_routing *out,
                                      pgmoe_stream_t stream);
 
+/* Fixed-size (padded) expert-parallel exchange: no host round trip for the
+ * all-to-all split sizes.  Rank p owns experts [p*El, (p+1)*El) and gets a
+ * slot of `cap` (>= T*k) rows from every rank.
+ *   pack_send: send[p][i] = bf16(x[perm[r] / k]), r = off[p*El] + i — the
+ *     rows the tcgen05 FFN consumes in bf16, so exact at half the bytes;
+ *   local_routing_padded: receiver routing over the padded rows (source p's
+ *     rows start at p*cap);
+ *   pack_recv: the received rows in local-expert order (the FFN operand),
+ *     count read on the device (off[El]);
+ *   expert_forward_packed: expert FFN on that operand, y rows scattered back
+ *     to their padded receive positions;
+ *   unpermute_padded: yw[perm[r]] = w_perm[r] * back[p][r - off[p*El]]. */
+PGMOE_API int pgmoe_ep_pack_send(const float *x, const pgmoe_routing *r, int32_t T, int32_t d, int32_t k, int32_t P,
+                                 int32_t El, int32_t cap, uint16_t *send, pgmoe_stream_t stream);
+PGMOE_API int pgmoe_ep_local_routing_padded(const int32_t *recv_cnt, int32_t P, int32_t El, int32_t cap,
+                                            const pgmoe_routing *out, pgmoe_stream_t stream);
+PGMOE_API int pgmoe_ep_pack_recv(const uint16_t *recv, const pgmoe_routing *local, int32_t El, int32_t n_max,
+                                 int32_t d, uint16_t *xb, pgmoe_stream_t stream);
+PGMOE_API int pgmoe_expert_forward_packed(const uint16_t *xb, int32_t n_max, int32_t d, int32_t f,
+                                          const void *experts, size_t expert_stride, const pgmoe_routing *r,
+                                          uint16_t *hb, float *y, pgmoe_stream_t stream);
+PGMOE_API int pgmoe_ep_unpermute_padded(const float *back, const pgmoe_routing *r, int32_t T, int32_t d, int32_t k,
+                                        int32_t P, int32_t El, int32_t cap, float *yw, pgmoe_stream_t stream);
+
 /* Reads routing status after a sync: returns the device-detected error (or
  * PGMOE_OK) and optionally the serial-fallback / flip counters. */
 PGMOE_API int pgmoe_check_routing(const pgmoe_routing *r, int32_t *fallbacks, int32_t *flips);

@@ -5,6 +5,8 @@
 //
 // Experts are partitioned contiguously (rank r owns [r*E/P, (r+1)*E/P)), so
 // K1's expert-grouped permutation is already grouped by destination rank.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace pgmoe {
@@ -40,13 +42,17 @@ __global__ void unpermute_kernel(const float *__restrict__ back, const int *__re
 // grouped by local expert ascending.  Regroup by local expert (sources in
 // rank order inside an expert) — the same stable order a single GPU would
 // produce for the concatenated batch.  cnt: [P][El].  One CTA.
-__global__ void ep_local_routing_kernel(const int *__restrict__ cnt, int P, int El, pgmoe_routing r) {
+// src_stride > 0: source p's rows start at row p * src_stride (fixed-size,
+// padded exchange) instead of right after source p-1's.
+__global__ void ep_local_routing_kernel(const int *__restrict__ cnt, int P, int El, int src_stride,
+                                        pgmoe_routing r) {
     extern __shared__ int sm[];
     int *src_base = sm;          // [P] first received row of source p
     int *src_off = sm + P;       // [P][El] offset of expert e inside source p's rows
     if (threadIdx.x == 0) {
         int run = 0;
         for (int p = 0; p < P; ++p) {
+            if (src_stride > 0) run = p * src_stride;
             src_base[p] = run;
             int o = 0;
             for (int e = 0; e < El; ++e) {
@@ -78,17 +84,134 @@ __global__ void ep_local_routing_kernel(const int *__restrict__ cnt, int P, int 
             for (int i = lane; i < c; i += 32) {
                 r.perm[pos + i] = base + i;
                 r.w_perm[pos + i] = 1.0f;
-                r.ids[base + i] = e;
-                r.w[base + i] = 1.0f;
+                if (r.ids) r.ids[base + i] = e;
+                if (r.w) r.w[base + i] = 1.0f;
             }
             pos += c;
         }
     }
 }
 
+// ---- fixed-size (padded) exchange: no host round trip for split sizes ----
+// Rank p owns experts [p*El, (p+1)*El), so K1's expert-grouped permutation
+// sends a contiguous run of routing positions to each peer: positions
+// [off[p*El], off[(p+1)*El]).  Each peer gets a fixed slot of `cap` rows.
+
+__device__ __forceinline__ int owner_of(const int *off, int El, int P, int r) {
+    int p = 0;
+    while (p + 1 < P && __ldg(off + (p + 1) * El) <= r) ++p;
+    return p;
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) |
+           ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
+}
+
+// send[p][i] = bf16(x[perm[r] / k]) for r = off[p*El] + i (the rows the
+// FFN consumes in bf16 anyway, so the exchange is exact and half the bytes)
+__global__ void ep_pack_send_kernel(const float *__restrict__ x, const int *__restrict__ perm,
+                                    const int *__restrict__ off, int n, int d, int k, int P, int El, int cap,
+                                    uint16_t *__restrict__ send) {
+    const int vec = d / 8;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * vec;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / vec), c = (int)(i - (long long)r * vec);
+        const int p = owner_of(off, El, P, r);
+        const int slot = r - __ldg(off + p * El);
+        const float4 *src = reinterpret_cast<const float4 *>(x + (size_t)(__ldg(perm + r) / k) * d) + 2 * c;
+        const float4 a = __ldg(src), b = __ldg(src + 1);
+        uint4 o;
+        o.x = pack_bf16x2(a.x, a.y);
+        o.y = pack_bf16x2(a.z, a.w);
+        o.z = pack_bf16x2(b.x, b.y);
+        o.w = pack_bf16x2(b.z, b.w);
+        reinterpret_cast<uint4 *>(send)[((size_t)p * cap + slot) * vec + c] = o;
+    }
+}
+
+// xb[pos] = recv[perm[pos]] for pos < off[El] (device count): the received
+// bf16 rows in local-expert order, the tcgen05 FFN's packed operand
+__global__ void ep_pack_recv_kernel(const uint16_t *__restrict__ recv, const int *__restrict__ perm,
+                                    const int *__restrict__ off_end, int n_max, int d, uint16_t *__restrict__ xb) {
+    const int vec = d / 8;
+    const int n = min(n_max, __ldg(off_end));
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * vec;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / vec), c = (int)(i - (long long)r * vec);
+        reinterpret_cast<uint4 *>(xb)[(size_t)r * vec + c] =
+            __ldg(reinterpret_cast<const uint4 *>(recv) + (size_t)__ldg(perm + r) * vec + c);
+    }
+}
+
+// yw[perm[r]] = w_perm[r] * back[p][r - off[p*El]] (the combine weight)
+__global__ void ep_unpermute_padded_kernel(const float *__restrict__ back, const int *__restrict__ perm,
+                                           const float *__restrict__ w_perm, const int *__restrict__ off, int n,
+                                           int d, int P, int El, int cap, float *__restrict__ yw) {
+    const int vec = d / 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * vec;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / vec), c = (int)(i - (long long)r * vec);
+        const int p = owner_of(off, El, P, r);
+        const size_t row = (size_t)p * cap + (r - __ldg(off + p * El));
+        const float w = __ldg(w_perm + r);
+        float4 v = __ldg(reinterpret_cast<const float4 *>(back) + row * vec + c);
+        v.x *= w; v.y *= w; v.z *= w; v.w *= w;
+        reinterpret_cast<float4 *>(yw)[(size_t)__ldg(perm + r) * vec + c] = v;
+    }
+}
+
+static int grid_for(long long work) { return (int)std::min<long long>(kNumSMs * 8, std::max(1LL, (work + 255) / 256)); }
+
 }  // namespace pgmoe
 
 using namespace pgmoe;
+
+extern "C" int pgmoe_ep_pack_send(const float *x, const pgmoe_routing *r, int32_t T, int32_t d, int32_t k, int32_t P,
+                                  int32_t El, int32_t cap, uint16_t *send, pgmoe_stream_t stream) {
+    PG_REQUIRE(d % 8 == 0, PGMOE_E_SHAPE, "ep_pack_send needs d %% 8 == 0");
+    PG_REQUIRE(cap >= T * k, PGMOE_E_CONFIG, "ep slot of %d rows cannot hold %d routed entries", cap, T * k);
+    const int n = T * k;
+    if (n == 0) return PGMOE_OK;
+    ep_pack_send_kernel<<<grid_for((long long)n * d / 8), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        x, r->perm, r->off, n, d, k, P, El, cap, send);
+    PG_CUDA(cudaGetLastError());
+    count_launch();
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_ep_pack_recv(const uint16_t *recv, const pgmoe_routing *local, int32_t El, int32_t n_max,
+                                  int32_t d, uint16_t *xb, pgmoe_stream_t stream) {
+    PG_REQUIRE(d % 8 == 0, PGMOE_E_SHAPE, "ep_pack_recv needs d %% 8 == 0");
+    if (n_max == 0) return PGMOE_OK;
+    ep_pack_recv_kernel<<<grid_for((long long)n_max * d / 8), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        recv, local->perm, local->off + El, n_max, d, xb);
+    PG_CUDA(cudaGetLastError());
+    count_launch();
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_ep_unpermute_padded(const float *back, const pgmoe_routing *r, int32_t T, int32_t d, int32_t k,
+                                         int32_t P, int32_t El, int32_t cap, float *yw, pgmoe_stream_t stream) {
+    PG_REQUIRE(d % 4 == 0, PGMOE_E_SHAPE, "ep_unpermute needs d %% 4 == 0");
+    const int n = T * k;
+    if (n == 0) return PGMOE_OK;
+    ep_unpermute_padded_kernel<<<grid_for((long long)n * d / 4), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        back, r->perm, r->w_perm, r->off, n, d, P, El, cap, yw);
+    PG_CUDA(cudaGetLastError());
+    count_launch();
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_ep_local_routing_padded(const int32_t *recv_cnt, int32_t P, int32_t El, int32_t cap,
+                                             const pgmoe_routing *out, pgmoe_stream_t stream) {
+    PG_REQUIRE(P >= 1 && El >= 1 && cap >= 1, PGMOE_E_CONFIG, "bad EP shape P=%d El=%d cap=%d", P, El, cap);
+    const size_t smem = (size_t)(P + P * El) * 4;
+    PG_REQUIRE(smem <= 48 * 1024, PGMOE_E_CONFIG, "EP routing table too large");
+    ep_local_routing_kernel<<<1, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(recv_cnt, P, El, cap, *out);
+    PG_CUDA(cudaGetLastError());
+    count_launch();
+    return PGMOE_OK;
+}
 
 extern "C" int pgmoe_gather_rows(const float *src, const int32_t *perm, int32_t n, int32_t d, int32_t k,
                                  float *out, pgmoe_stream_t stream) {
@@ -119,7 +242,7 @@ extern "C" int pgmoe_ep_local_routing(const int32_t *recv_cnt, int32_t P, int32_
     PG_REQUIRE(P >= 1 && El >= 1, PGMOE_E_CONFIG, "bad EP shape P=%d El=%d", P, El);
     const size_t smem = (size_t)(P + P * El) * 4;
     PG_REQUIRE(smem <= 48 * 1024, PGMOE_E_CONFIG, "EP routing table too large");
-    ep_local_routing_kernel<<<1, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(recv_cnt, P, El, *out);
+    ep_local_routing_kernel<<<1, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(recv_cnt, P, El, 0, *out);
     PG_CUDA(cudaGetLastError());
     count_launch();
     return PGMOE_OK;

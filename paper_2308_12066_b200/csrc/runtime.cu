@@ -550,6 +550,23 @@ extern "C" int pgmoe_expert_forward(const float *x, int32_t T, int32_t d, int32_
     return expert_ffn_simt(x, T, d, f, k, experts, expert_stride, wdtype, indexed_by_act, r, h, yw, s);
 }
 
+extern "C" int pgmoe_expert_forward_packed(const uint16_t *xb, int32_t n_max, int32_t d, int32_t f,
+                                           const void *experts, size_t expert_stride, const pgmoe_routing *r,
+                                           uint16_t *hb, float *y, pgmoe_stream_t stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (n_max == 0) return PGMOE_OK;
+    PG_REQUIRE(tc_supported(d, f), PGMOE_E_CONFIG, "tcgen05 kernels need d, f multiples of 128");
+    static void *ws = nullptr;
+    static size_t ws_bytes = 0;
+    if (!ws) {
+        ws_bytes = 64ull << 20;
+        PG_CUDA(cudaMalloc(&ws, ws_bytes));
+        PG_CUDA(cudaMemset(ws, 0, ws_bytes));
+    }
+    return expert_ffn_tc2(nullptr, n_max, d, f, 1, experts, expert_stride, 0, r, const_cast<uint16_t *>(xb), hb, y,
+                          nullptr, ws, ws_bytes, s, true);
+}
+
 extern "C" int pgmoe_dense_forward(const float *yw, int32_t T, int32_t d, int32_t k, const void *dense_w,
                                    int32_t wdtype, float *y, int32_t kernel, pgmoe_stream_t stream) {
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -14,10 +14,18 @@ per rank, the packed send buffer is already grouped by destination; the
 receiver regroups its rows by local expert with the same stable order a
 single GPU would use, so EP outputs equal the single-GPU outputs.
 
-The exchange plan (``dispatch_plan``/``local_routing_plan``) and the
-collectives (``Exchange``) are backend-neutral and are exercised on CPU
-with gloo in tests/test_ep_gloo.py; ``EPDecoder`` drives them with the
-sm_100a kernels.
+With bf16 weights on the tcgen05 path the exchange is FIXED-SIZE: every
+rank reserves a slot of cap = T*k rows for every peer, so both all-to-alls
+run with equal splits and the host never waits for split sizes (no device
+-> host round trip per block); rows travel as the bf16 operand the FFN
+consumes (exact, half the bytes), results come back in fp32 for the exact
+combine.  The split-size variant (``Exchange.rows``) remains for the fp32
+SIMT path.
+
+The exchange plans (``dispatch_plan``/``local_routing_plan`` and their
+padded forms) and the collectives (``Exchange``) are backend-neutral and are
+exercised on CPU with gloo in tests/test_ep_gloo.py; ``EPDecoder`` drives
+them with the sm_100a kernels.
 """
 
 from __future__ import annotations
@@ -63,6 +71,34 @@ def local_routing_plan(recv_cnt: np.ndarray):
     return hist.astype(np.int32), off.astype(np.int32), np.array(perm, dtype=np.int32)
 
 
+def padded_send_plan(hist: np.ndarray, P: int, cap: int) -> np.ndarray:
+    """Slot of every routing position r in the fixed-size send buffer
+    (rank p's slot starts at p*cap): host restatement of pgmoe_ep_pack_send."""
+    h = np.asarray(hist)
+    El = h.size // P
+    off = np.concatenate([[0], np.cumsum(h)])
+    slot = np.empty(int(off[-1]), dtype=np.int64)
+    for p in range(P):
+        a, b = off[p * El], off[(p + 1) * El]
+        slot[a:b] = p * cap + np.arange(b - a)
+    return slot
+
+
+def local_routing_plan_padded(recv_cnt: np.ndarray, cap: int):
+    """pgmoe_ep_local_routing_padded: like local_routing_plan, source p's rows
+    start at p*cap."""
+    P, El = recv_cnt.shape
+    src_off = np.concatenate([np.zeros((P, 1), np.int64), np.cumsum(recv_cnt, axis=1)[:, :-1]], axis=1)
+    hist = recv_cnt.sum(axis=0)
+    off = np.concatenate([[0], np.cumsum(hist)])
+    perm = []
+    for e in range(El):
+        for p in range(P):
+            b = p * cap + src_off[p, e]
+            perm.extend(range(b, b + recv_cnt[p, e]))
+    return hist.astype(np.int32), off.astype(np.int32), np.array(perm, dtype=np.int32)
+
+
 class Exchange:
     """The two all-to-all steps of a block, over a torch.distributed group
     (NCCL for device tensors; gloo works for CPU tensors)."""
@@ -76,6 +112,11 @@ class Exchange:
         """send_cnt [P][El] int32 -> recv_cnt [P][El] (row p = from rank p)."""
         recv = torch.empty_like(send_cnt)
         dist.all_to_all_single(recv, send_cnt.contiguous(), group=self.group)
+        return recv
+
+    def fixed(self, send: torch.Tensor, recv: torch.Tensor) -> torch.Tensor:
+        """Equal-split all-to-all (rank p's chunk = rows [p*cap, (p+1)*cap))."""
+        dist.all_to_all_single(recv, send, group=self.group)
         return recv
 
     def rows(self, send: torch.Tensor, send_splits: list, recv_splits: list) -> torch.Tensor:
@@ -106,8 +147,57 @@ class EPDecoder:
         self.routing = DeviceRouting(max_tokens, config.num_experts, k)
         self._L = _lib.load()
         self.timing = {"exchange_s": 0.0, "blocks": 0}
+        # fixed-size exchange buffers (tcgen05 path): slot of cap rows per peer
+        self.packed = dtype == "bf16" and kernel != "simt" and config.d_model % 128 == 0 \
+            and config.d_ff % 128 == 0 and config.d_ff >= config.d_model
+        self.cap = max_tokens * k
+        if self.packed:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            rows, d, f = self.P * self.cap, config.d_model, config.d_ff
+            bf = dict(dtype=torch.bfloat16, device=dev)
+            self.send = torch.zeros((rows, d), **bf)
+            self.recv = torch.zeros((rows, d), **bf)
+            self.xb = torch.zeros((rows, d), **bf)
+            self.hb = torch.zeros((rows, f), **bf)
+            self.y_recv = torch.zeros((rows, d), dtype=torch.float32, device=dev)
+            self.back = torch.zeros((rows, d), dtype=torch.float32, device=dev)
+            self.yw = torch.zeros((self.cap, d), dtype=torch.float32, device=dev)
+            self.recv_cnt = torch.zeros(self.P * self.El, dtype=torch.int32, device=dev)
 
     def block(self, b: int, x: torch.Tensor, r_in: DeviceRouting, stream=None):
+        if self.packed:
+            return self._block_fixed(b, x, r_in, stream)
+        return self._block_splits(b, x, r_in, stream)
+
+    def _block_fixed(self, b: int, x: torch.Tensor, r_in: DeviceRouting, stream=None):
+        """One block with the fixed-size exchange: no host synchronisation."""
+        c, L, ex = self.config, self._L, self.ex
+        T, d, f, k = x.shape[0], c.d_model, c.d_ff, c.top_k
+        P, El, cap = self.P, self.El, self.cap
+        if T * k > cap:
+            raise ShapeError(f"T={T} exceeds the EP buffers (max_tokens={self.max_tokens})")
+        s = _stream(stream)
+        _lib.check(L.pgmoe_ep_pack_send(_ptr(x), ctypes.byref(r_in.c), T, d, k, P, El, cap, _ptr(self.send), s))
+        ex.fixed(r_in.hist[:P * El], self.recv_cnt)     # counts [P][El]
+        ex.fixed(self.send, self.recv)                   # bf16 rows, cap per peer
+        _lib.check(L.pgmoe_ep_local_routing_padded(_ptr(self.recv_cnt), P, El, cap, ctypes.byref(self.lr.c), s))
+        _lib.check(L.pgmoe_ep_pack_recv(_ptr(self.recv), ctypes.byref(self.lr.c), El, P * cap, d, _ptr(self.xb), s))
+        base, stride = ctypes.c_void_p(), ctypes.c_size_t()
+        eb, nl = ctypes.c_int32(), ctypes.c_int32()
+        _lib.check(L.pgmoe_model_expert_records(self.model._h, b, ctypes.byref(base), ctypes.byref(stride),
+                                                ctypes.byref(eb), ctypes.byref(nl)))
+        _lib.check(L.pgmoe_expert_forward_packed(_ptr(self.xb), P * cap, d, f, base, stride.value,
+                                                 ctypes.byref(self.lr.c), _ptr(self.hb), _ptr(self.y_recv), s))
+        ex.fixed(self.y_recv, self.back)                 # fp32 results back to their senders
+        _lib.check(L.pgmoe_ep_unpermute_padded(_ptr(self.back), ctypes.byref(r_in.c), T, d, k, P, El, cap,
+                                               _ptr(self.yw), s))
+        y = torch.empty_like(x)
+        from .core import _KERNEL
+        _lib.check(L.pgmoe_dense_forward(_ptr(self.yw), T, d, k, _ptr(self.model.matrix("non_moe", b)),
+                                         self.model.wdt, _ptr(y), _KERNEL[self.kernel], s))
+        return y
+
+    def _block_splits(self, b: int, x: torch.Tensor, r_in: DeviceRouting, stream=None):
         c = self.config
         L = self._L
         T, d, f, k = x.shape[0], c.d_model, c.d_ff, c.top_k

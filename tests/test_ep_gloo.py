@@ -52,6 +52,37 @@ def _ep_block_numpy(x, ids, w, model, b, E, ex, P, rank):
     return np.stack([og.matvec(model.dense(b), mix[t]) for t in range(T)])
 
 
+def _ep_block_numpy_padded(x, ids, w, model, b, E, ex, P, rank):
+    """Same block with the fixed-size exchange (cap rows per peer, equal
+    splits): padded_send_plan / Exchange.fixed / local_routing_plan_padded."""
+    from paper_2308_12066_b200.ep import local_routing_plan_padded, padded_send_plan
+    T, k = ids.shape
+    El = E // P
+    cap = T * k
+    hist, off, perm, act = og.permute(ids, E)
+    slot = padded_send_plan(hist, P, cap)
+    send = np.zeros((P * cap, x.shape[1]))
+    send[slot] = x[perm // k]
+    recv_cnt = ex.fixed(torch.from_numpy(hist.astype(np.int32)), torch.zeros(E, dtype=torch.int32)).numpy()
+    recv = ex.fixed(torch.from_numpy(send), torch.zeros_like(torch.from_numpy(send))).numpy()
+    lhist, loff, lperm = local_routing_plan_padded(recv_cnt.reshape(P, El), cap)
+    y_recv = np.full_like(recv, np.nan)  # unfilled slots must never be read back
+    for le in range(El):
+        e = rank * El + le
+        for r in lperm[loff[le]:loff[le + 1]]:
+            y_recv[r] = og.expert_forward(recv[r], model.w1(b, e), model.w2(b, e))
+    back = ex.fixed(torch.from_numpy(y_recv), torch.zeros_like(torch.from_numpy(y_recv))).numpy()
+    wflat = w.reshape(-1)
+    yw = np.zeros((T * k, x.shape[1]))
+    for r in range(T * k):
+        yw[perm[r]] = wflat[perm[r]] * back[slot[r]]
+    mix = np.zeros((T, x.shape[1]))
+    for t in range(T):
+        for s in range(k):
+            mix[t] = mix[t] + yw[t * k + s]
+    return np.stack([og.matvec(model.dense(b), mix[t]) for t in range(T)])
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -65,10 +96,11 @@ def _worker(rank, world, port, q):
         x = np.stack([og.token_input(dims, rank * T + t) for t in range(T)])
         ids, w = og.gate_batch(x, model.gate(0), 2)
         y = _ep_block_numpy(x, ids, w, model, 0, 8, ex, world, rank)
+        yp = _ep_block_numpy_padded(x, ids, w, model, 0, 8, ex, world, rank)
         # single-process reference for the same tokens
         ref = og.block_batch(x, ids, w, {e: model.w1(0, e) for e in range(8)},
                              {e: model.w2(0, e) for e in range(8)}, model.dense(0), 8)
-        q.put((rank, float(np.max(np.abs(y - ref)))))
+        q.put((rank, float(max(np.max(np.abs(y - ref)), np.max(np.abs(yp - ref))))))
     finally:
         dist.destroy_process_group()
 
