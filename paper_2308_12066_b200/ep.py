@@ -147,6 +147,10 @@ class EPDecoder:
         self.routing = DeviceRouting(max_tokens, config.num_experts, k)
         self._L = _lib.load()
         self.timing = {"exchange_s": 0.0, "blocks": 0}
+        import os
+        self.use_graph = os.environ.get("PGMOE_EP_GRAPH", "1") != "0"
+        self._graphs: dict = {}
+        self.replayed_kernels = 0  # our kernels launched by graph replays (benchmark evidence)
         # fixed-size exchange buffers (tcgen05 path): slot of cap rows per peer
         self.packed = dtype == "bf16" and kernel != "simt" and config.d_model % 128 == 0 \
             and config.d_ff % 128 == 0 and config.d_ff >= config.d_model
@@ -236,7 +240,46 @@ class EPDecoder:
         return y
 
     def decoder_iteration(self, x: torch.Tensor, trace: bool = False):
-        """Local tokens x [T][d] (cuda fp32) -> (y, consumed ids per block)."""
+        """Local tokens x [T][d] (cuda fp32) -> (y, consumed ids per block).
+
+        With the fixed-size exchange nothing in an iteration waits on the
+        host, so the whole iteration (routing, packs, NCCL all-to-alls, FFN,
+        combine, dense) is captured once per input buffer into a CUDA graph
+        and replayed; the returned y is the graph's output buffer."""
+        if self.packed and self.use_graph and not trace:
+            key = (x.data_ptr(), tuple(x.shape))
+            entry = self._graphs.get(key)
+            if entry is None:
+                try:
+                    entry = self._capture(x)
+                except Exception as e:  # noqa: BLE001 - capture unsupported: run the same work eagerly
+                    import warnings
+                    warnings.warn(f"EP graph capture failed ({e}); running eagerly")
+                    self.use_graph = False
+                    return self._iteration(x, trace)
+                if len(self._graphs) >= 4:
+                    self._graphs.pop(next(iter(self._graphs)))
+                self._graphs[key] = entry
+            g, y, n = entry
+            g.replay()
+            self.replayed_kernels += n
+            return y, None
+        return self._iteration(x, trace)
+
+    def _capture(self, x: torch.Tensor):
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._iteration(x, False)  # warm-up: communicators, workspaces, allocator
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = self._L.pgmoe_launch_count()
+        with torch.cuda.graph(g):
+            y, _ = self._iteration(x, False)
+        return g, y, self._L.pgmoe_launch_count() - n0  # our kernels per replay
+
+    def _iteration(self, x: torch.Tensor, trace: bool = False):
         from .core import route
         c = self.config
         pending: dict = {}

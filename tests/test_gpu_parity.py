@@ -476,6 +476,11 @@ def test_ep_decoder_single_rank_nccl_equals_single_gpu():
         torch.cuda.synchronize()
         assert torch.equal(ids_ep, ids)
         assert torch.equal(y_ep, y)
+        # without a trace the iteration is captured once and replayed
+        for _ in range(3):
+            y_g, _ = ep.decoder_iteration(x)
+        torch.cuda.synchronize()
+        assert ep.replayed_kernels > 0 and torch.equal(y_g, y)
         ep.close()
         ref.close()
     finally:
