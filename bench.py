@@ -254,6 +254,9 @@ def run_ours(args, rank: int, world: int):
     torch.cuda.synchronize()
     tl = model.timeline()
     model.set_timeline(False)
+    # the profile pass runs the host loop (no graph replay), so its stats say
+    # which stages ran inside the block launch
+    st_prof = model.stats()
     gpu_launches_per_step = launches / args.steps
 
     # ---- per-kernel roofline from the CUDA events on the compute stream ---
@@ -274,10 +277,10 @@ def run_ours(args, rank: int, world: int):
     # per routed token: bf16 x packed+read, bf16 h write+read, fp32 yw + bf16 mix written
     act_bytes_per_token = 2 * d * 2 + 2 * f * 2 + d * 6
     ffn_bytes = nact_total * rec + prof_steps * nb * T * act_bytes_per_token
-    fused = st.get("fused_blocks", 0) > 0
+    fused = st_prof.get("fused_blocks", 0) > 0
     if fused:  # the dense layer runs inside the same launch: its weights and activations
         ffn_bytes += prof_steps * nb * (d * d * sw + T * d * (2 + 4))
-    routed_in_launch = st.get("fused_routes", 0) > 0
+    routed_in_launch = st_prof.get("fused_routes", 0) > 0
     if routed_in_launch:  # resident: the next block's pre-gate (gate weights + block input) too
         ffn_bytes += prof_steps * (nb - 1) * (d * E * sw + T * d * 4)
     ffn_gbs = ffn_bytes / ffn_s / 1e9 if ffn_s > 0 else None

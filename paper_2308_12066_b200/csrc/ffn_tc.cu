@@ -1066,7 +1066,7 @@ int tc_pack_rows(const float *x, const int *perm, int n, int d, int k, uint16_t 
 int block_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
              const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, bool xb_ready,
              const void *dense_w, float *y, uint16_t *next_xb, const int *next_inv, void *ws, size_t ws_bytes,
-             cudaStream_t s, const FusedRoute *route, const LaunchChain *chain) {
+             cudaStream_t s, const FusedRoute *route, const LaunchChain *chain, int n_experts) {
     PG_REQUIRE(tc_supported(d, f), PGMOE_E_CONFIG, "tcgen05 path needs d, f multiples of 128 and f >= d");
     PG_REQUIRE((reinterpret_cast<uintptr_t>(experts) & 15) == 0 && stride % 16 == 0, PGMOE_E_CONFIG,
                "expert records must be 16-byte aligned");
@@ -1117,7 +1117,11 @@ int block_tc(const float *x, int T, int d, int f, int k, const void *experts, si
         p.epoch_set = chain->epoch_set;
         parity = chain->parity & 1;
     }
-    return tc::run(mp, p, (n >= 2048) ? 256 : 64, ws, ws_bytes, s, parity);
+    // N tile: 64 tokens (8 weight stages) while the average expert holds at
+    // most 64 routed tokens; 256 (4 stages) only for compute-heavy groups —
+    // a group wider than the N tile re-reads its weight tile per N tile
+    const bool wide = n_experts > 0 ? (long long)n > 64LL * n_experts : n >= 2048;
+    return tc::run(mp, p, wide ? 256 : 64, ws, ws_bytes, s, parity);
 }
 
 int expert_ffn_tc2(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,

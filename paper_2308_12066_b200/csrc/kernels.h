@@ -39,7 +39,8 @@ struct LaunchChain {
 int block_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
              const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, bool xb_ready,
              const void *dense_w, float *y, uint16_t *next_xb, const int *next_inv, void *ws, size_t ws_bytes,
-             cudaStream_t s, const FusedRoute *route = nullptr, const LaunchChain *chain = nullptr);
+             cudaStream_t s, const FusedRoute *route = nullptr, const LaunchChain *chain = nullptr,
+             int n_experts = 0);
 // next_xb / next_inv (optional): scatter y as the next block's packed bf16
 // up-projection operand (the next block's routing is already known).
 int dense_tc2(const float *yw, const uint16_t *mixb_ready, int T, int d, int k, const void *dense_w, float *y,

@@ -427,8 +427,12 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
     // Resident top-1 blocks compute their pre-gate inside the block launch
     // (it depends only on the block input); offloaded blocks keep the
     // separate K1 launch because the host needs the active list at once.
+    // The routing role (2 warps per CTA) keeps up with the expert GEMMs while
+    // its work (~T·d·E fp64 FMAs + the permutation) is small next to theirs
+    // (~E·d·f weight bytes): measured crossover T ≈ f/8 (Base-64 better fused
+    // at T=256, separate at 512; Large-128 fused at 512, separate at 1024).
     const bool fuse_route = !off && use_tc(m) && c.top_k == 1 && L == 1 && m->fuse_route &&
-                            fused_route_supported(c.num_experts) && T <= (1 << 16);
+                            fused_route_supported(c.num_experts) && (long long)T * 8 <= c.d_ff;
     const float *cur = x_in;
     // Chained block launches (fused routing): each launch waits for its
     // predecessor's dense phase through a device counter instead of for its
@@ -480,7 +484,7 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
             PG_TRY(block_tc(cur, T, c.d_model, c.d_ff, 1, experts, m->rec_bytes, indexed, &rb.r, m->xb, m->hb, m->yw,
                             m->mixb, xb_ready, bw.dense, nxt, next_r ? m->xb : nullptr, next_r ? next_r->inv : nullptr,
                             m->tc_ws, m->tc_ws_bytes, s, fr.active ? &fr : nullptr,
-                            chain ? &lc : nullptr));
+                            chain ? &lc : nullptr, m->e_local));
             if (fr.active) m->fused_routes++;
             tl_end(m, s);
             if (off) {
