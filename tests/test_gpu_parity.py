@@ -291,7 +291,7 @@ def test_offloaded_equals_resident_and_ledger(dtype):
     off.close()
 
 
-@pytest.mark.parametrize("E,T", [(64, 1), (64, 40), (128, 256), (256, 17)])
+@pytest.mark.parametrize("E,T", [(64, 1), (64, 10), (64, 40), (128, 33), (128, 256), (256, 17)])
 def test_fused_routing_equals_separate_launch_and_offloaded(E, T):
     """Resident top-1 decoding computes each pre-gate inside the block's
     tcgen05 launch (route_common.cuh).  Routing ids, weights and block
