@@ -81,7 +81,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 // Debug probes (tools/probe.py): per-CTA %globaltimer stamps written when a
 // probe buffer is installed with pgmoe_debug_set_probe(); null otherwise.
-constexpr int kProbeSlots = 32;
+constexpr int kProbeSlots = 48;
 unsigned long long *probe_buffer(int kind, int ctas);  // 0: route, 1: tcgen05 block kernel
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;

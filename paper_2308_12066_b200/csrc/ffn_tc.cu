@@ -60,7 +60,9 @@ constexpr int kMetaInts = 512;        // per-column epilogue metadata staged in 
 // split-K cost model (bytes per microsecond; microseconds)
 constexpr float kSmBytesPerUs = 150e3f;   // one SM's TMA stream when few CTAs load
 constexpr float kHbmBytesPerUs = 6.5e6f;  // whole-chip HBM stream
-constexpr float kFixUs = 3.0f;            // split-K fix-up chain
+constexpr float kFixUs = 3.0f;            // split-K fix-up chain (stores, fence, ticket)
+constexpr float kFixRoundUs = 1.0f;       // + one dependent partial-load round per kFixSplits splits
+constexpr int kFixSplits = 4;
 
 enum Mode { kUp = 0, kDown = 1, kDense = 2 };
 
@@ -88,6 +90,7 @@ struct Params {
     unsigned long long *probe;  // debug stamps [grid][kProbeSlots] or null
     FusedRoute route;           // the next block's routing, computed by warps 7-8 (resident)
     int max_inflight;           // weight stages the producer keeps in flight (<= STAGES)
+    int max_split;              // cap on the split-K factor (0: cost model only)
     // Chained launches (resident decoder): instead of waiting for the previous
     // launch to COMPLETE (griddepcontrol.wait, ~4-6 us after its last CTA),
     // phase 0 and the routing role wait for its dense phase to be written:
@@ -213,10 +216,10 @@ __device__ __forceinline__ Unit decode_unit(const PhaseSched *ps, int nphase, co
     int ph = 0;
     while (ph + 1 < nphase && u >= ps[ph + 1].unit0) ++ph;
     const PhaseSched &sc = ps[ph];
-    const long long lu = u - sc.unit0;
+    const int lu = (int)(u - sc.unit0);  // 32-bit: a 64-bit divide is ~100 instructions per unit
     x.ph = ph;
-    x.tile = (int)(lu / sc.S);
-    x.s = (int)(lu - (long long)x.tile * sc.S);
+    x.tile = lu / sc.S;
+    x.s = lu - x.tile * sc.S;
     int ng;
     if (sc.mode == kDense) {
         x.g = 0;
@@ -495,11 +498,14 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
     if (tid == 0) probe(p.probe, blockIdx.x, 1);  // prologue done
     const int max_npad_expert = s_flag[1], ntiles_expert = s_flag[2];
 
-    if (tid == 0) {
+    // One warp: every lane prices one split factor (the cost model is on the
+    // critical path of every CTA that enters after its dependency resolved)
+    if (warp == 0) {
     long long total_units = 0, part_used = 0;
     int ctr_used = 0;
+    const int grid = (int)gridDim.x;
     for (int i = 0; i < p.nphase; ++i) {
-        PhaseSched &sc = ps[i];
+        PhaseSched sc;
         sc.mode = p.ph[i].mode;
         sc.M = p.ph[i].M;
         sc.K = p.ph[i].K;
@@ -524,18 +530,29 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         // time of a unit = its bytes / per-CTA bandwidth, where the per-CTA
         // bandwidth is the single-SM TMA limit when few CTAs stream and the
         // HBM share when all do (measured on B200 with tools/probe.py).
-        const int s_cap = max(1, min(sc.kb_total, 8 * 16 / min(BN, max_npad)));
+        int s_cap = max(1, min(sc.kb_total, 8 * 16 / min(BN, max_npad)));
+        if (p.max_split > 0) s_cap = min(s_cap, p.max_split);
         const float kb_bytes = (float)(kABytes + max_npad * 128);
+        const int tiles = (int)sc.tiles;
+        const int cand = lane + 1;
+        float t = 3.4e38f;
+        // Beyond 2, a split only pays as coverage (at most one unit per
+        // CTA): the epilogue runs one split tile at a time, each paying the
+        // fix-up chain, so more units per CTA serialise on it
+        // (tools/gpu_split_sweep2.sh: Base-64 T=4..128 -3..10 % capped at 2)
+        if (cand <= s_cap && tiles > 0 && !(cand > 2 && tiles * cand > grid)) {
+            const int units = tiles * cand;
+            const int kbs = (sc.kb_total + cand - 1) / cand;
+            const int waves = (units + grid - 1) / grid;
+            const float bw = fminf(kSmBytesPerUs, kHbmBytesPerUs / (float)min(units, grid));
+            const float fix = cand > 1 ? kFixUs + kFixRoundUs * ((cand + kFixSplits - 1) / kFixSplits) : 0.f;
+            t = (float)waves * kbs * kb_bytes / bw + fix;
+        }
         int S = 1;
         float best = 3.4e38f;
-        for (int cand = 1; cand <= s_cap && sc.tiles > 0; ++cand) {
-            const long long units = sc.tiles * cand;
-            const int kbs = (sc.kb_total + cand - 1) / cand;
-            const long long waves = (units + gridDim.x - 1) / gridDim.x;
-            const float active = (float)min(units, (long long)gridDim.x);
-            const float bw = fminf(kSmBytesPerUs, kHbmBytesPerUs / active);
-            const float t = (float)waves * kbs * kb_bytes / bw + (cand > 1 ? kFixUs : 0.f);
-            if (t < best * 0.98f) { best = t; S = cand; }
+        for (int c = 0; c < 32; ++c) {  // ascending: a larger split must win by 2 %
+            const float tc = __shfl_sync(0xffffffffu, t, c);
+            if (tc < best * 0.98f) { best = tc; S = c + 1; }
         }
         // phases can run concurrently (per-expert gating), so each phase's
         // tickets and partial tiles live in their own ranges
@@ -552,8 +569,13 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         sc.units = sc.tiles * sc.S;
         sc.unit0 = total_units;
         total_units += sc.units;
+        if (lane == 0) ps[i] = sc;
     }
-    s_total_units = total_units;
+    if (lane == 0) {
+        s_total_units = total_units;
+        if (p.probe && blockIdx.x == 0)  // chosen split per phase (slots 23, 24, 31: values, not times)
+            for (int i = 0; i < p.nphase; ++i) p.probe[(i == 2) ? 31 : 23 + i] = (unsigned long long)ps[i].S;
+    }
     }
     __syncthreads();
     const long long total_units = s_total_units;
@@ -853,23 +875,24 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                     __threadfence();
                     if (et == 0) probe(p.probe, blockIdx.x, 14);  // fix-up start (last unit)
                     const float *base = p.partial + sc.part0 + (size_t)x.tile * S * (BN * BM) + et;
-                    // 32 partial loads in flight per thread: 16 columns x 2
-                    // splits at a time, summed in split order (deterministic)
+                    // 64 partial loads in flight per thread: 16 columns x 4
+                    // splits at a time (one dependent round for S <= 4),
+                    // summed in split order (deterministic)
                     for (int n0 = 0; n0 < x.n_valid; n0 += 16) {
                         float a[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) a[j] = 0.f;
-                        for (int s0 = 0; s0 < S; s0 += 2) {
-                            float v[2][16];
+                        for (int s0 = 0; s0 < S; s0 += kFixSplits) {
+                            float v[kFixSplits][16];
 #pragma unroll
-                            for (int h = 0; h < 2; ++h)
+                            for (int h = 0; h < kFixSplits; ++h)
 #pragma unroll
                                 for (int j = 0; j < 16; ++j)
                                     v[h][j] = (s0 + h < S && n0 + j < x.n_valid)
                                                   ? __ldcg(base + ((size_t)(s0 + h) * BN + n0 + j) * BM)
                                                   : 0.f;
 #pragma unroll
-                            for (int h = 0; h < 2; ++h)
+                            for (int h = 0; h < kFixSplits; ++h)
 #pragma unroll
                                 for (int j = 0; j < 16; ++j)
                                     if (s0 + h < S) a[j] += v[h][j];
@@ -1039,6 +1062,7 @@ static int run(const PhaseMaps *mp, Params p, int bn, void *ws, size_t ws_bytes,
     p.probe = probe_buffer(1, kNumSMs);
     if (p.max_inflight <= 0) p.max_inflight = 8;
     { const char *e = getenv("PGMOE_INFLIGHT"); if (e) p.max_inflight = atoi(e); }
+    { const char *e = getenv("PGMOE_MAX_SPLIT"); if (e) p.max_split = atoi(e); }
     if (bn <= 64) return launch<64, 8>(mp, p, s);
     return launch<256, 4>(mp, p, s);
 }

@@ -84,8 +84,10 @@ template <> struct Vec<float> {
 template <typename GT> __device__ __forceinline__ double gval(const GT *G, size_t i) { return Vec<GT>::one(G + i); }
 
 // Serial fp64 logit in the reference order (linalg.py:35-37): out += x_i*G_ij.
+// Not inlined: the rare uncertified path would otherwise put NJ unrolled
+// copies of this loop into the routing role's instruction stream.
 template <typename GT>
-__device__ double serial_logit(const float *x, const GT *G, int d, int E, int j) {
+__device__ __noinline__ double serial_logit(const float *x, const GT *G, int d, int E, int j) {
     double acc = 0.0;
     for (int i = 0; i < d; ++i) acc = __dadd_rn(acc, __dmul_rn((double)x[i], gval(G, (size_t)i * E + j)));
     return acc;
@@ -122,7 +124,16 @@ struct FusedRoute {
     double *plogit;      // [splits][T][E]
     float *pcmax;        // [tiles][splits][E]
     double *pxsum;       // [splits][T]
+    double gam, bscale;  // error-bound constants of d (route_bound_constants)
 };
+
+// gamma_d = d u / (1 - d u) and the certified-ranking bound scale, computed
+// once on the host (IEEE double, the same values route.cu derives on device)
+inline void route_bound_constants(int d, double *gam, double *bscale) {
+    const double u = 1.1102230246251565e-16;  // 2^-53
+    *gam = (double)d * u / (1.0 - (double)d * u);
+    *bscale = 2.0 * *gam / (1.0 - *gam) * 1.001;
+}
 
 // Splits for a fused routing of T tokens: one unit per SM where possible,
 // at most kRouterMaxKn gate rows per split.
@@ -277,7 +288,8 @@ __device__ __forceinline__ TileSums tile_sums_layout(float *xs, int E) {
     ts.cms = reinterpret_cast<float *>(ts.lgs + kRouterTok * E);
     return ts;
 }
-static __device__ __noinline__ void router_reduce_tile(const FusedRoute &r, int tile, int t0, int ntok, int rt, const TileSums &ts) {
+static __device__ __noinline__ void router_reduce_tile(const FusedRoute &r, int tile, int t0, int ntok, int rt, const TileSums &ts,
+                                                       unsigned long long *pr) {
     const int E = r.E, T = r.T, S = r.splits;
     const int lane = rt & 31, w = rt >> 5;
     for (int t = w; t < ntok; t += kRouterWarps) {
@@ -286,6 +298,7 @@ static __device__ __noinline__ void router_reduce_tile(const FusedRoute &r, int 
         sx = warp_sumd(sx);
         if (lane == 0) ts.sxs[t] = sx;
     }
+    if (rt == 0 && t0 == tile * kRouterTok) probe(pr, blockIdx.x, 35);  // sum |x| loaded
     const int n = ntok * E;
     for (int q0 = rt; q0 < n; q0 += 2 * kRouterThreads) {
         double pl[2][16];
@@ -329,11 +342,10 @@ static __device__ __noinline__ void router_reduce_tile(const FusedRoute &r, int 
 // token's index in the tile (shared sums), `tok`: its global index.
 template <typename GT, int NJ>
 __device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int t, int tok, int lane,
-                                    int *s_ids, float *s_w) {
+                                    int *s_ids, float *s_w, unsigned long long *pr = nullptr) {
+    if (t != 0 || lane != 0) pr = nullptr;
     const int E = r.E, k = r.k, d = r.d;
-    const double u = 1.1102230246251565e-16;  // 2^-53
-    const double gam = (double)d * u / (1.0 - (double)d * u);
-    const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
+    const double gam = r.gam, bscale = r.bscale;
     const double bpad = 1e-300;
     const double sx = ts.sxs[t] * (1.0 + 2.0 * gam);
     double lg[NJ], bd[NJ];
@@ -350,6 +362,7 @@ __device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int
             if (jj == (bi >> 5)) mine = a[jj];
         return __shfl_sync(0xffffffffu, mine, bi & 31);
     };
+    probe(pr, blockIdx.x, 37);
     bool finite = true;
 #pragma unroll
     for (int jj = 0; jj < NJ; ++jj) finite &= (bool)isfinite(lg[jj]);
@@ -413,6 +426,7 @@ __device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int
         }
         if (lane == 0) atomicAdd(r.out.status + 1, 1);
     }
+    probe(pr, blockIdx.x, 38);
     // softmax over all E (linalg.py:54-59), max-subtracted; same order as route.cu
     double m = -INFINITY;
 #pragma unroll
@@ -422,6 +436,7 @@ __device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int
 #pragma unroll
     for (int jj = 0; jj < NJ; ++jj) z += exp(lg[jj] - m);
     z = warp_sumd(z);
+    probe(pr, blockIdx.x, 39);
     for (int s = 0; s < k; ++s) {
         const double pr = exp(pick(lg, sel[s]) - m) / z;
         if (lane == 0) {
@@ -539,9 +554,12 @@ __device__ void router_role(const FusedRoute &r, int rt, float *xs, int *s_flag,
         static_assert(CH >= 1, "routing scratch too small");
         for (int c0 = 0; c0 < ntok; c0 += CH) {
             const int nc = min(CH, ntok - c0);
-            router_reduce_tile(r, tile, t0 + c0, nc, rt, ts);
+            router_reduce_tile(r, tile, t0 + c0, nc, rt, ts, pr);
+            if (rt == 0 && c0 == 0) probe(pr, blockIdx.x, 32);  // partials reduced
             for (int t = w; t < nc; t += kRouterWarps)
-                router_select_token<GT, NJ>(r, ts, t, t0 + c0 + t, lane, s_ids + c0 * r.k, s_w + c0 * r.k);
+                router_select_token<GT, NJ>(r, ts, t, t0 + c0 + t, lane, s_ids + c0 * r.k, s_w + c0 * r.k,
+                                            c0 == 0 ? pr : nullptr);
+            if (rt == 0 && c0 == 0) probe(pr, blockIdx.x, 33);  // warp 0 selected
             router_sync();  // the sums are rewritten by the next chunk
         }
         __threadfence();

@@ -379,6 +379,7 @@ static FusedRoute fused_route_args(pgmoe_model *m, const float *x, int T, const 
     r.E = c.num_experts;
     r.T = T;
     r.k = c.top_k;
+    route_bound_constants(r.d, &r.gam, &r.bscale);
     r.splits = fused_route_splits(T, c.d_model, kNumSMs);
     r.tiles = (T + kRouterTok - 1) / kRouterTok;
     r.x = x;

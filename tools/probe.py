@@ -32,7 +32,8 @@ ROUTE_SLOTS = {0: "entry", 1: "pdl", 2: "logits", 3: "sel0", 7: "selred", 8: "ra
                6: "perm1"}
 BLOCK_SLOTS = {0: "entry", 1: "prolog", 2: "gate0", 3: "gate1", 4: "gate2", 5: "acc0", 6: "ph0", 7: "ph1",
                8: "ph2", 11: "lastld", 12: "accN", 13: "partN", 14: "fixN", 15: "endN",
-               25: "r_pdl", 26: "r_logits", 27: "r_sel0", 28: "r_sel1", 29: "r_perm", 30: "r_trig", 9: "exit"}
+               25: "r_pdl", 26: "r_logits", 27: "r_sel0", 35: "r_sx", 32: "r_red", 37: "s_load", 38: "s_cert", 39: "s_z", 33: "r_selt", 28: "r_sel1", 29: "r_perm",
+               30: "r_trig", 9: "exit"}
 ROWS = 1 << 15
 
 
@@ -71,8 +72,8 @@ def main():
         m.set_fused_route(False)
     x = torch.from_numpy(token_batch(0, cfg.d_model, args.tokens)).cuda()
     y = torch.empty_like(x)
-    pr = torch.zeros((ROWS, 32), dtype=torch.int64, device="cuda")
-    pb = torch.zeros((ROWS, 32), dtype=torch.int64, device="cuda")
+    pr = torch.zeros((ROWS, 48), dtype=torch.int64, device="cuda")
+    pb = torch.zeros((ROWS, 48), dtype=torch.int64, device="cuda")
     for it in range(4):
         if it == 0 or args.placement != "resident":
             _lib.check(L.pgmoe_debug_set_probe(0, pr.data_ptr(), ROWS))
@@ -135,6 +136,7 @@ def main():
     b = bl[1]
     res["producer_us"] = {k: [round(float(np.percentile(b[:, s] / 1.86e3, q)), 1) for q in (0, 50, 100)]
                           for k, s in (("gate", 16), ("empty", 17), ("atomic", 18))}
+    res["split_per_phase"] = [int(b[0, 23]), int(b[0, 24]), int(b[0, 31])]
     res["units_per_cta"] = [int(b[:, 19].min()), float(np.median(b[:, 19])), int(b[:, 19].max())]
     print(json.dumps(res))
 
