@@ -163,7 +163,7 @@ __device__ __forceinline__ void router_sync() { asm volatile("bar.sync 2, %0;" :
 constexpr int kRouterSmemFloats = 3328;  // x slice + row-split reduction (13 KB)
 
 template <typename GT, int NJ>
-__device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs) {
+__device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs, unsigned long long *pr) {
     const int E = r.E, T = r.T, d = r.d;
     const int tile = unit / r.splits, split = unit - tile * r.splits;
     const int t0 = tile * kRouterTok, ntok = min(kRouterTok, T - t0);
@@ -192,6 +192,7 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs) 
         sx = warp_sumd(sx);
         if (lane == 0) r.pxsum[(size_t)split * T + t0 + t] = sx;
     }
+    if (rt == 0) probe(pr, blockIdx.x, 40);  // x slice in shared memory
     const int cg = rt % CG, tg = rt / CG;
     const int tbase = rowsplit ? 0 : tg * NJ;
     const int rstart = rowsplit ? tg : 0, rstep = rowsplit ? TG : 1;
@@ -207,7 +208,7 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs) 
     // runs next to the expert GEMMs' weight stream, so every load sees the
     // loaded memory latency (in-flight bytes / bandwidth)
     using Raw = typename Vec<GT>::Raw;
-    constexpr int RB = sizeof(Raw) <= 8 ? 16 : 8;
+    constexpr int RB = (sizeof(Raw) <= 8 ? 16 : 8) * (NJ <= 2 ? 2 : 1);  // E=64: small accumulators, 32 rows in flight
     for (int n0 = 0; n0 < nrows; n0 += RB) {
         Raw raw[RB];
 #pragma unroll
@@ -231,6 +232,7 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs) 
             }
         }
     }
+    if (rt == 0) probe(pr, blockIdx.x, 41);  // gate rows consumed
     if (!rowsplit) {
 #pragma unroll
         for (int tt = 0; tt < NJ; ++tt) {
@@ -281,11 +283,12 @@ struct TileSums {
     float *cms;   // [ntok][E]
     double *sxs;  // [kRouterTok]
 };
-__device__ __forceinline__ TileSums tile_sums_layout(float *xs, int E) {
+// ch: tokens per chunk (the scratch holds ch rows of sums, see router_role)
+__device__ __forceinline__ TileSums tile_sums_layout(float *xs, int E, int ch) {
     TileSums ts;
     ts.sxs = reinterpret_cast<double *>(xs);
     ts.lgs = ts.sxs + kRouterTok;
-    ts.cms = reinterpret_cast<float *>(ts.lgs + kRouterTok * E);
+    ts.cms = reinterpret_cast<float *>(ts.lgs + ch * E);
     return ts;
 }
 static __device__ __noinline__ void router_reduce_tile(const FusedRoute &r, int tile, int t0, int ntok, int rt, const TileSums &ts,
@@ -532,7 +535,7 @@ __device__ void router_role(const FusedRoute &r, int rt, float *xs, int *s_flag,
     const int lane = rt & 31, w = rt >> 5;
     const int units = r.tiles * r.splits;
     for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
-        router_logits<GT, NJ>(r, unit, rt, xs);
+        router_logits<GT, NJ>(r, unit, rt, xs, unit == (int)blockIdx.x ? pr : nullptr);
         if (rt == 0) probe(pr, blockIdx.x, 26);  // partial logits written
         const int tile = unit / r.splits;
         __threadfence();
@@ -543,7 +546,7 @@ __device__ void router_role(const FusedRoute &r, int rt, float *xs, int *s_flag,
         __threadfence();
         const int t0 = tile * kRouterTok, ntok = min(kRouterTok, r.T - t0);
         if (rt == 0) probe(pr, blockIdx.x, 27);  // tile select start
-        const TileSums ts = tile_sums_layout(xs, r.E);
+
         // the tile's ids / weights also stay in shared memory (the end of the
         // scratch, clear of the sums and of the permutation's histograms)
         int *s_ids = reinterpret_cast<int *>(xs + kRouterSmemFloats - 2 * kRouterTok * 8);
@@ -552,6 +555,9 @@ __device__ void router_role(const FusedRoute &r, int rt, float *xs, int *s_flag,
         constexpr int kChunk = (kRouterSmemFloats - 2 * kRouterTok * 8 - 2 * kRouterTok) / (NJ * 32 * 3);
         constexpr int CH = kChunk < kRouterTok ? kChunk : kRouterTok;
         static_assert(CH >= 1, "routing scratch too small");
+        static_assert(2 * kRouterTok + CH * NJ * 32 * 3 + 2 * kRouterTok * 8 <= kRouterSmemFloats,
+                      "tile sums + ids / weights exceed the routing scratch");
+        const TileSums ts = tile_sums_layout(xs, r.E, CH);
         for (int c0 = 0; c0 < ntok; c0 += CH) {
             const int nc = min(CH, ntok - c0);
             router_reduce_tile(r, tile, t0 + c0, nc, rt, ts, pr);

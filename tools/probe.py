@@ -32,7 +32,7 @@ ROUTE_SLOTS = {0: "entry", 1: "pdl", 2: "logits", 3: "sel0", 7: "selred", 8: "ra
                6: "perm1"}
 BLOCK_SLOTS = {0: "entry", 1: "prolog", 2: "gate0", 3: "gate1", 4: "gate2", 5: "acc0", 6: "ph0", 7: "ph1",
                8: "ph2", 11: "lastld", 12: "accN", 13: "partN", 14: "fixN", 15: "endN",
-               25: "r_pdl", 26: "r_logits", 27: "r_sel0", 35: "r_sx", 32: "r_red", 37: "s_load", 38: "s_cert", 39: "s_z", 33: "r_selt", 28: "r_sel1", 29: "r_perm",
+               25: "r_pdl", 40: "r_xs", 41: "r_rows", 26: "r_logits", 27: "r_sel0", 35: "r_sx", 32: "r_red", 37: "s_load", 38: "s_cert", 39: "s_z", 33: "r_selt", 28: "r_sel1", 29: "r_perm",
                30: "r_trig", 9: "exit"}
 ROWS = 1 << 15
 
