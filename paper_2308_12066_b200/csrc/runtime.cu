@@ -432,8 +432,13 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
     // its work (~T·d·E fp64 FMAs + the permutation) is small next to theirs
     // (~E·d·f weight bytes): measured crossover T ≈ f/8 (Base-64 better fused
     // at T=256, separate at 512; Large-128 fused at 512, separate at 1024).
+    // Between, for d_model >= 1024 and 6..24 tokens, the role's serial tile
+    // chain (16 splits, one warp selecting 4 tokens in turn) outlasts the
+    // GEMM chain and the separate launch wins (Large-128 T=8: 67 vs 78 µs per
+    // block; tools/gpu_env_sweep.sh VAR=PGMOE_FUSED_ROUTE).
+    const bool mid_t_wide = c.d_model >= 1024 && T >= 6 && T <= 24;
     const bool fuse_route = !off && use_tc(m) && c.top_k == 1 && L == 1 && m->fuse_route &&
-                            fused_route_supported(c.num_experts) && (long long)T * 8 <= c.d_ff;
+                            fused_route_supported(c.num_experts) && (long long)T * 8 <= c.d_ff && !mid_t_wide;
     const float *cur = x_in;
     // Chained block launches (fused routing): each launch waits for its
     // predecessor's dense phase through a device counter instead of for its
@@ -703,6 +708,7 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
     if (cudaMalloc(&m->epoch, 256) != cudaSuccess || cudaMemset(m->epoch, 0, 256) != cudaSuccess)
         return fail(PGMOE_E_OOM);
     if (const char *e = getenv("PGMOE_CHAIN")) m->chain_launches = (e[0] == '1');
+    if (const char *e = getenv("PGMOE_FUSED_ROUTE")) m->fuse_route = (e[0] == '1');
     cudaEventCreate(&m->t0);
     m->stats.pinned_hbm_bytes = (int64_t)pinned;
     m->stats.slot_capacity_bytes = (int64_t)m->slot_capacity;
