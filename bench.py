@@ -63,10 +63,16 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs ~0.1-0.5 s for its first line: wait for it, so
+            # a timed region shorter than the sampling period still has the
+            # sample taken at its start
+            t_end = time.time() + 3.0
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
@@ -475,8 +481,10 @@ def run_reference(args, rank: int, world: int):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(s * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference RNG weights rounded to bf16, SURVEY §8(d) tokens)",
-        "config": {"workload": f"Switch-{args.preset} pre-gated decoder iteration (BASELINE configs[3]) on host cores",
-                   "preset": args.preset, "tokens_per_step": sample, "num_blocks": p["num_blocks"]},
+        "config": {"workload": workload_name(args.preset, getattr(args, "placement", "offloaded"),
+                                             getattr(args, "tokens", 256)),
+                   "preset": args.preset, "tokens_per_step": sample, "num_blocks": p["num_blocks"],
+                   "host": "reference CPU path on host cores, bounded sample per step"},
         "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": nth, "kind": "port",
                          "sample": f"{sample} tokens x 1 decoder iteration per step; oracle C restatement of "
                                    f"moesim (bit-exact vs the reference on its golden fixtures), {nth} threads"},
@@ -503,10 +511,15 @@ def main():
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    # stdout carries exactly the one JSON line: anything native libraries
+    # print there (NCCL's version banner) goes to stderr instead
+    json_out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     if args.impl == "reference":
         out = run_reference(args, rank, world)
         if out is not None:
-            print(json.dumps(out), flush=True)
+            print(json.dumps(out), file=json_out, flush=True)
         return
     mode = args.mode if args.mode != "auto" else ("ep" if world > 1 else "single")
     if world > 1 or mode == "ep":
@@ -517,7 +530,7 @@ def main():
         torch.distributed.init_process_group("nccl", rank=rank, world_size=world)
     out = run_ep(args, rank, world) if mode == "ep" else run_ours(args, rank, world)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=json_out, flush=True)
     if world > 1 or mode == "ep":
         import torch
         torch.distributed.destroy_process_group()
