@@ -448,6 +448,20 @@ def run_ep(args, rank: int, world: int):
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     e2e_s = float(t.item())
     nb = cfg.num_blocks
+    # roofline of the dominant kernel (the expert FFN launch, up + down over
+    # the rank's active local experts): one eager iteration with CUDA events
+    # on the launching stream around each launch
+    dec.use_graph, use_graph = False, dec.use_graph
+    dec.ffn_events = []
+    dec.decoder_iteration(x)
+    torch.cuda.synchronize()
+    evs, dec.ffn_events, dec.use_graph = dec.ffn_events, None, use_graph
+    d, f = cfg.d_model, cfg.d_ff
+    rows = world * T  # packed rows per launch (cap per peer)
+    alg = [int(n.item()) * 2 * d * f * 2 + rows * (d * 2 + f * 2 * 2 + d * 4) for _, _, n in evs]
+    us = [a.elapsed_time(b) * 1e3 for a, b, _ in evs]
+    hbm_peak, _, peak_kind = peaks()
+    achieved = sum(alg) / (sum(us) * 1e-6) / 1e9 if us and sum(us) > 0 else None
     out = {
         "metric": METRIC, "value": round(T * world / (ms * 1e-3), 3), "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
@@ -462,6 +476,11 @@ def run_ep(args, rank: int, world: int):
         "e2e": {"value": round(T * world / e2e_s, 3), "unit": "tokens/s",
                 "h2d_bytes_per_step": T * cfg.d_model * 4, "d2h_bytes_per_step": T * cfg.d_model * 4},
         "gpu_launches": int(launches), "clocks": clk, "setup_s": round(setup_s, 2),
+        "roofline": {"bound": "hbm", "kernel": "expert FFN launch (up + down, local experts), rank 0",
+                     "achieved": round(achieved, 1) if achieved else None, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(achieved / hbm_peak, 4) if achieved else None, "traffic": None,
+                     "peak_kind": peak_kind, "algorithmic_bytes_per_launch": int(sum(alg) / max(len(alg), 1)),
+                     "avg_launch_us": round(sum(us) / max(len(us), 1), 2)},
     }
     dec.close()
     return out

@@ -147,6 +147,9 @@ class EPDecoder:
         self.routing = DeviceRouting(max_tokens, config.num_experts, k)
         self._L = _lib.load()
         self.timing = {"exchange_s": 0.0, "blocks": 0}
+        # benchmark hook: (start, end, n_act tensor) CUDA events around each
+        # expert FFN launch of an eager iteration (None: off)
+        self.ffn_events = None
         import os
         self.use_graph = os.environ.get("PGMOE_EP_GRAPH", "1") != "0"
         self._graphs: dict = {}
@@ -190,8 +193,15 @@ class EPDecoder:
         eb, nl = ctypes.c_int32(), ctypes.c_int32()
         _lib.check(L.pgmoe_model_expert_records(self.model._h, b, ctypes.byref(base), ctypes.byref(stride),
                                                 ctypes.byref(eb), ctypes.byref(nl)))
+        ev = None
+        if self.ffn_events is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(torch.cuda.current_stream() if stream is None else stream)
         _lib.check(L.pgmoe_expert_forward_packed(_ptr(self.xb), P * cap, d, f, base, stride.value,
                                                  ctypes.byref(self.lr.c), _ptr(self.hb), _ptr(self.y_recv), s))
+        if ev is not None:
+            ev[1].record(torch.cuda.current_stream() if stream is None else stream)
+            self.ffn_events.append((ev[0], ev[1], self.lr.act_n[El:El + 1].clone()))
         ex.fixed(self.y_recv, self.back)                 # fp32 results back to their senders
         _lib.check(L.pgmoe_ep_unpermute_padded(_ptr(self.back), ctypes.byref(r_in.c), T, d, k, P, El, cap,
                                                _ptr(self.yw), s))
