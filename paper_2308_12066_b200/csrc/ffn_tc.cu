@@ -46,7 +46,7 @@ namespace pgmoe {
 
 namespace tc {
 
-constexpr int kThreads = 288;
+constexpr int kThreads = 352;  // 11 warps (3 per scheduler at most: 168 registers either way)
 constexpr int BM = 128;               // UMMA M (weight rows per tile)
 constexpr int BK = 64;                // bf16 elements per 128-byte swizzle row
 constexpr int kABytes = BM * BK * 2;  // 16 KB
@@ -88,7 +88,7 @@ struct Params {
     float *partial;
     long long partial_cap;  // floats
     unsigned long long *probe;  // debug stamps [grid][kProbeSlots] or null
-    FusedRoute route;           // the next block's routing, computed by warps 7-8 (resident)
+    FusedRoute route;           // the next block's routing, computed by warps 7-10 (resident)
     int max_inflight;           // weight stages the producer keeps in flight (<= STAGES)
     int max_split;              // cap on the split-K factor (0: cost model only)
     // Chained launches (resident decoder): instead of waiting for the previous
@@ -722,7 +722,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             if (p.probe) p.probe[(size_t)blockIdx.x * kProbeSlots + 16] = cyc_gate;
         }
     } else if (warp >= 7) {
-        // ================= routing role (warps 7-8) ========================
+        // ================= routing role (warps 7-10) =======================
         // The next block's pre-gated routing (route_common.cuh), overlapped
         // with this block's expert GEMMs; once it is complete the next launch
         // (which schedules from it) may start.

@@ -104,8 +104,9 @@ __device__ __noinline__ double serial_logit(const float *x, const GT *G, int d, 
 // Work: units (token tile of kRouterTok tokens) x (K split) spread over the
 // grid; the last split of a tile selects (one warp per token); the last
 // tile builds histogram, scan, stable permutation and active list.
-constexpr int kRouterThreads = 64;
-constexpr int kRouterWarps = 2;
+constexpr int kRouterThreads = 128;
+constexpr int kRouterWarps = 4;
+constexpr int kRouterLogitThreads = 64;  // threads of the partial-logit layout (the others load and reduce)
 constexpr int kRouterTok = 8;
 constexpr int kRouterMaxKn = 256;  // gate rows per split (x slice in shared memory)
 // route workspace: [counter @0 | done @64 | tile counters @256 (8192 ints) | partials]
@@ -170,7 +171,7 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs, 
     const int k0 = (int)((long)d * split / r.splits), k1 = (int)((long)d * (split + 1) / r.splits);
     const int kn = k1 - k0;
     constexpr int CG = 8 * NJ;                 // E / 4 column groups
-    constexpr int TG = kRouterThreads / CG;    // token (or row) groups
+    constexpr int TG = kRouterLogitThreads / CG;     // token (or row) groups
     const bool rowsplit = TG > 1 && ntok <= NJ;
     const int tslots = rowsplit ? NJ : kRouterTok;
     for (int i0 = rt; i0 < tslots * kn; i0 += 8 * kRouterThreads) {  // 8 loads in flight
@@ -193,10 +194,11 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs, 
         if (lane == 0) r.pxsum[(size_t)split * T + t0 + t] = sx;
     }
     if (rt == 0) probe(pr, blockIdx.x, 40);  // x slice in shared memory
-    const int cg = rt % CG, tg = rt / CG;
+    const bool lt = rt < kRouterLogitThreads;  // the others wait at the next barrier
+    const int cg = rt % CG, tg = (rt % kRouterLogitThreads) / CG;
     const int tbase = rowsplit ? 0 : tg * NJ;
     const int rstart = rowsplit ? tg : 0, rstep = rowsplit ? TG : 1;
-    const int nrows = rowsplit ? (kn - tg + TG - 1) / TG : kn;
+    const int nrows = !lt ? 0 : rowsplit ? (kn - tg + TG - 1) / TG : kn;
     double acc[NJ][4];
     float cm[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -237,23 +239,25 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs, 
 #pragma unroll
         for (int tt = 0; tt < NJ; ++tt) {
             const int t = tbase + tt;
-            if (t < ntok)
+            if (lt && t < ntok)
 #pragma unroll
                 for (int v = 0; v < 4; ++v) r.plogit[((size_t)split * T + t0 + t) * E + cg * 4 + v] = acc[tt][v];
         }
-        if (tg == 0)
+        if (lt && tg == 0)
 #pragma unroll
             for (int v = 0; v < 4; ++v) r.pcmax[((size_t)tile * r.splits + split) * E + cg * 4 + v] = cm[v];
     } else {
         // [TG][NJ][E] partial sums and [TG][E] column maxima after the x slice
         double *red = reinterpret_cast<double *>(xs + ((tslots * kn + 1) & ~1));
         float *cmr = reinterpret_cast<float *>(red + TG * NJ * E);
+        if (lt) {
 #pragma unroll
-        for (int tt = 0; tt < NJ; ++tt)
+            for (int tt = 0; tt < NJ; ++tt)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) red[(tg * NJ + tt) * E + cg * 4 + v] = acc[tt][v];
+                for (int v = 0; v < 4; ++v) red[(tg * NJ + tt) * E + cg * 4 + v] = acc[tt][v];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) cmr[tg * E + cg * 4 + v] = cm[v];
+            for (int v = 0; v < 4; ++v) cmr[tg * E + cg * 4 + v] = cm[v];
+        }
         router_sync();
         for (int q = rt; q < ntok * E; q += kRouterThreads) {
             const int tt = q / E, j = q - tt * E;
@@ -453,7 +457,7 @@ __device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int
 }
 
 // Histogram, exclusive scan, stable permutation, active list (permute_all
-// of route.cu with the router's two warps).  sm: >= 3 * E ints.
+// of route.cu with the router's warps).  sm: >= (kRouterWarps + 1) * E ints.
 static __device__ __noinline__ void router_permute(const FusedRoute &r, int rt, int *sm, const int *ids_src,
                                                    const float *w_src) {
     const int E = r.E, k = r.k, lane = rt & 31, w = rt >> 5;
