@@ -1129,9 +1129,9 @@ int block_tc(const float *x, int T, int d, int f, int k, const void *experts, si
         // The routing role's loads queue behind the weight stream; when its
         // work rivals the GEMMs' (small experts, many tokens) a shallower
         // weight pipeline (lower queueing delay) finishes the block sooner
-        // (tools/gpu_env_sweep.sh VAR=PGMOE_INFLIGHT: Base-64 T=32..256 best
-        // at 6-7 stages, -1..6 % vs 8; Large-128 needs 8).
-        if (route->E <= 64 && n >= 16 && (size_t)d * f <= (size_t)768 * 3072) p.max_inflight = 6;
+        // (tools/gpu_retune.sh VAR=PGMOE_INFLIGHT: Base-64 T=16..32 best at
+        // 6 stages, -1..3 % vs 8; from T=64 on, and for Large-128, 8 wins).
+        if (route->E <= 64 && n >= 16 && n < 64 && (size_t)d * f <= (size_t)768 * 3072) p.max_inflight = 6;
     }
     int parity = 0;
     if (chain && chain->epoch) {

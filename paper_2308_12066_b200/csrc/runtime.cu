@@ -131,6 +131,7 @@ struct pgmoe_model {
     int64_t fused_blocks = 0;  // blocks whose dense layer ran inside the expert launch
     int64_t fused_routes = 0;  // pre-gates computed inside the block launch
     bool fuse_route = true;    // resident: route inside the block launch (pgmoe_model_set_fused_route)
+    long long fuse_max_t = 0;  // largest T routed inside the block launch (0: d_ff / 8; PGMOE_FUSE_MAX_T)
     // fused: launches chained on the previous dense phase instead of its
     // completion (PGMOE_CHAIN=1).  Measured: saves the ~4.5 us completion
     // latency but pays ~3-4 us of atomic + fence + poll, net -1 % at T=256
@@ -428,17 +429,14 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
     // Resident top-1 blocks compute their pre-gate inside the block launch
     // (it depends only on the block input); offloaded blocks keep the
     // separate K1 launch because the host needs the active list at once.
-    // The routing role (2 warps per CTA) keeps up with the expert GEMMs while
+    // The routing role (4 warps per CTA) keeps up with the expert GEMMs while
     // its work (~T·d·E fp64 FMAs + the permutation) is small next to theirs
-    // (~E·d·f weight bytes): measured crossover T ≈ f/8 (Base-64 better fused
-    // at T=256, separate at 512; Large-128 fused at 512, separate at 1024).
-    // Between, for d_model >= 1024 and 6..24 tokens, the role's serial tile
-    // chain (16 splits, one warp selecting 4 tokens in turn) outlasts the
-    // GEMM chain and the separate launch wins (Large-128 T=8: 67 vs 78 µs per
-    // block; tools/gpu_env_sweep.sh VAR=PGMOE_FUSED_ROUTE).
-    const bool mid_t_wide = c.d_model >= 1024 && T >= 6 && T <= 24;
+    // (~E·d·f weight bytes): measured crossover T ≈ f/8 (Base-64 fused
+    // better through T=384, separate at 512; Large-128 fused through 768,
+    // even at 1024; tools/gpu_env_sweep.sh VAR=PGMOE_FUSE_MAX_T).
     const bool fuse_route = !off && use_tc(m) && c.top_k == 1 && L == 1 && m->fuse_route &&
-                            fused_route_supported(c.num_experts) && (long long)T * 8 <= c.d_ff && !mid_t_wide;
+                            fused_route_supported(c.num_experts) &&
+                            (long long)T <= (m->fuse_max_t > 0 ? m->fuse_max_t : c.d_ff / 8);
     const float *cur = x_in;
     // Chained block launches (fused routing): each launch waits for its
     // predecessor's dense phase through a device counter instead of for its
@@ -709,6 +707,7 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
         return fail(PGMOE_E_OOM);
     if (const char *e = getenv("PGMOE_CHAIN")) m->chain_launches = (e[0] == '1');
     if (const char *e = getenv("PGMOE_FUSED_ROUTE")) m->fuse_route = (e[0] == '1');
+    if (const char *e = getenv("PGMOE_FUSE_MAX_T")) m->fuse_max_t = atoll(e);
     cudaEventCreate(&m->t0);
     m->stats.pinned_hbm_bytes = (int64_t)pinned;
     m->stats.slot_capacity_bytes = (int64_t)m->slot_capacity;
