@@ -82,6 +82,28 @@ template <> struct Vec<float> {
     __device__ __forceinline__ static double one(const float *p) { return __ldg(p); }
 };
 template <typename GT> __device__ __forceinline__ double gval(const GT *G, size_t i) { return Vec<GT>::one(G + i); }
+// Two adjacent experts per load (the routing role's partial logits: 128
+// threads x 2 experts cover a token group, so each warp's dependent FP64
+// chain per gate row is half as long as with 4 experts per thread).
+template <typename GT> struct Vec2;
+template <> struct Vec2<uint16_t> {
+    using Raw = uint32_t;
+    __device__ __forceinline__ static Raw ld(const uint16_t *p) { return __ldg(reinterpret_cast<const uint32_t *>(p)); }
+    __device__ __forceinline__ static void cvt(Raw v, double (&d)[2], float (&a)[2]) {
+        const float f[2] = {__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u)};
+        d[0] = f[0]; d[1] = f[1];
+        a[0] = fabsf(f[0]); a[1] = fabsf(f[1]);
+    }
+};
+template <> struct Vec2<float> {
+    using Raw = float2;
+    __device__ __forceinline__ static Raw ld(const float *p) { return __ldg(reinterpret_cast<const float2 *>(p)); }
+    __device__ __forceinline__ static void cvt(Raw v, double (&d)[2], float (&a)[2]) {
+        d[0] = v.x; d[1] = v.y;
+        a[0] = fabsf(v.x); a[1] = fabsf(v.y);
+    }
+};
+
 
 // Serial fp64 logit in the reference order (linalg.py:35-37): out += x_i*G_ij.
 // Not inlined: the rare uncertified path would otherwise put NJ unrolled
@@ -106,7 +128,6 @@ __device__ __noinline__ double serial_logit(const float *x, const GT *G, int d, 
 // tile builds histogram, scan, stable permutation and active list.
 constexpr int kRouterThreads = 128;
 constexpr int kRouterWarps = 4;
-constexpr int kRouterLogitThreads = 64;  // threads of the partial-logit layout (the others load and reduce)
 constexpr int kRouterTok = 8;
 constexpr int kRouterMaxKn = 256;  // gate rows per split (x slice in shared memory)
 // route workspace: [counter @0 | done @64 | tile counters @256 (8192 ints) | partials]
@@ -155,7 +176,8 @@ inline size_t fused_route_ws_bytes(int T, int d, int E, int grid) {
 __device__ __forceinline__ void router_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kRouterThreads)); }
 
 // Partial fp64 logits of one (tile, split) unit.  NJ = E / 32: each thread
-// owns 4 adjacent experts x NJ tokens (64 threads cover 8 tokens x E).  When
+// owns 2 adjacent experts x NJ tokens (128 threads cover 8 tokens x E; the
+// loop is latency-bound per warp, so more, shorter chains finish sooner).  When
 // the tile holds <= NJ tokens (small batches) the token groups take row
 // slices instead and are summed in shared memory in a fixed order, so each
 // thread has a quarter (E=64) or half (E=128) of the rows to load: at small T
@@ -170,8 +192,9 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs, 
     const int t0 = tile * kRouterTok, ntok = min(kRouterTok, T - t0);
     const int k0 = (int)((long)d * split / r.splits), k1 = (int)((long)d * (split + 1) / r.splits);
     const int kn = k1 - k0;
-    constexpr int CG = 8 * NJ;                 // E / 4 column groups
-    constexpr int TG = kRouterLogitThreads / CG;     // token (or row) groups
+    constexpr int CG = 16 * NJ;                // E / 2 column groups (2 experts per thread)
+    constexpr int TG = kRouterThreads / CG;    // token (or row) groups: TG x NJ = 8 tokens
+    static_assert(TG * NJ == kRouterTok, "the role's threads cover a token tile");
     const bool rowsplit = TG > 1 && ntok <= NJ;
     const int tslots = rowsplit ? NJ : kRouterTok;
     for (int i0 = rt; i0 < tslots * kn; i0 += 8 * kRouterThreads) {  // 8 loads in flight
@@ -194,42 +217,41 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs, 
         if (lane == 0) r.pxsum[(size_t)split * T + t0 + t] = sx;
     }
     if (rt == 0) probe(pr, blockIdx.x, 40);  // x slice in shared memory
-    const bool lt = rt < kRouterLogitThreads;  // the others wait at the next barrier
-    const int cg = rt % CG, tg = (rt % kRouterLogitThreads) / CG;
+    const int cg = rt % CG, tg = rt / CG;
     const int tbase = rowsplit ? 0 : tg * NJ;
     const int rstart = rowsplit ? tg : 0, rstep = rowsplit ? TG : 1;
-    const int nrows = !lt ? 0 : rowsplit ? (kn - tg + TG - 1) / TG : kn;
-    double acc[NJ][4];
-    float cm[4] = {0.f, 0.f, 0.f, 0.f};
+    const int nrows = rowsplit ? (kn - tg + TG - 1) / TG : kn;
+    double acc[NJ][2];
+    float cm[2] = {0.f, 0.f};
 #pragma unroll
     for (int tt = 0; tt < NJ; ++tt)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[tt][v] = 0.0;
-    const GT *G = static_cast<const GT *>(r.G) + (size_t)k0 * E + cg * 4;
-    // 16 gate rows in flight per thread (raw, converted on use): this role
+        for (int v = 0; v < 2; ++v) acc[tt][v] = 0.0;
+    const GT *G = static_cast<const GT *>(r.G) + (size_t)k0 * E + cg * 2;
+    // 32 gate rows in flight per thread (raw, converted on use): this role
     // runs next to the expert GEMMs' weight stream, so every load sees the
     // loaded memory latency (in-flight bytes / bandwidth)
-    using Raw = typename Vec<GT>::Raw;
-    constexpr int RB = (sizeof(Raw) <= 8 ? 16 : 8) * (NJ <= 2 ? 2 : 1);  // E=64: small accumulators, 32 rows in flight
+    using Raw = typename Vec2<GT>::Raw;
+    constexpr int RB = 32;
     for (int n0 = 0; n0 < nrows; n0 += RB) {
         Raw raw[RB];
 #pragma unroll
         for (int b = 0; b < RB; ++b)
-            raw[b] = Vec<GT>::ld(G + (size_t)(rstart + min(n0 + b, nrows - 1) * rstep) * E);
+            raw[b] = Vec2<GT>::ld(G + (size_t)(rstart + min(n0 + b, nrows - 1) * rstep) * E);
 #pragma unroll
         for (int b = 0; b < RB; ++b) {
             if (n0 + b < nrows) {
                 const int i = rstart + (n0 + b) * rstep;
-                double g[4];
-                float a[4];
-                Vec<GT>::cvt(raw[b], g, a);
+                double g[2];
+                float a[2];
+                Vec2<GT>::cvt(raw[b], g, a);
 #pragma unroll
-                for (int v = 0; v < 4; ++v) cm[v] = fmaxf(cm[v], a[v]);
+                for (int v = 0; v < 2; ++v) cm[v] = fmaxf(cm[v], a[v]);
 #pragma unroll
                 for (int tt = 0; tt < NJ; ++tt) {
                     const double xv = xs[(tbase + tt) * kn + i];
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) acc[tt][v] = fma(xv, g[v], acc[tt][v]);  // exact product, one rounding
+                    for (int v = 0; v < 2; ++v) acc[tt][v] = fma(xv, g[v], acc[tt][v]);  // exact product, one rounding
                 }
             }
         }
@@ -239,25 +261,23 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs, 
 #pragma unroll
         for (int tt = 0; tt < NJ; ++tt) {
             const int t = tbase + tt;
-            if (lt && t < ntok)
+            if (t < ntok)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) r.plogit[((size_t)split * T + t0 + t) * E + cg * 4 + v] = acc[tt][v];
+                for (int v = 0; v < 2; ++v) r.plogit[((size_t)split * T + t0 + t) * E + cg * 2 + v] = acc[tt][v];
         }
-        if (lt && tg == 0)
+        if (tg == 0)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) r.pcmax[((size_t)tile * r.splits + split) * E + cg * 4 + v] = cm[v];
+            for (int v = 0; v < 2; ++v) r.pcmax[((size_t)tile * r.splits + split) * E + cg * 2 + v] = cm[v];
     } else {
         // [TG][NJ][E] partial sums and [TG][E] column maxima after the x slice
         double *red = reinterpret_cast<double *>(xs + ((tslots * kn + 1) & ~1));
         float *cmr = reinterpret_cast<float *>(red + TG * NJ * E);
-        if (lt) {
 #pragma unroll
-            for (int tt = 0; tt < NJ; ++tt)
+        for (int tt = 0; tt < NJ; ++tt)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) red[(tg * NJ + tt) * E + cg * 4 + v] = acc[tt][v];
+            for (int v = 0; v < 2; ++v) red[(tg * NJ + tt) * E + cg * 2 + v] = acc[tt][v];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) cmr[tg * E + cg * 4 + v] = cm[v];
-        }
+        for (int v = 0; v < 2; ++v) cmr[tg * E + cg * 2 + v] = cm[v];
         router_sync();
         for (int q = rt; q < ntok * E; q += kRouterThreads) {
             const int tt = q / E, j = q - tt * E;
