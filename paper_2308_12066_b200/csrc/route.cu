@@ -336,13 +336,16 @@ route_kernel(const RouteParams p_in) {
     const int j0 = cg * V;
     constexpr int U = 4;  // gate rows in flight per thread
     if (rg < RG && cg < CG) {
-        for (int i = rg; i < kn; i += RG * U) {
-            double gd[U][V];
-            float ga[U][V];
+        // U rows per batch with no per-row guard (a guard per row makes each
+        // row its own basic block and serialises the load -> convert -> FMA
+        // chains); the tail rows one at a time, in the same order
+        auto rows = [&](auto nu, int i) {
+            constexpr int NU = decltype(nu)::value;
+            double gd[NU][V];
+            float ga[NU][V];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int ii = i + u * RG;
-                const GT *row = G + (size_t)(k0 + min(ii, kn - 1)) * E;
+            for (int u = 0; u < NU; ++u) {
+                const GT *row = G + (size_t)(k0 + i + u * RG) * E;
                 if (VECLOAD) {
                     Vec<GT>::load(row + j0, gd[u], ga[u]);
                 } else {
@@ -354,20 +357,21 @@ route_kernel(const RouteParams p_in) {
                 }
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
+            for (int u = 0; u < NU; ++u) {
                 const int ii = i + u * RG;
-                if (ii < kn) {
 #pragma unroll
-                    for (int v = 0; v < V; ++v) cmax[v] = fmaxf(cmax[v], ga[u][v]);
+                for (int v = 0; v < V; ++v) cmax[v] = fmaxf(cmax[v], ga[u][v]);
 #pragma unroll
-                    for (int t = 0; t < TOK; ++t) {
-                        const double xv = xd[t * kn + ii];
+                for (int t = 0; t < TOK; ++t) {
+                    const double xv = xd[t * kn + ii];
 #pragma unroll
-                        for (int v = 0; v < V; ++v) acc[t][v] = fma(xv, gd[u][v], acc[t][v]);
-                    }
+                    for (int v = 0; v < V; ++v) acc[t][v] = fma(xv, gd[u][v], acc[t][v]);
                 }
             }
-        }
+        };
+        int i = rg;
+        for (; i + (U - 1) * RG < kn; i += RG * U) rows(std::integral_constant<int, U>{}, i);
+        for (; i < kn; i += RG) rows(std::integral_constant<int, 1>{}, i);
     }
     __syncthreads();  // x tile no longer needed: reuse smem for the reduction
     if (rg < RG && cg < CG) {
