@@ -1126,12 +1126,9 @@ int block_tc(const float *x, int T, int d, int f, int k, const void *experts, si
         PG_REQUIRE(dense_w != nullptr && fused_route_supported(route->E), PGMOE_E_CONFIG,
                    "fused routing needs the dense phase and E in {64, 128, 256}");
         p.route = *route;
-        // The routing role's loads queue behind the weight stream; when its
-        // work rivals the GEMMs' (small experts, many tokens) a shallower
-        // weight pipeline (lower queueing delay) finishes the block sooner
-        // (tools/gpu_retune.sh VAR=PGMOE_INFLIGHT: Base-64 T=16..32 best at
-        // 6 stages, -1..3 % vs 8; from T=64 on, and for Large-128, 8 wins).
-        if (route->E <= 64 && n >= 16 && n < 64 && (size_t)d * f <= (size_t)768 * 3072) p.max_inflight = 6;
+        // (In-flight stage limits for the routing role's sake were measured
+        // and dropped once the role ran on 4 warps: within 1 % at every T,
+        // tools/gpu_env_sweep.sh VAR=PGMOE_INFLIGHT.)
     }
     int parity = 0;
     if (chain && chain->epoch) {
