@@ -324,14 +324,14 @@ __device__ __forceinline__ TileSums tile_sums_layout(float *xs, int E, int ch) {
 static __device__ __noinline__ void router_reduce_tile(const FusedRoute &r, int tile, int t0, int ntok, int rt, const TileSums &ts,
                                                        unsigned long long *pr) {
     const int E = r.E, T = r.T, S = r.splits;
-    const int lane = rt & 31, w = rt >> 5;
-    for (int t = w; t < ntok; t += kRouterWarps) {
-        double sx = 0.0;
-        for (int z = lane; z < S; z += 32) sx += __ldcg(r.pxsum + (size_t)z * T + t0 + t);
-        sx = warp_sumd(sx);
-        if (lane == 0) ts.sxs[t] = sx;
-    }
-    if (rt == 0 && t0 == tile * kRouterTok) probe(pr, blockIdx.x, 35);  // sum |x| loaded
+    // sum |x| per token: one (token, split) per lane, 16 lanes per token
+    // (4 warps x 2 tokens = the tile), summed by a fixed butterfly; issued
+    // before the first batch of partials so both share one load round
+    static_assert(kRouterThreads >= 16 * kRouterTok, "16 lanes per token");
+    const int st = rt >> 4, sz = rt & 15;
+    double sxv = 0.0;
+    if (st < ntok)
+        for (int z = sz; z < S; z += 16) sxv += __ldcg(r.pxsum + (size_t)z * T + t0 + st);
     const int n = ntok * E;
     for (int q0 = rt; q0 < n; q0 += 2 * kRouterThreads) {
         double pl[2][16];
@@ -367,6 +367,10 @@ static __device__ __noinline__ void router_reduce_tile(const FusedRoute &r, int 
             ts.cms[q] = cm;
         }
     }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) sxv += __shfl_xor_sync(0xffffffffu, sxv, o);
+    if (sz == 0 && st < ntok) ts.sxs[st] = sxv;
+    if (rt == 0 && t0 == tile * kRouterTok) probe(pr, blockIdx.x, 35);  // sums in shared memory
     router_sync();
 }
 
