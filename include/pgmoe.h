@@ -130,20 +130,26 @@ PGMOE_API int pgmoe_ep_local_routing(const int32_t *recv_cnt, int32_t P, int32_t
                                      pgmoe_stream_t stream);
 
 /* Fixed-size (padded) expert-parallel exchange: no host round trip for the
- * all-to-all split sizes.  Rank p owns experts [p*El, (p+1)*El) and gets a
- * slot of `cap` (>= T*k) rows from every rank.
+ * all-to-all split sizes, and ONE all-to-all for rows and counts.  Rank p
+ * owns experts [p*El, (p+1)*El); every rank sends every peer a slot of
+ * slot_rows(cap, El, d) rows: cap (>= T*k) routed rows, then header rows
+ * carrying the sender's per-expert counts for that peer (int32 [El]).
+ *   slot_rows: cap + ceil(4 El / 2 d);
  *   pack_send: send[p][i] = bf16(x[perm[r] / k]), r = off[p*El] + i — the
- *     rows the tcgen05 FFN consumes in bf16, so exact at half the bytes;
- *   local_routing_padded: receiver routing over the padded rows (source p's
- *     rows start at p*cap);
+ *     rows the tcgen05 FFN consumes in bf16, so exact at half the bytes —
+ *     and send[p][cap..] = hist[p*El .. (p+1)*El);
+ *   local_routing_padded: receiver routing over the padded rows, counts read
+ *     from the received headers (source p's rows start at p * slot_rows);
  *   pack_recv: the received rows in local-expert order (the FFN operand),
  *     count read on the device (off[El]);
  *   expert_forward_packed: expert FFN on that operand, y rows scattered back
  *     to their padded receive positions;
- *   unpermute_padded: yw[perm[r]] = w_perm[r] * back[p][r - off[p*El]]. */
+ *   unpermute_padded: yw[perm[r]] = w_perm[r] * back[p][r - off[p*El]]
+ *     (back in the same slot layout). */
 PGMOE_API int pgmoe_ep_pack_send(const float *x, const pgmoe_routing *r, int32_t T, int32_t d, int32_t k, int32_t P,
                                  int32_t El, int32_t cap, uint16_t *send, pgmoe_stream_t stream);
-PGMOE_API int pgmoe_ep_local_routing_padded(const int32_t *recv_cnt, int32_t P, int32_t El, int32_t cap,
+PGMOE_API int32_t pgmoe_ep_slot_rows(int32_t cap, int32_t El, int32_t d);
+PGMOE_API int pgmoe_ep_local_routing_padded(const uint16_t *recv, int32_t P, int32_t El, int32_t cap, int32_t d,
                                             const pgmoe_routing *out, pgmoe_stream_t stream);
 PGMOE_API int pgmoe_ep_pack_recv(const uint16_t *recv, const pgmoe_routing *local, int32_t El, int32_t n_max,
                                  int32_t d, uint16_t *xb, pgmoe_stream_t stream);

@@ -69,7 +69,7 @@ EXPORTS = (
     "pgmoe_model_load_pgmoe1", "pgmoe_model_save_pgmoe1", "pgmoe_model_set_strategy", "pgmoe_model_set_cache",
     "pgmoe_cache_replay", "pgmoe_debug_set_probe", "pgmoe_model_set_fused_route",
     "pgmoe_ep_pack_send", "pgmoe_ep_local_routing_padded", "pgmoe_ep_pack_recv", "pgmoe_expert_forward_packed",
-    "pgmoe_ep_unpermute_padded",
+    "pgmoe_ep_unpermute_padded", "pgmoe_ep_slot_rows",
 )
 
 _lib = None
@@ -126,7 +126,8 @@ def load():
         "pgmoe_debug_set_probe": (i32, [i32, vp, i64]),
         "pgmoe_model_set_fused_route": (i32, [vp, i32]),
         "pgmoe_ep_pack_send": (i32, [vp, P(Routing), i32, i32, i32, i32, i32, i32, vp, vp]),
-        "pgmoe_ep_local_routing_padded": (i32, [vp, i32, i32, i32, P(Routing), vp]),
+        "pgmoe_ep_local_routing_padded": (i32, [vp, i32, i32, i32, i32, P(Routing), vp]),
+        "pgmoe_ep_slot_rows": (i32, [i32, i32, i32]),
         "pgmoe_ep_pack_recv": (i32, [vp, P(Routing), i32, i32, i32, vp, vp]),
         "pgmoe_expert_forward_packed": (i32, [vp, i32, i32, i32, vp, sz, P(Routing), vp, vp, vp]),
         "pgmoe_ep_unpermute_padded": (i32, [vp, P(Routing), i32, i32, i32, i32, i32, i32, vp, vp]),

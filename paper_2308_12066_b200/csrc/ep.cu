@@ -44,7 +44,8 @@ __global__ void unpermute_kernel(const float *__restrict__ back, const int *__re
 // produce for the concatenated batch.  cnt: [P][El].  One CTA.
 // src_stride > 0: source p's rows start at row p * src_stride (fixed-size,
 // padded exchange) instead of right after source p-1's.
-__global__ void ep_local_routing_kernel(const int *__restrict__ cnt, int P, int El, int src_stride,
+// cnt_stride: ints between sources' count rows (El when contiguous).
+__global__ void ep_local_routing_kernel(const int *__restrict__ cnt, int cnt_stride, int P, int El, int src_stride,
                                         pgmoe_routing r) {
     extern __shared__ int sm[];
     int *src_base = sm;          // [P] first received row of source p
@@ -57,14 +58,14 @@ __global__ void ep_local_routing_kernel(const int *__restrict__ cnt, int P, int 
             int o = 0;
             for (int e = 0; e < El; ++e) {
                 src_off[p * El + e] = o;
-                o += cnt[p * El + e];
+                o += cnt[p * cnt_stride + e];
             }
             run += o;
         }
         int off = 0, nact = 0;
         for (int e = 0; e < El; ++e) {
             int h = 0;
-            for (int p = 0; p < P; ++p) h += cnt[p * El + e];
+            for (int p = 0; p < P; ++p) h += cnt[p * cnt_stride + e];
             r.hist[e] = h;
             r.off[e] = off;
             if (h > 0) r.act[nact++] = e;
@@ -79,7 +80,7 @@ __global__ void ep_local_routing_kernel(const int *__restrict__ cnt, int P, int 
     for (int e = warp; e < El; e += blockDim.x >> 5) {
         int pos = r.off[e];
         for (int p = 0; p < P; ++p) {
-            const int c = cnt[p * El + e];
+            const int c = cnt[p * cnt_stride + e];
             const int base = src_base[p] + src_off[p * El + e];
             for (int i = lane; i < c; i += 32) {
                 r.perm[pos + i] = base + i;
@@ -107,17 +108,27 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
            ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
 }
 
+// Each peer's slot is `slot` rows: cap routed rows, then header rows whose
+// bytes carry this rank's per-expert counts for that peer (int32 [El]), so
+// the counts travel in the same all-to-all as the rows.
+__host__ __device__ inline int ep_header_rows(int El, int d) { return (El * 4 + 2 * d - 1) / (2 * d); }
+
 // send[p][i] = bf16(x[perm[r] / k]) for r = off[p*El] + i (the rows the
-// FFN consumes in bf16 anyway, so the exchange is exact and half the bytes)
+// FFN consumes in bf16 anyway, so the exchange is exact and half the bytes);
+// send[p][cap..] = hist[p*El .. (p+1)*El) as int32
 __global__ void ep_pack_send_kernel(const float *__restrict__ x, const int *__restrict__ perm,
-                                    const int *__restrict__ off, int n, int d, int k, int P, int El, int cap,
-                                    uint16_t *__restrict__ send) {
+                                    const int *__restrict__ off, const int *__restrict__ hist, int n, int d, int k,
+                                    int P, int El, int cap, int slot, uint16_t *__restrict__ send) {
     const int vec = d / 8;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P * El; i += gridDim.x * blockDim.x) {
+        const int p = i / El, e = i - p * El;
+        reinterpret_cast<int *>(send + ((size_t)p * slot + cap) * d)[e] = __ldg(hist + i);
+    }
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * vec;
          i += (long long)gridDim.x * blockDim.x) {
         const int r = (int)(i / vec), c = (int)(i - (long long)r * vec);
         const int p = owner_of(off, El, P, r);
-        const int slot = r - __ldg(off + p * El);
+        const int row = r - __ldg(off + p * El);
         const float4 *src = reinterpret_cast<const float4 *>(x + (size_t)(__ldg(perm + r) / k) * d) + 2 * c;
         const float4 a = __ldg(src), b = __ldg(src + 1);
         uint4 o;
@@ -125,7 +136,7 @@ __global__ void ep_pack_send_kernel(const float *__restrict__ x, const int *__re
         o.y = pack_bf16x2(a.z, a.w);
         o.z = pack_bf16x2(b.x, b.y);
         o.w = pack_bf16x2(b.z, b.w);
-        reinterpret_cast<uint4 *>(send)[((size_t)p * cap + slot) * vec + c] = o;
+        reinterpret_cast<uint4 *>(send)[((size_t)p * slot + row) * vec + c] = o;
     }
 }
 
@@ -146,13 +157,13 @@ __global__ void ep_pack_recv_kernel(const uint16_t *__restrict__ recv, const int
 // yw[perm[r]] = w_perm[r] * back[p][r - off[p*El]] (the combine weight)
 __global__ void ep_unpermute_padded_kernel(const float *__restrict__ back, const int *__restrict__ perm,
                                            const float *__restrict__ w_perm, const int *__restrict__ off, int n,
-                                           int d, int P, int El, int cap, float *__restrict__ yw) {
+                                           int d, int P, int El, int slot, float *__restrict__ yw) {
     const int vec = d / 4;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * vec;
          i += (long long)gridDim.x * blockDim.x) {
         const int r = (int)(i / vec), c = (int)(i - (long long)r * vec);
         const int p = owner_of(off, El, P, r);
-        const size_t row = (size_t)p * cap + (r - __ldg(off + p * El));
+        const size_t row = (size_t)p * slot + (r - __ldg(off + p * El));
         const float w = __ldg(w_perm + r);
         float4 v = __ldg(reinterpret_cast<const float4 *>(back) + row * vec + c);
         v.x *= w; v.y *= w; v.z *= w; v.w *= w;
@@ -170,10 +181,10 @@ extern "C" int pgmoe_ep_pack_send(const float *x, const pgmoe_routing *r, int32_
                                   int32_t El, int32_t cap, uint16_t *send, pgmoe_stream_t stream) {
     PG_REQUIRE(d % 8 == 0, PGMOE_E_SHAPE, "ep_pack_send needs d %% 8 == 0");
     PG_REQUIRE(cap >= T * k, PGMOE_E_CONFIG, "ep slot of %d rows cannot hold %d routed entries", cap, T * k);
-    const int n = T * k;
-    if (n == 0) return PGMOE_OK;
-    ep_pack_send_kernel<<<grid_for((long long)n * d / 8), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-        x, r->perm, r->off, n, d, k, P, El, cap, send);
+    const int n = T * k;  // n == 0 still sends the (zero) counts
+    ep_pack_send_kernel<<<grid_for(std::max((long long)n * d / 8, (long long)P * El)), 256, 0,
+                          reinterpret_cast<cudaStream_t>(stream)>>>(x, r->perm, r->off, r->hist, n, d, k, P, El, cap,
+                                                                    cap + ep_header_rows(El, d), send);
     PG_CUDA(cudaGetLastError());
     count_launch();
     return PGMOE_OK;
@@ -196,18 +207,25 @@ extern "C" int pgmoe_ep_unpermute_padded(const float *back, const pgmoe_routing 
     const int n = T * k;
     if (n == 0) return PGMOE_OK;
     ep_unpermute_padded_kernel<<<grid_for((long long)n * d / 4), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-        back, r->perm, r->w_perm, r->off, n, d, P, El, cap, yw);
+        back, r->perm, r->w_perm, r->off, n, d, P, El, cap + ep_header_rows(El, d), yw);
     PG_CUDA(cudaGetLastError());
     count_launch();
     return PGMOE_OK;
 }
 
-extern "C" int pgmoe_ep_local_routing_padded(const int32_t *recv_cnt, int32_t P, int32_t El, int32_t cap,
+extern "C" int32_t pgmoe_ep_slot_rows(int32_t cap, int32_t El, int32_t d) { return cap + ep_header_rows(El, d); }
+
+extern "C" int pgmoe_ep_local_routing_padded(const uint16_t *recv, int32_t P, int32_t El, int32_t cap, int32_t d,
                                              const pgmoe_routing *out, pgmoe_stream_t stream) {
-    PG_REQUIRE(P >= 1 && El >= 1 && cap >= 1, PGMOE_E_CONFIG, "bad EP shape P=%d El=%d cap=%d", P, El, cap);
+    PG_REQUIRE(P >= 1 && El >= 1 && cap >= 1 && d >= 1, PGMOE_E_CONFIG, "bad EP shape P=%d El=%d cap=%d", P, El, cap);
     const size_t smem = (size_t)(P + P * El) * 4;
     PG_REQUIRE(smem <= 48 * 1024, PGMOE_E_CONFIG, "EP routing table too large");
-    ep_local_routing_kernel<<<1, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(recv_cnt, P, El, cap, *out);
+    const int slot = cap + ep_header_rows(El, d);
+    // counts of source p: the header of its slot (slot * d bf16 = slot * d / 2 ints apart)
+    const int *cnt = reinterpret_cast<const int *>(recv + (size_t)cap * d);
+    PG_REQUIRE(d % 2 == 0, PGMOE_E_SHAPE, "ep header needs an even d");
+    ep_local_routing_kernel<<<1, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(cnt, slot * d / 2, P, El, slot,
+                                                                                      *out);
     PG_CUDA(cudaGetLastError());
     count_launch();
     return PGMOE_OK;
@@ -242,7 +260,7 @@ extern "C" int pgmoe_ep_local_routing(const int32_t *recv_cnt, int32_t P, int32_
     PG_REQUIRE(P >= 1 && El >= 1, PGMOE_E_CONFIG, "bad EP shape P=%d El=%d", P, El);
     const size_t smem = (size_t)(P + P * El) * 4;
     PG_REQUIRE(smem <= 48 * 1024, PGMOE_E_CONFIG, "EP routing table too large");
-    ep_local_routing_kernel<<<1, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(recv_cnt, P, El, 0, *out);
+    ep_local_routing_kernel<<<1, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(recv_cnt, El, P, El, 0, *out);
     PG_CUDA(cudaGetLastError());
     count_launch();
     return PGMOE_OK;

@@ -161,15 +161,18 @@ class EPDecoder:
         if self.packed:
             dev = torch.device("cuda", torch.cuda.current_device())
             rows, d, f = self.P * self.cap, config.d_model, config.d_ff
+            # per-peer slot: cap rows + a header carrying the counts (one
+            # all-to-all moves both)
+            self.slot = int(self._L.pgmoe_ep_slot_rows(self.cap, self.El, d))
+            srows = self.P * self.slot
             bf = dict(dtype=torch.bfloat16, device=dev)
-            self.send = torch.zeros((rows, d), **bf)
-            self.recv = torch.zeros((rows, d), **bf)
+            self.send = torch.zeros((srows, d), **bf)
+            self.recv = torch.zeros((srows, d), **bf)
             self.xb = torch.zeros((rows, d), **bf)
             self.hb = torch.zeros((rows, f), **bf)
-            self.y_recv = torch.zeros((rows, d), dtype=torch.float32, device=dev)
-            self.back = torch.zeros((rows, d), dtype=torch.float32, device=dev)
+            self.y_recv = torch.zeros((srows, d), dtype=torch.float32, device=dev)
+            self.back = torch.zeros((srows, d), dtype=torch.float32, device=dev)
             self.yw = torch.zeros((self.cap, d), dtype=torch.float32, device=dev)
-            self.recv_cnt = torch.zeros(self.P * self.El, dtype=torch.int32, device=dev)
 
     def block(self, b: int, x: torch.Tensor, r_in: DeviceRouting, stream=None):
         if self.packed:
@@ -185,9 +188,8 @@ class EPDecoder:
             raise ShapeError(f"T={T} exceeds the EP buffers (max_tokens={self.max_tokens})")
         s = _stream(stream)
         _lib.check(L.pgmoe_ep_pack_send(_ptr(x), ctypes.byref(r_in.c), T, d, k, P, El, cap, _ptr(self.send), s))
-        ex.fixed(r_in.hist[:P * El], self.recv_cnt)     # counts [P][El]
-        ex.fixed(self.send, self.recv)                   # bf16 rows, cap per peer
-        _lib.check(L.pgmoe_ep_local_routing_padded(_ptr(self.recv_cnt), P, El, cap, ctypes.byref(self.lr.c), s))
+        ex.fixed(self.send, self.recv)                   # bf16 rows + counts header, one slot per peer
+        _lib.check(L.pgmoe_ep_local_routing_padded(_ptr(self.recv), P, El, cap, d, ctypes.byref(self.lr.c), s))
         _lib.check(L.pgmoe_ep_pack_recv(_ptr(self.recv), ctypes.byref(self.lr.c), El, P * cap, d, _ptr(self.xb), s))
         base, stride = ctypes.c_void_p(), ctypes.c_size_t()
         eb, nl = ctypes.c_int32(), ctypes.c_int32()
