@@ -596,8 +596,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         // activation bytes.  The activation boxes come from the gated
         // producer (warp 6), so a gate wait never stalls the weight stream.
         if (lane == 0) {
-            uint64_t policy;
+            uint64_t policy, policy_keep;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+            // the dense weight tiles are re-read by every token tile: keep them
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy_keep));
             int stage = 0, qi = 0;
             uint32_t phase = 0, qphase = 0;
             bool pdl_done = false;
@@ -632,7 +634,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                     cyc_empty += clock64() - c1;
                     mbar_expect_tx(&full[stage], kABytes + x.n_pad * 128);
                     tma_load_3d(sA + stage * kABytes, amaps[x.ph], &full[stage], kb * BK, x.m_tile * BM, x.rec,
-                                policy);
+                                (ps[x.ph].mode == kDense && ps[x.ph].tiles > ps[x.ph].m_tiles) ? policy_keep : policy);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 if (!pdl_done) {  // the unit counter is re-armed by the previous launch
