@@ -536,6 +536,26 @@ extern "C" int pgmoe_debug_set_probe(int32_t kind, void *device_buffer, int64_t 
     return PGMOE_OK;
 }
 
+// Workspaces of the standalone (model-less) tcgen05 entry points: split-K
+// tickets and partials, re-armed by each launch's last CTA, so calls that
+// share one must be stream-ordered.  Allocated once per process, under a
+// lock (EP ranks may be threads of one process).
+constexpr size_t kSharedWsBytes = 64ull << 20;
+static int shared_tc_ws(int slot, void **out) {
+    static std::mutex mu;
+    static void *ws[3] = {nullptr, nullptr, nullptr};
+    std::lock_guard<std::mutex> lock(mu);
+    if (!ws[slot]) {
+        void *p = nullptr;
+        PG_CUDA(cudaMalloc(&p, kSharedWsBytes));
+        PG_CUDA(cudaMemset(p, 0, kSharedWsBytes));
+        PG_CUDA(cudaDeviceSynchronize());
+        ws[slot] = p;
+    }
+    *out = ws[slot];
+    return PGMOE_OK;
+}
+
 extern "C" int pgmoe_expert_forward(const float *x, int32_t T, int32_t d, int32_t f, int32_t k,
                                     const void *experts, size_t expert_stride, int32_t wdtype,
                                     int32_t indexed_by_act, const pgmoe_routing *r, float *h, float *yw,
@@ -546,13 +566,9 @@ extern "C" int pgmoe_expert_forward(const float *x, int32_t T, int32_t d, int32_
     if (kernel == PGMOE_KERNEL_TCGEN05)
         PG_REQUIRE(tc, PGMOE_E_CONFIG, "tcgen05 kernels need bf16 weights and d, f multiples of 128");
     if (tc) {
-        static void *ws = nullptr;
-        static size_t ws_bytes = 0;
-        if (!ws) {
-            ws_bytes = 64ull << 20;
-            PG_CUDA(cudaMalloc(&ws, ws_bytes));
-            PG_CUDA(cudaMemset(ws, 0, ws_bytes));
-        }
+        void *ws = nullptr;
+        const size_t ws_bytes = kSharedWsBytes;
+        PG_TRY(shared_tc_ws(0, &ws));
         return expert_ffn_tc(x, T, d, f, k, experts, expert_stride, indexed_by_act, r, h, yw, ws, ws_bytes, s);
     }
     return expert_ffn_simt(x, T, d, f, k, experts, expert_stride, wdtype, indexed_by_act, r, h, yw, s);
@@ -564,13 +580,9 @@ extern "C" int pgmoe_expert_forward_packed(const uint16_t *xb, int32_t n_max, in
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (n_max == 0) return PGMOE_OK;
     PG_REQUIRE(tc_supported(d, f), PGMOE_E_CONFIG, "tcgen05 kernels need d, f multiples of 128");
-    static void *ws = nullptr;
-    static size_t ws_bytes = 0;
-    if (!ws) {
-        ws_bytes = 64ull << 20;
-        PG_CUDA(cudaMalloc(&ws, ws_bytes));
-        PG_CUDA(cudaMemset(ws, 0, ws_bytes));
-    }
+    void *ws = nullptr;
+    const size_t ws_bytes = kSharedWsBytes;
+    PG_TRY(shared_tc_ws(1, &ws));
     return expert_ffn_tc2(nullptr, n_max, d, f, 1, experts, expert_stride, 0, r, const_cast<uint16_t *>(xb), hb, y,
                           nullptr, ws, ws_bytes, s, true);
 }
@@ -583,13 +595,9 @@ extern "C" int pgmoe_dense_forward(const float *yw, int32_t T, int32_t d, int32_
     if (kernel == PGMOE_KERNEL_TCGEN05)
         PG_REQUIRE(tc, PGMOE_E_CONFIG, "tcgen05 dense needs bf16 weights and d multiple of 128");
     if (tc) {
-        static void *ws = nullptr;
-        static size_t ws_bytes = 0;
-        if (!ws) {
-            ws_bytes = 64ull << 20;
-            PG_CUDA(cudaMalloc(&ws, ws_bytes));
-            PG_CUDA(cudaMemset(ws, 0, ws_bytes));
-        }
+        void *ws = nullptr;
+        const size_t ws_bytes = kSharedWsBytes;
+        PG_TRY(shared_tc_ws(2, &ws));
         return dense_tc(yw, T, d, k, dense_w, y, ws, ws_bytes, s);
     }
     return dense_simt(yw, T, d, k, dense_w, wdtype, y, s);
@@ -623,7 +631,7 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
     const size_t d = c.d_model, f = c.d_ff, E = m->e_local, nb = c.num_blocks, k = c.top_k;
     m->sw = dtype_bytes(wdtype);
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    m->gate_bytes = al(d * E * m->sw);
+    m->gate_bytes = al(d * (size_t)c.num_experts * m->sw);  // gates span all experts, also on an EP shard
     m->dense_bytes = al(d * d * m->sw);
     m->w1_bytes = f * d * m->sw;
     m->rec_bytes = al(2 * f * d * m->sw);

@@ -487,6 +487,70 @@ def test_ep_decoder_single_rank_nccl_equals_single_gpu():
         dist.destroy_process_group()
 
 
+def test_ep_two_ranks_in_one_process_equal_single_gpu(monkeypatch):
+    """The P > 1 device path of the fixed-size EP exchange (slots per peer,
+    in-band counts, receiver routing over two sources, un-permute) on one
+    GPU: two EPDecoder ranks in two threads, the all-to-all replaced by a
+    copy of the peers' slots.  Both ranks' outputs and routing must equal
+    the single-GPU decoder on the concatenated batch bit-for-bit."""
+    import threading
+    import paper_2308_12066_b200.ep as epm
+    p = P()
+    Pn, T = 2, 24
+    cfg = p.ModelConfig(d_model=256, d_ff=512, num_blocks=4, num_experts=16, top_k=2, activation_level=1)
+
+    class Hub:
+        barrier = threading.Barrier(Pn)
+        bufs: dict = {}
+
+    class SlotExchange:  # what all_to_all_single does with equal splits
+        def __init__(self, rank):
+            self.P, self.rank = Pn, rank
+
+        def fixed(self, send, recv):
+            torch.cuda.synchronize()
+            Hub.bufs[self.rank] = send
+            Hub.barrier.wait()
+            c = send.shape[0] // Pn
+            for q in range(Pn):
+                recv[q * c:(q + 1) * c].copy_(Hub.bufs[q][self.rank * c:(self.rank + 1) * c])
+            torch.cuda.synchronize()
+            Hub.barrier.wait()
+            return recv
+
+    monkeypatch.setattr(epm, "Exchange", lambda group: group)
+    from paper_2308_12066_b200._rng import token_batch
+    xs = [torch.from_numpy(token_batch(0, 256, T, offset=r * T)).cuda() for r in range(Pn)]
+    out, errs = {}, []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            ep = epm.EPDecoder(cfg, dtype="bf16", max_tokens=T, group=SlotExchange(r))
+            ep.use_graph = False
+            y, ids = ep.decoder_iteration(xs[r], trace=True)
+            torch.cuda.synchronize()
+            out[r] = (y.clone(), ids.clone())
+            ep.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+            Hub.barrier.abort()
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(Pn)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    ref = p.DeviceModel(cfg, dtype="bf16", max_tokens=Pn * T)
+    y, ids, _ = ref.decoder_iteration(torch.cat(xs), trace=True)
+    torch.cuda.synchronize()
+    for r in range(Pn):
+        assert torch.equal(out[r][1], ids[:, r * T:(r + 1) * T])
+        assert torch.equal(out[r][0], y[r * T:(r + 1) * T])
+    ref.close()
+
+
 # ------------------------------------------------- migration strategies ----
 
 @pytest.mark.parametrize("strategy", ["pre_gated", "on_demand", "prefetch_all"])
