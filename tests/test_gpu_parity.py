@@ -487,16 +487,18 @@ def test_ep_decoder_single_rank_nccl_equals_single_gpu():
         dist.destroy_process_group()
 
 
-def test_ep_two_ranks_in_one_process_equal_single_gpu(monkeypatch):
+@pytest.mark.parametrize("Pn", [2, 4])
+def test_ep_ranks_in_one_process_equal_single_gpu(monkeypatch, Pn):
     """The P > 1 device path of the fixed-size EP exchange (slots per peer,
-    in-band counts, receiver routing over two sources, un-permute) on one
-    GPU: two EPDecoder ranks in two threads, the all-to-all replaced by a
-    copy of the peers' slots.  Both ranks' outputs and routing must equal
-    the single-GPU decoder on the concatenated batch bit-for-bit."""
+    in-band counts, receiver routing over P sources, un-permute) on one GPU:
+    P EPDecoder ranks in P threads (one stream: stream-ordered like P
+    processes), the all-to-all replaced by a copy of the peers' slots.  Every
+    rank's outputs and routing must equal the single-GPU decoder on the
+    concatenated batch bit-for-bit."""
     import threading
     import paper_2308_12066_b200.ep as epm
     p = P()
-    Pn, T = 2, 24
+    T = 24
     cfg = p.ModelConfig(d_model=256, d_ff=512, num_blocks=4, num_experts=16, top_k=2, activation_level=1)
 
     class Hub:
