@@ -302,12 +302,12 @@ __device__ void router_logits(const FusedRoute &r, int unit, int rt, float *xs, 
     router_sync();  // the x slice is rewritten by the next unit
 }
 
-// Sum the K-split partials of a tile's tokens (all 64 threads, loads of two
-// (token, expert) entries = up to 64 partials in flight per thread, summed in
-// split order) into shared memory: lgs[t][j] (fp64 logit), cms[t][j] (column
-// max |G|), sxs[t] (sum |x|).  The per-token selection then works from
-// shared memory, so the tile costs one or two dependent load rounds rather
-// than one per 32 experts per token.
+// Sum the K-split partials of a tile's tokens (all 128 role threads, loads
+// of two (token, expert) entries = up to 64 partials in flight per thread,
+// summed in split order) into shared memory: lgs[t][j] (fp64 logit),
+// cms[t][j] (column max |G|), sxs[t] (sum |x|).  The per-token selection
+// then works from shared memory, so the tile costs one or two dependent
+// load rounds rather than one per 32 experts per token.
 struct TileSums {
     double *lgs;  // [ntok][E]
     float *cms;   // [ntok][E]
