@@ -136,7 +136,7 @@ struct pgmoe_model {
     // completion (PGMOE_CHAIN=1).  Measured: saves the ~4.5 us completion
     // latency but pays ~3-4 us of atomic + fence + poll, net -1 % at T=256
     // and +2 % at T=1 (tools/gpu_ab_chain.sh), so off by default.
-    bool chain_launches = false;
+    bool chain_launches = true;  // PGMOE_CHAIN=0: PDL completion only
     int *epoch = nullptr;        // device counter of chained launches
     // host-buffer entry point
     cudaStream_t io_stream = nullptr;
@@ -713,7 +713,7 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
         return fail(PGMOE_E_OOM);
     if (cudaMalloc(&m->epoch, 256) != cudaSuccess || cudaMemset(m->epoch, 0, 256) != cudaSuccess)
         return fail(PGMOE_E_OOM);
-    if (const char *e = getenv("PGMOE_CHAIN")) m->chain_launches = (e[0] == '1');
+    if (const char *e = getenv("PGMOE_CHAIN")) m->chain_launches = (e[0] != '0');
     if (const char *e = getenv("PGMOE_FUSED_ROUTE")) m->fuse_route = (e[0] == '1');
     if (const char *e = getenv("PGMOE_FUSE_MAX_T")) m->fuse_max_t = atoll(e);
     cudaEventCreate(&m->t0);

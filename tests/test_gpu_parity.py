@@ -329,11 +329,13 @@ def test_fused_routing_equals_separate_launch_and_offloaded(E, T):
 
 
 def test_chained_block_launches_equal_pdl_chain(monkeypatch):
-    """PGMOE_CHAIN=1: each resident block launch waits for its predecessor's
-    dense phase through a device counter (parity-buffered counters) instead
-    of its completion; outputs and routing must be identical."""
+    """Chained launches (the default; PGMOE_CHAIN=0 turns them off): each
+    resident block launch waits for its predecessor's dense phase through a
+    device counter (parity-buffered counters) instead of its completion;
+    outputs and routing must be identical, eagerly and from the graph."""
     dims = og.Dims(256, 512, 6, 128, 1, seed=9)
     x0 = torch.from_numpy(tokens(256, 48)).cuda()
+    monkeypatch.setenv("PGMOE_CHAIN", "0")
     base = _device_model(dims, "bf16", "resident", max_tokens=48)
     monkeypatch.setenv("PGMOE_CHAIN", "1")
     chained = _device_model(dims, "bf16", "resident", max_tokens=48)
@@ -343,8 +345,14 @@ def test_chained_block_launches_equal_pdl_chain(monkeypatch):
             y, ids, w = m.decoder_iteration(x0, trace=True)
         torch.cuda.synchronize()
         outs.append((y.clone(), ids.clone(), w.clone()))
+        yg = torch.empty_like(x0)
+        for _ in range(3):  # captured once, then replayed (persistent buffers)
+            m.decoder_iteration(x0, out=yg)
+        torch.cuda.synchronize()
+        outs[-1] = outs[-1] + (yg.clone(),)
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
+    assert torch.equal(outs[1][0], outs[1][3])
     base.close()
     chained.close()
 
