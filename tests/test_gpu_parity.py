@@ -510,7 +510,7 @@ def test_ep_ranks_in_one_process_equal_single_gpu(monkeypatch, Pn):
     cfg = p.ModelConfig(d_model=256, d_ff=512, num_blocks=4, num_experts=16, top_k=2, activation_level=1)
 
     class Hub:
-        barrier = threading.Barrier(Pn)
+        barrier = threading.Barrier(Pn, timeout=120)  # a stuck rank fails the test instead of hanging it
         bufs: dict = {}
 
     class SlotExchange:  # what all_to_all_single does with equal splits
@@ -552,6 +552,7 @@ def test_ep_ranks_in_one_process_equal_single_gpu(monkeypatch, Pn):
     for t in th:
         t.join(timeout=300)
     assert not errs, errs
+    assert len(out) == Pn
     ref = p.DeviceModel(cfg, dtype="bf16", max_tokens=Pn * T)
     y, ids, _ = ref.decoder_iteration(torch.cat(xs), trace=True)
     torch.cuda.synchronize()
