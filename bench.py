@@ -341,7 +341,9 @@ def run_ours(args, rank: int, world: int):
                    "preset": args.preset, "placement": args.placement, "tokens_per_rank": T,
                    "global_batch": T * world, "num_blocks": nb, "d_model": d, "d_ff": f, "num_experts": E,
                    "top_k": 1, "activation_level": 1, "parallelism": f"sequences x{world} (replicas)",
-                   "l2": "per-step expert bytes >> 126 MB L2 (no reuse across steps)", "kernel": args.kernel},
+                   "l2": "inputs larger than L2: per-step expert bytes >> 126 MB (streamed evict-first); only the "
+                         "dense weights (d^2 per block, loaded evict-last) may stay L2-resident across steps",
+                   "kernel": args.kernel},
         "per_block_latency_ms": round(block_ms, 4),
         "per_block_phase_ms": phases,
         "block_roofline": {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / block_ms, 4),
