@@ -92,3 +92,14 @@ def test_host_token_generator_matches_oracle():
     got = token_batch(3, 768, 9)
     ref = np.stack([og.token_input(dims, t) for t in range(9)]).astype(np.float32)
     assert np.array_equal(got, ref)
+
+
+def test_ep_slot_layout_is_host_computable():
+    """pgmoe_ep_slot_rows: each peer slot is cap routed rows plus the header
+    rows that carry the sender's per-expert int32 counts in-band (one
+    all-to-all for rows and counts).  Pure host arithmetic: no GPU needed."""
+    from paper_2308_12066_b200 import _lib
+    L = _lib.load()
+    assert L.pgmoe_ep_slot_rows(256, 16, 1024) == 257     # Large-128 over 8 ranks
+    assert L.pgmoe_ep_slot_rows(48, 8, 256) == 49
+    assert L.pgmoe_ep_slot_rows(4, 600, 256) == 4 + 5     # 2400 B of counts in 512-byte rows
