@@ -418,6 +418,7 @@ __device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int
     uint32_t taken = 0;
     bool certified = true;
     double minlow = INFINITY;
+    double top = 0.0;  // the largest logit: the first selected one (the softmax shift)
     for (int s = 0; s < k; ++s) {
         double bf = -INFINITY;
         int bi = -1;
@@ -428,6 +429,7 @@ __device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int
                 bi = lane + 32 * jj;
             }
         warp_argmax(bf, bi);
+        if (s == 0) top = bf;
         sel[s] = bi;
         if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
         const double low = bf - pick(bd, bi);
@@ -458,6 +460,9 @@ __device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int
                     bi = lane + 32 * jj;
                 }
             warp_argmax(bf, bi);
+            // the recomputed candidates bound every other logit from above
+            // (those stay below minlow), so the maximum is still the first pick
+            if (s == 0) top = bf;
             sel[s] = bi;
             if ((bi & 31) == lane) cand &= ~(1u << (bi >> 5));
         }
@@ -465,10 +470,7 @@ __device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int
     }
     probe(pr, blockIdx.x, 38);
     // softmax over all E (linalg.py:54-59), max-subtracted; same order as route.cu
-    double m = -INFINITY;
-#pragma unroll
-    for (int jj = 0; jj < NJ; ++jj) m = fmax(m, lg[jj]);
-    m = warp_max(m);
+    const double m = top;  // == max over all E logits (no extra warp reduction)
     double z = 0.0;
 #pragma unroll
     for (int jj = 0; jj < NJ; ++jj) z += exp(lg[jj] - m);
