@@ -76,8 +76,7 @@ typedef struct {
     int32_t *act;    /* [E]    active experts ascending (first *n_act valid) */
     int32_t *n_act;  /* [1] */
     int32_t *status; /* [4] [0] device error code, [1] tokens that needed the
-                        serial-fp64 recompute, [2] routing flips (0 by
-                        construction), [3] reserved */
+                        serial-fp64 recompute, [2], [3] reserved */
     int32_t *inv;    /* [T*k] optional (may be NULL): position of entry t*k+s in perm */
 } pgmoe_routing;
 
@@ -160,8 +159,19 @@ PGMOE_API int pgmoe_ep_unpermute_padded(const float *back, const pgmoe_routing *
                                         int32_t P, int32_t El, int32_t cap, float *yw, pgmoe_stream_t stream);
 
 /* Reads routing status after a sync: returns the device-detected error (or
- * PGMOE_OK) and optionally the serial-fallback / flip counters. */
-PGMOE_API int pgmoe_check_routing(const pgmoe_routing *r, int32_t *fallbacks, int32_t *flips);
+ * PGMOE_OK) and optionally the serial-fallback counter.  (Flips against the
+ * reference are not a device quantity: tests/ and bench.py measure them by
+ * running the oracle on the same inputs.) */
+PGMOE_API int pgmoe_check_routing(const pgmoe_routing *r, int32_t *fallbacks);
+
+/* Supplied decisions: the `supplied_decisions` path of decoder_iteration
+ * (core.py:342-364) and synthetic routing traces (gen_routing_trace,
+ * core.py:436-479).  ids [T][k] / w [T][k] (device) are copied into `out`
+ * with RoutingDecision's checks (core.py:110-140: ids distinct and in
+ * [0, E), weights in (0, 1]; a violation sets status[0] = PGMOE_E_ROUTING),
+ * and the same histogram / scan / stable permutation K1 builds. */
+PGMOE_API int pgmoe_route_from_decisions(const int32_t *ids, const float *w, int32_t T, int32_t E, int32_t k,
+                                         const pgmoe_routing *out, pgmoe_stream_t stream);
 
 /* Deterministic weights: fills `out` ([rows][cols], wdtype) on the device
  * with Xoshiro256StarStar(derive_seed(seed, tag, block, expert)).fill_matrix
@@ -181,7 +191,7 @@ typedef struct {
     int64_t h2d_bytes;            /* expert bytes migrated since reset */
     int64_t h2d_copies;
     int64_t route_fallbacks;      /* tokens needing the serial fp64 recompute */
-    int64_t route_flips;          /* always 0: certified routing */
+    int64_t reserved0;
     double h2d_seconds;           /* copy-stream busy time (CUDA events) */
     double last_step_seconds;
     int64_t cache_bytes;          /* HBM expert-cache region (0 = no cache) */
@@ -262,6 +272,28 @@ PGMOE_API int pgmoe_model_set_fused_route(pgmoe_model *m, int32_t enabled);
  * (scheduler.py:344-373) runs on the model's copy stream when offloaded. */
 PGMOE_API int pgmoe_decoder_iteration(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
                             int32_t *ids_trace, float *w_trace, pgmoe_stream_t stream);
+
+/* Optional inputs / outputs of one decoder iteration (all device, may be NULL):
+ *   ids_trace / w_trace  [num_blocks][T][k]  decisions each block consumed
+ *   x_trace              [num_blocks][T][d]  each block's input (fp32), for
+ *                        teacher-forced parity at the exact launch sequence
+ *   ids_supplied / w_supplied [num_blocks][T][k]  supplied decisions
+ *                        (core.py:342-364): every block consumes them, no
+ *                        gate runs; migration follows the same issue points */
+typedef struct {
+    int32_t *ids_trace;
+    float *w_trace;
+    float *x_trace;
+    const int32_t *ids_supplied;
+    const float *w_supplied;
+} pgmoe_iteration_io;
+
+PGMOE_API int pgmoe_decoder_iteration_ex(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
+                                         const pgmoe_iteration_io *io, pgmoe_stream_t stream);
+
+/* Synchronises and surfaces a device-detected routing error of the model's
+ * last iterations (GateOverflowError / RoutingError), then clears it. */
+PGMOE_API int pgmoe_model_check_routing(pgmoe_model *m);
 
 /* Same call on HOST buffers: copies x in, runs, copies y (and the trace)
  * back, synchronises, and raises device-detected routing errors. */

@@ -46,11 +46,15 @@ class Routing(ctypes.Structure):
                 ("ids", "w", "hist", "off", "perm", "w_perm", "act", "n_act", "status", "inv")]
 
 
+class IterationIO(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("ids_trace", "w_trace", "x_trace", "ids_supplied", "w_supplied")]
+
+
 class Stats(ctypes.Structure):
     _fields_ = [("pinned_hbm_bytes", ctypes.c_int64), ("slot_capacity_bytes", ctypes.c_int64),
                 ("eq1_peak_bytes", ctypes.c_int64), ("ledger_peak_bytes", ctypes.c_int64),
                 ("h2d_bytes", ctypes.c_int64), ("h2d_copies", ctypes.c_int64),
-                ("route_fallbacks", ctypes.c_int64), ("route_flips", ctypes.c_int64),
+                ("route_fallbacks", ctypes.c_int64), ("reserved0", ctypes.c_int64),
                 ("h2d_seconds", ctypes.c_double), ("last_step_seconds", ctypes.c_double),
                 ("cache_bytes", ctypes.c_int64), ("cache_hits", ctypes.c_int64), ("cache_misses", ctypes.c_int64),
                 ("d2d_bytes", ctypes.c_int64), ("fused_blocks", ctypes.c_int64),
@@ -69,7 +73,8 @@ EXPORTS = (
     "pgmoe_model_load_pgmoe1", "pgmoe_model_save_pgmoe1", "pgmoe_model_set_strategy", "pgmoe_model_set_cache",
     "pgmoe_cache_replay", "pgmoe_debug_set_probe", "pgmoe_model_set_fused_route",
     "pgmoe_ep_pack_send", "pgmoe_ep_local_routing_padded", "pgmoe_ep_pack_recv", "pgmoe_expert_forward_packed",
-    "pgmoe_ep_unpermute_padded", "pgmoe_ep_slot_rows",
+    "pgmoe_ep_unpermute_padded", "pgmoe_ep_slot_rows", "pgmoe_route_from_decisions", "pgmoe_decoder_iteration_ex",
+    "pgmoe_model_check_routing",
 )
 
 _lib = None
@@ -92,7 +97,10 @@ def load():
         "pgmoe_gate_forward": (i32, [vp, i32, i32, vp, i32, i32, i32, P(Routing), vp, vp]),
         "pgmoe_expert_forward": (i32, [vp, i32, i32, i32, i32, vp, sz, i32, i32, P(Routing), vp, vp, i32, vp]),
         "pgmoe_dense_forward": (i32, [vp, i32, i32, i32, vp, i32, vp, i32, vp]),
-        "pgmoe_check_routing": (i32, [P(Routing), P(i32), P(i32)]),
+        "pgmoe_check_routing": (i32, [P(Routing), P(i32)]),
+        "pgmoe_route_from_decisions": (i32, [vp, vp, i32, i32, i32, P(Routing), vp]),
+        "pgmoe_model_check_routing": (i32, [vp]),
+        "pgmoe_decoder_iteration_ex": (i32, [vp, vp, i32, vp, P(IterationIO), vp]),
         "pgmoe_fill_weights": (i32, [vp, i32, ctypes.c_uint64, i32, i32, i32, i64, i64, vp]),
         "pgmoe_model_create": (i32, [P(Config), i32, i32, i32, P(vp)]),
         "pgmoe_model_destroy": (i32, [vp]),

@@ -176,10 +176,10 @@ class DeviceRouting:
 
     def check(self) -> dict:
         """Surface device-detected errors (raises) and return counters."""
-        fb, fl = ctypes.c_int32(0), ctypes.c_int32(0)
+        fb = ctypes.c_int32(0)
         torch.cuda.synchronize()
-        _lib.check(_lib.load().pgmoe_check_routing(ctypes.byref(self._c), ctypes.byref(fb), ctypes.byref(fl)))
-        return {"fallbacks": fb.value, "flips": fl.value}
+        _lib.check(_lib.load().pgmoe_check_routing(ctypes.byref(self._c), ctypes.byref(fb)))
+        return {"fallbacks": fb.value}
 
     def decisions(self) -> list:
         ids = self.ids.cpu().tolist()
@@ -380,11 +380,18 @@ class DeviceModel:
         return t.view(shape)
 
     # -- execution --
-    def decoder_iteration(self, x: torch.Tensor, trace: bool = False, stream=None, out: torch.Tensor = None):
+    def decoder_iteration(self, x: torch.Tensor, trace: bool = False, stream=None, out: torch.Tensor = None,
+                          x_trace: torch.Tensor = None, supplied: tuple = None, trace_out: tuple = None):
         """core.py:342-383 for T tokens (x: cuda fp32 [T][d]).
         Returns (y, ids [nb][T][k], w [nb][T][k]) — trace tensors None unless asked.
+
+        x_trace (optional, cuda fp32 [nb][T][d]) receives every block's input.
+        supplied = (ids [nb][T][k] int32, w [nb][T][k] fp32) on the device:
+        the `supplied_decisions` path (core.py:342-364) — every block
+        consumes them and no gate runs.  trace_out = (ids, w) persistent
+        trace buffers (instead of fresh ones when trace=True).
         Resident models replay a CUDA graph keyed by the buffer addresses, so
-        passing a persistent `out` keeps every call on the replay path."""
+        passing persistent buffers keeps every call on the replay path."""
         c = self.config
         if x.dim() != 2 or x.shape[1] != c.d_model:
             raise ShapeError(f"expected [T][{c.d_model}] input, got {tuple(x.shape)}")
@@ -392,12 +399,33 @@ class DeviceModel:
         x = x.contiguous()
         y = out if out is not None else torch.empty_like(x)
         ids = w = None
-        if trace:
+        if trace_out is not None:
+            ids, w = trace_out
+        elif trace:
             ids = torch.empty((c.num_blocks, T, c.top_k), dtype=torch.int32, device=x.device)
             w = torch.empty((c.num_blocks, T, c.top_k), dtype=torch.float32, device=x.device)
-        _lib.check(self._L.pgmoe_decoder_iteration(self._h, _ptr(x), T, _ptr(y), _ptr(ids), _ptr(w),
-                                                   _stream(stream)))
+        io = _lib.IterationIO(ids.data_ptr() if ids is not None else None, w.data_ptr() if w is not None else None,
+                              None, None, None)
+        if x_trace is not None:
+            if tuple(x_trace.shape) != (c.num_blocks, T, c.d_model) or x_trace.dtype != torch.float32:
+                raise ShapeError(f"x_trace must be float32 [{c.num_blocks}][{T}][{c.d_model}]")
+            io.x_trace = x_trace.data_ptr()
+        if supplied is not None:
+            sid, sw = supplied
+            shp = (c.num_blocks, T, c.top_k)
+            if tuple(sid.shape) != shp or tuple(sw.shape) != shp or sid.dtype != torch.int32 \
+                    or sw.dtype != torch.float32:
+                raise ShapeError(f"supplied decisions must be int32 / float32 {shp}")
+            io.ids_supplied = sid.contiguous().data_ptr()
+            io.w_supplied = sw.contiguous().data_ptr()
+        _lib.check(self._L.pgmoe_decoder_iteration_ex(self._h, _ptr(x), T, _ptr(y), ctypes.byref(io),
+                                                      _stream(stream)))
         return y, ids, w
+
+    def check_routing(self) -> None:
+        """Surface device-detected routing errors of the last iterations
+        (GateOverflowError / RoutingError), after a synchronize."""
+        _lib.check(self._L.pgmoe_model_check_routing(self._h))
 
     def decoder_iteration_host(self, x: np.ndarray, trace: bool = False):
         """Same on host buffers (H2D + blocks + D2H inside one C-ABI call)."""

@@ -39,7 +39,13 @@ void count_launch(int n = 1);  // kernels launched by this library (bench eviden
         }                                     \
     } while (0)
 
-constexpr int kNumSMs = 148;
+constexpr int kNumSMs = 148;  // B200; grid sizing heuristics only — persistent launches use device_sm_count()
+
+// SMs of the current device (cudaDevAttrMultiProcessorCount, cached per
+// device): the persistent kernels put one CTA on each and spin on grid-wide
+// counters, so their grid must never exceed what is co-resident.
+int device_sm_count();
+int current_device();
 
 __device__ __forceinline__ float bf16_to_f32(uint16_t h) {
     return __uint_as_float(static_cast<uint32_t>(h) << 16);

@@ -36,6 +36,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -676,8 +677,11 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
             int stage = 0, qi = 0;
             uint32_t phase = 0, qphase = 0;
             long long cyc_gate = 0;
-            // the activations of phase 0 come from the previous launch
-            if (p.epoch) {
+            // the activations of phase 0 come from the previous launch: its
+            // dense phase (chained, epoch_wait > 0) or its completion (PDL) —
+            // the first launch of a chain follows a non-chained producer (the
+            // operand pack), whose writes only griddepcontrol.wait orders
+            if (p.epoch && p.epoch_wait > 0) {
                 while (ld_acquire(p.epoch) < p.epoch_wait) __nanosleep(32);
                 asm volatile("fence.proxy.async.global;" ::: "memory");
             } else {
@@ -729,7 +733,7 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
         // with this block's expert GEMMs; once it is complete the next launch
         // (which schedules from it) may start.
         if (p.route.active) {
-            if (p.epoch) {  // the block input is the previous launch's dense output
+            if (p.epoch && p.epoch_wait > 0) {  // the block input is the previous launch's dense output
                 if (tid == 7 * 32)
                     while (ld_acquire(p.epoch) < p.epoch_wait) __nanosleep(32);
                 router_sync();
@@ -1035,15 +1039,28 @@ template <int BN, int STAGES>
 static int launch(const PhaseMaps *mp, const Params &p, cudaStream_t s) {
     constexpr size_t smem = smem_bytes<BN, STAGES>();
     static_assert(smem <= 227 * 1024, "shared memory budget");
-    static bool attr = false;
-    if (!attr) {
+    // Per device: the attribute and the co-residency check belong to the
+    // device the launch goes to.  The kernel spins on grid-wide counters
+    // (phase gates, split-K tickets), so every CTA must be resident at once:
+    // one per SM of THIS device (cudaDevAttrMultiProcessorCount), and the
+    // launch is refused — not hung — if even that does not fit (a reduced-SM
+    // context, another kernel's shared-memory carve-out).
+    static std::atomic<unsigned long long> attr_set{0};
+    const int dev = current_device();
+    PG_REQUIRE(dev >= 0 && dev < 64, PGMOE_E_CONFIG, "device ordinal %d unsupported", dev);
+    if (!(attr_set.load() & (1ull << dev))) {
         PG_CUDA(cudaFuncSetAttribute(block_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-        attr = true;
+        int per_sm = 0;
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_gemm_kernel<BN, STAGES>, kThreads, smem));
+        PG_REQUIRE(per_sm >= 1, PGMOE_E_CUDA,
+                   "the persistent tcgen05 block kernel does not fit on an SM (%zu B shared memory)", smem);
+        attr_set.fetch_or(1ull << dev);
     }
+    const int grid = device_sm_count();  // of the current context (green contexts: its own SMs)
     // unused phase slots repeat phase 0's maps (never dereferenced)
     const PhaseMaps &m0 = mp[0], &m1 = p.nphase > 1 ? mp[1] : mp[0], &m2 = p.nphase > 2 ? mp[2] : mp[0];
-    PG_CUDA(launch_pdl(block_gemm_kernel<BN, STAGES>, dim3(kNumSMs), dim3(kThreads), smem, s, m0.a, m0.b, m1.a, m1.b,
+    PG_CUDA(launch_pdl(block_gemm_kernel<BN, STAGES>, dim3(grid), dim3(kThreads), smem, s, m0.a, m0.b, m1.a, m1.b,
                        m2.a, m2.b, p));
     count_launch();
     return PGMOE_OK;
@@ -1061,7 +1078,7 @@ static int run(const PhaseMaps *mp, Params p, int bn, void *ws, size_t ws_bytes,
     p.sync = p.counters + kCounterInts;
     p.partial = reinterpret_cast<float *>(static_cast<char *>(ws) + 2 * head + (size_t)parity * half);
     p.partial_cap = (long long)(half / 4);
-    p.probe = probe_buffer(1, kNumSMs);
+    p.probe = probe_buffer(1, device_sm_count());
     if (p.max_inflight <= 0) p.max_inflight = 8;
     { const char *e = getenv("PGMOE_INFLIGHT"); if (e) p.max_inflight = atoi(e); }
     { const char *e = getenv("PGMOE_MAX_SPLIT"); if (e) p.max_split = atoi(e); }

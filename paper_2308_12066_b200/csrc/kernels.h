@@ -32,7 +32,7 @@ struct FusedRoute;
 // Chained resident launches (see tc::Params::epoch).
 struct LaunchChain {
     int *epoch;       // device counter, zeroed at the start of each decoder iteration
-    int epoch_wait;   // 0: wait for the previous launch to complete (PDL)
+    int epoch_wait;   // > 0: wait for *epoch >= epoch_wait; 0: for the previous launch to complete (PDL)
     int epoch_set;
     int parity;       // alternates between consecutive block launches
 };

@@ -13,7 +13,9 @@
 // reference order is certified; otherwise the candidates that could reach
 // the top-k are recomputed in exactly the reference order (serial
 // __dadd_rn/__dmul_rn) and ranked with the reference key (-logit, id).
-// The fallback count is reported; flips are zero by construction.
+// The fallback count is reported: ids equal the serial-fp64 ranking by
+// construction (flips against the reference are measured by the tests and
+// bench.py on the same inputs, not assumed).
 //
 // One kernel, grid (token tiles x K splits):
 //   1. every CTA accumulates fp64 partial logits of TOK tokens over its K
@@ -547,11 +549,10 @@ extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const vo
     return PGMOE_E_CONFIG;
 }
 
-extern "C" int pgmoe_check_routing(const pgmoe_routing *r, int32_t *fallbacks, int32_t *flips) {
+extern "C" int pgmoe_check_routing(const pgmoe_routing *r, int32_t *fallbacks) {
     int32_t st[4];
     PG_CUDA(cudaMemcpy(st, r->status, sizeof(st), cudaMemcpyDeviceToHost));
     if (fallbacks) *fallbacks = st[1];
-    if (flips) *flips = st[2];
     if (st[0] == PGMOE_E_GATE_OVERFLOW) {
         set_error("numerical overflow in gate");
         return PGMOE_E_GATE_OVERFLOW;
@@ -560,5 +561,72 @@ extern "C" int pgmoe_check_routing(const pgmoe_routing *r, int32_t *fallbacks, i
         set_error("gate routing weight underflowed to zero");
         return PGMOE_E_GATE_UNDERFLOW;
     }
+    if (st[0] == PGMOE_E_ROUTING) {
+        set_error("supplied routing decision invalid (expert id out of range, duplicate id, or combine weight "
+                  "outside (0, 1])");
+        return PGMOE_E_ROUTING;
+    }
     return st[0];
+}
+
+// Supplied decisions (core.py:342-364 `supplied_decisions`, synthetic traces
+// core.py:436-479): ids/w [T][k] given, gate math bypassed.  One CTA copies
+// them into the routing buffer while checking RoutingDecision's invariants
+// (core.py:110-140: ids distinct and in [0, E), weights in (0, 1]), then
+// builds the same histogram / scan / stable permutation K1 builds.
+__global__ void __launch_bounds__(kSelectThreads) route_from_decisions_kernel(const int32_t *__restrict__ ids,
+                                                                              const float *__restrict__ w,
+                                                                              const RouteParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
+    const int N = p.T * p.k;
+    bool bad = false;
+    for (int r = threadIdx.x; r < N; r += kSelectThreads) {
+        const int e = __ldg(ids + r);
+        const float wv = __ldg(w + r);
+        bad |= (e < 0 || e >= p.E || !(wv > 0.f && wv <= 1.f));
+        const int t = r / p.k;
+        for (int s = t * p.k; s < r; ++s) bad |= (__ldg(ids + s) == e);
+        p.out.ids[r] = (e < 0 || e >= p.E) ? 0 : e;  // keep the permutation in range
+        p.out.w[r] = wv;
+    }
+    if (__syncthreads_or(bad)) {
+        if (threadIdx.x == 0) atomicCAS(p.out.status, 0, (int)PGMOE_E_ROUTING);
+    }
+    __threadfence_block();
+    __syncthreads();
+    permute_all(p, smem_raw);
+    __threadfence();
+    __syncthreads();
+    pdl_trigger();
+}
+
+extern "C" int pgmoe_route_from_decisions(const int32_t *ids, const float *w, int32_t T, int32_t E, int32_t k,
+                                          const pgmoe_routing *out, pgmoe_stream_t stream) {
+    PG_REQUIRE(out != nullptr, PGMOE_E_CONFIG, "route_from_decisions: null routing buffers");
+    PG_REQUIRE(k >= 1 && k <= 8 && k <= E, PGMOE_E_CONFIG, "top_k=%d unsupported for E=%d", k, E);
+    PG_REQUIRE(E >= 1 && E <= 1024, PGMOE_E_CONFIG, "num_experts=%d unsupported (1..1024)", E);
+    PG_REQUIRE(T >= 0, PGMOE_E_SHAPE, "negative token count");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (T == 0) {
+        PG_CUDA(cudaMemsetAsync(out->hist, 0, sizeof(int32_t) * E, s));
+        PG_CUDA(cudaMemsetAsync(out->off, 0, sizeof(int32_t) * (E + 1), s));
+        PG_CUDA(cudaMemsetAsync(out->n_act, 0, sizeof(int32_t), s));
+        return PGMOE_OK;
+    }
+    RouteParams p{};
+    p.T = T;
+    p.E = E;
+    p.k = k;
+    p.out = *out;
+    const size_t smem = (size_t)(kSelectWarps + 1) * E * 4;
+    static bool attr = false;
+    if (!attr && smem > 48 * 1024) {
+        PG_CUDA(cudaFuncSetAttribute(route_from_decisions_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smem, 64 * 1024)));
+        attr = true;
+    }
+    PG_CUDA(launch_pdl(route_from_decisions_kernel, dim3(1), dim3(kSelectThreads), smem, s, ids, w, p));
+    count_launch();
+    return PGMOE_OK;
 }

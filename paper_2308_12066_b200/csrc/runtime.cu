@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "expert_cache.h"
 #include "kernels.h"
@@ -40,6 +42,56 @@ unsigned long long *probe_buffer(int kind, int ctas) {
     unsigned long long *b = g_probe[kind] + (size_t)g_probe_next[kind] * kProbeSlots;
     g_probe_next[kind] += ctas;
     return b;
+}
+
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
+// SMs the CURRENT context may use: a green context (or any context carved
+// out of the device's SMs) reports its own share through cuCtxGetDevResource;
+// otherwise the device attribute.  Cached per context.  PGMOE_SM_LIMIT caps
+// it (testing the persistent kernels on fewer co-resident CTAs).
+int device_sm_count() {
+    using GetCur = CUresult (*)(CUcontext *);
+    using GetRes = CUresult (*)(CUcontext, CUdevResource *, CUdevResourceType);
+    static std::mutex mu;
+    static std::vector<std::pair<CUcontext, int>> cache;
+    static GetCur get_cur = nullptr;
+    static GetRes get_res = nullptr;
+    static bool looked = false;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!looked) {
+        looked = true;
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuCtxGetCurrent", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            get_cur = reinterpret_cast<GetCur>(p);
+        p = nullptr;
+        if (cudaGetDriverEntryPoint("cuCtxGetDevResource", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            get_res = reinterpret_cast<GetRes>(p);
+    }
+    cudaFree(nullptr);  // make sure a context is current
+    CUcontext ctx = nullptr;
+    if (get_cur) get_cur(&ctx);
+    for (auto &e : cache)
+        if (e.first == ctx) return e.second;
+    int n = 0;
+    CUdevResource res;
+    memset(&res, 0, sizeof(res));
+    if (ctx && get_res && get_res(ctx, &res, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS) n = (int)res.sm.smCount;
+    if (n <= 0 && (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device()) != cudaSuccess || n <= 0))
+        n = kNumSMs;
+    if (const char *e = getenv("PGMOE_SM_LIMIT")) {
+        const int lim = atoi(e);
+        if (lim > 0) n = std::min(n, lim);
+    }
+    cache.emplace_back(ctx, n);
+    return n;
 }
 
 void set_error(const char *fmt, ...) {
@@ -101,6 +153,9 @@ struct pgmoe_model {
     unsigned char *slots = nullptr;
     size_t slot_capacity = 0;  // bytes per slot
     int slot_experts = 0;
+    // expert slots: L+1 (one per routing decision in flight); prefetch_all
+    // needs max(L+1, 2) because block b+1's set streams while b computes
+    int nslots = 0;
     cudaStream_t copy = nullptr;
     std::vector<cudaEvent_t> ready, done, routed;
     cudaEvent_t gated = nullptr;  // on_demand: compute reached the block
@@ -121,8 +176,7 @@ struct pgmoe_model {
         const float *x = nullptr;
         float *y = nullptr;
         int T = -1;
-        int32_t *ids = nullptr;
-        float *w = nullptr;
+        pgmoe_iteration_io io{};
         unsigned long long last_use = 0;
         long long launches = 0;  // kernels per replay (benchmark evidence)
     };
@@ -291,17 +345,17 @@ static int fetch_cached(pgmoe_model *m, int tb, const int32_t *ids, int n, unsig
 // (scheduler.py:287-330 `issue`, made real).  Waits on the host for K1's
 // active list (pinned mirror), then enqueues one DMA per expert on the copy
 // stream after the slot's previous consumer finished.
-static int issue_fetch(pgmoe_model *m, int tb, int ri) {
+static int issue_fetch(pgmoe_model *m, int tb, int ri, int si) {
     const auto &c = m->cfg;
     RoutingBuf &rb = m->routing[ri];
     PG_CUDA(cudaEventSynchronize(m->routed[ri]));
     const int n = rb.act_host[c.num_experts];
     PG_REQUIRE(n >= 0 && n <= m->slot_experts, PGMOE_E_OOM,
                "block %d routes to %d experts but the HBM slot holds %d", tb, n, m->slot_experts);
-    if (m->slot_used[ri]) PG_CUDA(cudaStreamWaitEvent(m->copy, m->done[ri], 0));
+    if (m->slot_used[si]) PG_CUDA(cudaStreamWaitEvent(m->copy, m->done[si], 0));
     if (!m->cp_a.empty()) PG_CUDA(cudaEventRecord(m->cp_a[tb], m->copy));
     tl_begin(m, "transfer", "fetch[" + std::to_string(n) + "]", tb, m->copy);
-    unsigned char *dst = m->slots + (size_t)ri * m->slot_capacity;
+    unsigned char *dst = m->slots + (size_t)si * m->slot_capacity;
     const unsigned char *src = m->blocks[tb].experts;
     int misses = n;
     if (m->cache) {
@@ -318,46 +372,54 @@ static int issue_fetch(pgmoe_model *m, int tb, int ri) {
     }
     tl_end(m, m->copy);
     if (!m->cp_b.empty()) PG_CUDA(cudaEventRecord(m->cp_b[tb], m->copy));
-    PG_CUDA(cudaEventRecord(m->ready[ri], m->copy));
+    PG_CUDA(cudaEventRecord(m->ready[si], m->copy));
     m->stats.h2d_bytes += (int64_t)misses * (int64_t)m->rec_bytes;
-    m->slot_used[ri] = true;
+    m->slot_used[si] = true;
     if ((int)m->nact_iter.size() == c.num_blocks) m->nact_iter[tb] = n;
     return PGMOE_OK;
 }
 
 // prefetch_all (scheduler.py:336-342): the whole expert set of block `tb`
 // (one contiguous DMA of E records) into slot `ri`, indexed by expert id.
-static int issue_fetch_all(pgmoe_model *m, int tb, int ri) {
+static int issue_fetch_all(pgmoe_model *m, int tb, int si) {
     const int E = m->e_local;
-    if (m->slot_used[ri]) PG_CUDA(cudaStreamWaitEvent(m->copy, m->done[ri], 0));
+    if (m->slot_used[si]) PG_CUDA(cudaStreamWaitEvent(m->copy, m->done[si], 0));
     if (!m->cp_a.empty()) PG_CUDA(cudaEventRecord(m->cp_a[tb], m->copy));
     tl_begin(m, "transfer", "fetch[" + std::to_string(E) + "]", tb, m->copy);
     int misses = E;
     if (m->cache) {
         std::vector<int32_t> all(E);
         for (int e = 0; e < E; ++e) all[e] = e;
-        PG_TRY(fetch_cached(m, tb, all.data(), E, m->slots + (size_t)ri * m->slot_capacity, &misses));
+        PG_TRY(fetch_cached(m, tb, all.data(), E, m->slots + (size_t)si * m->slot_capacity, &misses));
     } else {
-        PG_CUDA(cudaMemcpyAsync(m->slots + (size_t)ri * m->slot_capacity, m->blocks[tb].experts,
+        PG_CUDA(cudaMemcpyAsync(m->slots + (size_t)si * m->slot_capacity, m->blocks[tb].experts,
                                 (size_t)E * m->rec_bytes, cudaMemcpyHostToDevice, m->copy));
         m->stats.h2d_copies++;
     }
     tl_end(m, m->copy);
     if (!m->cp_b.empty()) PG_CUDA(cudaEventRecord(m->cp_b[tb], m->copy));
-    PG_CUDA(cudaEventRecord(m->ready[ri], m->copy));
+    PG_CUDA(cudaEventRecord(m->ready[si], m->copy));
     m->stats.h2d_bytes += (int64_t)misses * (int64_t)m->rec_bytes;
-    m->slot_used[ri] = true;
+    m->slot_used[si] = true;
     if ((int)m->nact_iter.size() == m->cfg.num_blocks) m->nact_iter[tb] = E;
     return PGMOE_OK;
 }
 
+// Routing decision of block `target` into ring buffer `ri`: the gate (K1)
+// on x, or — supplied decisions — the given ids/w of that block.
 static int route_into(pgmoe_model *m, const float *x, int T, const void *G, int ri, bool mirror,
-                      cudaStream_t s, const char *label, int block) {
+                      cudaStream_t s, const char *label, int block, const pgmoe_iteration_io &io, int target) {
     const auto &c = m->cfg;
     RoutingBuf &rb = m->routing[ri];
     tl_begin(m, "compute", label, block, s);
-    PG_TRY(pgmoe_gate_forward(x, T, c.d_model, G, m->wdtype, c.num_experts, c.top_k, &rb.r, m->route_ws,
-                              reinterpret_cast<pgmoe_stream_t>(s)));
+    if (io.ids_supplied) {
+        const size_t o = (size_t)target * T * c.top_k;
+        PG_TRY(pgmoe_route_from_decisions(io.ids_supplied + o, io.w_supplied + o, T, c.num_experts, c.top_k, &rb.r,
+                                          reinterpret_cast<pgmoe_stream_t>(s)));
+    } else {
+        PG_TRY(pgmoe_gate_forward(x, T, c.d_model, G, m->wdtype, c.num_experts, c.top_k, &rb.r, m->route_ws,
+                                  reinterpret_cast<pgmoe_stream_t>(s)));
+    }
     tl_end(m, s);
     if (mirror) {
         PG_CUDA(cudaMemcpyAsync(rb.act_host, rb.r.act, sizeof(int32_t) * (c.num_experts + 1),
@@ -381,7 +443,7 @@ static FusedRoute fused_route_args(pgmoe_model *m, const float *x, int T, const 
     r.T = T;
     r.k = c.top_k;
     route_bound_constants(r.d, &r.gam, &r.bscale);
-    r.splits = fused_route_splits(T, c.d_model, kNumSMs);
+    r.splits = fused_route_splits(T, c.d_model, device_sm_count());
     r.tiles = (T + kRouterTok - 1) / kRouterTok;
     r.x = x;
     r.G = G;
@@ -399,9 +461,13 @@ static FusedRoute fused_route_args(pgmoe_model *m, const float *x, int T, const 
     return r;
 }
 
-int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, int32_t *ids_trace,
-                      float *w_trace, cudaStream_t s) {
+int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, const pgmoe_iteration_io &io,
+                      cudaStream_t s) {
     const auto &c = m->cfg;
+    int32_t *ids_trace = io.ids_trace;
+    float *w_trace = io.w_trace;
+    PG_REQUIRE((io.ids_supplied == nullptr) == (io.w_supplied == nullptr), PGMOE_E_ROUTING,
+               "supplied decisions need both expert ids and combine weights");
     PG_REQUIRE(T >= 0 && T <= m->max_tokens, PGMOE_E_SHAPE, "T=%d exceeds max_tokens=%d", T,
                m->max_tokens);
     PG_REQUIRE(m->e_local == c.num_experts, PGMOE_E_CONFIG,
@@ -409,6 +475,7 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
                m->e_begin + m->e_local);
     if (T == 0) return PGMOE_OK;
     const int L = c.activation_level, R = L + 1, nb = c.num_blocks;
+    const int NS = std::max(1, m->nslots);  // expert slots (offloaded)
     const bool off = m->placement == PGMOE_OFFLOADED;
     const size_t tk = (size_t)T * c.top_k;
     if (m->timeline && !m->t0_recorded) {  // events accumulate until set_timeline() resets them
@@ -434,7 +501,7 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
     // (~E·d·f weight bytes): measured crossover T ≈ f/8 (Base-64 fused
     // better through T=384, separate at 512; Large-128 fused through 768,
     // even at 1024; tools/gpu_env_sweep.sh VAR=PGMOE_FUSE_MAX_T).
-    const bool fuse_route = !off && use_tc(m) && c.top_k == 1 && L == 1 && m->fuse_route &&
+    const bool fuse_route = !off && !io.ids_supplied && use_tc(m) && c.top_k == 1 && L == 1 && m->fuse_route &&
                             fused_route_supported(c.num_experts) &&
                             (long long)T <= (m->fuse_max_t > 0 ? m->fuse_max_t : c.d_ff / 8);
     const float *cur = x_in;
@@ -445,15 +512,19 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
     if (chain) PG_CUDA(cudaMemsetAsync(m->epoch, 0, sizeof(int), s));
     for (int b = 0; b < nb; ++b) {
         const BlockW &bw = m->blocks[b];
-        const int ri = b % R;
+        const int ri = b % R;   // routing buffer of the decision block b consumes
+        const int si = b % NS;  // expert slot of block b (offloaded)
         int pending_fetch = -1;
-        if (prefetch_all) {
+        if (prefetch_all) {  // NS >= 2: block b+1's set never lands in the slot block b reads
             if (b == 0) PG_TRY(issue_fetch_all(m, 0, 0));
-            if (b + 1 < nb) PG_TRY(issue_fetch_all(m, b + 1, (b + 1) % R));
+            if (b + 1 < nb) PG_TRY(issue_fetch_all(m, b + 1, (b + 1) % NS));
         }
+        if (io.x_trace)  // the block input, for teacher-forced parity at this exact launch sequence
+            PG_CUDA(cudaMemcpyAsync(io.x_trace + (size_t)b * T * c.d_model, cur, (size_t)T * c.d_model * 4,
+                                    cudaMemcpyDeviceToDevice, s));
         if (has_conv_gate(c, b)) {
-            PG_TRY(route_into(m, cur, T, bw.gate, ri, off && !prefetch_all, s, "gate", b));
-            if (off && strat == PGMOE_PRE_GATED) PG_TRY(issue_fetch(m, b, ri));  // exposed serial fetch
+            PG_TRY(route_into(m, cur, T, bw.gate, ri, off && !prefetch_all, s, "gate", b, io, b));
+            if (off && strat == PGMOE_PRE_GATED) PG_TRY(issue_fetch(m, b, ri, si));  // exposed serial fetch
         }
         FusedRoute fr{};
         if (has_pre_gate(c, b)) {
@@ -461,19 +532,19 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
             if (fuse_route) {
                 fr = fused_route_args(m, cur, T, bw.pre_gate, m->routing[tr].r, b & 1);
             } else {
-                PG_TRY(route_into(m, cur, T, bw.pre_gate, tr, off && !prefetch_all, s, "pre_gate", b));
+                PG_TRY(route_into(m, cur, T, bw.pre_gate, tr, off && !prefetch_all, s, "pre_gate", b, io, b + L));
             }
             if (off && strat == PGMOE_PRE_GATED) pending_fetch = b + L;
         }
         if (off && strat == PGMOE_ON_DEMAND) {  // fetch starts once compute reaches block b
             PG_CUDA(cudaEventRecord(m->gated, s));
             PG_CUDA(cudaStreamWaitEvent(m->copy, m->gated, 0));
-            PG_TRY(issue_fetch(m, b, ri));
+            PG_TRY(issue_fetch(m, b, ri, si));
         }
         const RoutingBuf &rb = m->routing[ri];
-        const void *experts = off ? (const void *)(m->slots + (size_t)ri * m->slot_capacity)
+        const void *experts = off ? (const void *)(m->slots + (size_t)si * m->slot_capacity)
                                   : (const void *)bw.experts;
-        if (off) PG_CUDA(cudaStreamWaitEvent(s, m->ready[ri], 0));
+        if (off) PG_CUDA(cudaStreamWaitEvent(s, m->ready[si], 0));
         float *nxt = (b == nb - 1) ? y_out : m->act_buf[b & 1];
         // Pre-gating at work: block b+1's routing is already on the device
         // (unless b+1 carries a conventional gate), so this block's dense
@@ -492,7 +563,7 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
             if (fr.active) m->fused_routes++;
             tl_end(m, s);
             if (off) {
-                PG_CUDA(cudaEventRecord(m->done[ri], s));
+                PG_CUDA(cudaEventRecord(m->done[si], s));
                 if (!m->ffn_b.empty()) PG_CUDA(cudaEventRecord(m->ffn_b[b], s));
             }
             tl_begin(m, "compute", "non_moe", b, s);  // fused into the launch above
@@ -503,7 +574,7 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
             PG_TRY(run_ffn(m, cur, T, experts, indexed, &rb.r, s, xb_ready));
             tl_end(m, s);
             if (off) {
-                PG_CUDA(cudaEventRecord(m->done[ri], s));
+                PG_CUDA(cudaEventRecord(m->done[si], s));
                 if (!m->ffn_b.empty()) PG_CUDA(cudaEventRecord(m->ffn_b[b], s));
             }
             tl_begin(m, "compute", "non_moe", b, s);
@@ -515,7 +586,7 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, in
             PG_CUDA(cudaMemcpyAsync(ids_trace + (size_t)b * tk, rb.r.ids, tk * 4, cudaMemcpyDeviceToDevice, s));
             PG_CUDA(cudaMemcpyAsync(w_trace + (size_t)b * tk, rb.r.w, tk * 4, cudaMemcpyDeviceToDevice, s));
         }
-        if (pending_fetch >= 0) PG_TRY(issue_fetch(m, pending_fetch, pending_fetch % R));
+        if (pending_fetch >= 0) PG_TRY(issue_fetch(m, pending_fetch, pending_fetch % R, pending_fetch % NS));
         cur = nxt;
     }
     return PGMOE_OK;
@@ -540,19 +611,23 @@ extern "C" int pgmoe_debug_set_probe(int32_t kind, void *device_buffer, int64_t 
 // tickets and partials, re-armed by each launch's last CTA, so calls that
 // share one must be stream-ordered.  Allocated once per process, under a
 // lock (EP ranks may be threads of one process).
+// One set per device: models or EP ranks on other GPUs of the same process
+// must not share device-0 memory.
 constexpr size_t kSharedWsBytes = 64ull << 20;
 static int shared_tc_ws(int slot, void **out) {
     static std::mutex mu;
-    static void *ws[3] = {nullptr, nullptr, nullptr};
+    static void *ws[64][3] = {};
+    const int dev = current_device();
+    PG_REQUIRE(dev >= 0 && dev < 64, PGMOE_E_CONFIG, "device ordinal %d unsupported", dev);
     std::lock_guard<std::mutex> lock(mu);
-    if (!ws[slot]) {
+    if (!ws[dev][slot]) {
         void *p = nullptr;
         PG_CUDA(cudaMalloc(&p, kSharedWsBytes));
         PG_CUDA(cudaMemset(p, 0, kSharedWsBytes));
         PG_CUDA(cudaDeviceSynchronize());
-        ws[slot] = p;
+        ws[dev][slot] = p;
     }
-    *out = ws[slot];
+    *out = ws[dev][slot];
     return PGMOE_OK;
 }
 
@@ -669,6 +744,7 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
         }
         for (size_t b = 0; b < nb; ++b) m->blocks[b].experts = m->host_pool + b * E * m->rec_bytes;
         const int R = c.activation_level + 1;
+        m->nslots = R;
         m->slot_experts = (int)std::min<size_t>(E, (size_t)max_tokens * k);
         m->slot_capacity = (size_t)m->slot_experts * m->rec_bytes;
         if (cudaMalloc(&m->slots, m->slot_capacity * R) != cudaSuccess) {
@@ -696,7 +772,7 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
     }
     size_t rws = pgmoe_route_workspace_bytes(max_tokens, c.num_experts);
     for (int t = 1; t <= max_tokens; ++t)  // the routing role fused into the block kernel (resident)
-        rws = std::max(rws, kFusedRouteHead + fused_route_ws_bytes(t, d, c.num_experts, kNumSMs));
+        rws = std::max(rws, kFusedRouteHead + fused_route_ws_bytes(t, d, c.num_experts, device_sm_count()));
     if (cudaMalloc(&m->route_ws, rws) != cudaSuccess || cudaMemset(m->route_ws, 0, rws) != cudaSuccess)
         return fail(PGMOE_E_OOM);
     const size_t T = max_tokens;
@@ -783,13 +859,15 @@ extern "C" int pgmoe_model_set_strategy(pgmoe_model *m, int32_t strategy) {
     PG_REQUIRE(strategy != PGMOE_PRE_GATED || m->cfg.activation_level >= 1, PGMOE_E_CONFIG,
                "pre_gated strategy requires a model with activation_level >= 1");
     std::lock_guard<std::mutex> g(m->mu);
-    if (strategy == PGMOE_PREFETCH_ALL && m->slot_experts < m->e_local) {  // slots must hold a whole block
+    // prefetch_all: slots hold a whole block, and there are at least two of
+    // them (block b+1's set streams in while block b reads its own)
+    const int ns_need = std::max(m->cfg.activation_level + 1, 2);
+    if (strategy == PGMOE_PREFETCH_ALL && (m->slot_experts < m->e_local || m->nslots < ns_need)) {
         PG_CUDA(cudaDeviceSynchronize());
-        const int R = m->cfg.activation_level + 1;
         const size_t cap = (size_t)m->e_local * m->rec_bytes;
         unsigned char *ns = nullptr;
-        if (cudaMalloc(&ns, cap * R) != cudaSuccess) {
-            set_error("OOM: %zu B of HBM for %d whole-block expert slots", cap * R, R);
+        if (cudaMalloc(&ns, cap * ns_need) != cudaSuccess) {
+            set_error("OOM: %zu B of HBM for %d whole-block expert slots", cap * ns_need, ns_need);
             return PGMOE_E_OOM;
         }
         cudaFree(m->slots);
@@ -797,7 +875,14 @@ extern "C" int pgmoe_model_set_strategy(pgmoe_model *m, int32_t strategy) {
         m->slot_capacity = cap;
         m->slot_experts = m->e_local;
         m->stats.slot_capacity_bytes = (int64_t)cap;
-        m->slot_used.assign(R, false);
+        for (int i = m->nslots; i < ns_need; ++i) {
+            m->ready.push_back(nullptr);
+            m->done.push_back(nullptr);
+            cudaEventCreateWithFlags(&m->ready.back(), cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&m->done.back(), cudaEventDisableTiming);
+        }
+        m->nslots = ns_need;
+        m->slot_used.assign(ns_need, false);
     }
     m->strategy = strategy;
     return PGMOE_OK;
@@ -969,12 +1054,17 @@ extern "C" const void *pgmoe_model_matrix_ptr(pgmoe_model *m, const char *name, 
 // Resident iterations have no host round trip, so the whole block loop
 // (route, pack, up, down, dense per block; PDL edges between them) is
 // captured once per buffer set and replayed as one graph launch.
-static int decoder_iteration_graph(pgmoe_model *m, const float *x_in, int T, float *y_out, int32_t *ids,
-                                   float *w, cudaStream_t s) {
+static bool same_io(const pgmoe_iteration_io &a, const pgmoe_iteration_io &b) {
+    return a.ids_trace == b.ids_trace && a.w_trace == b.w_trace && a.x_trace == b.x_trace &&
+           a.ids_supplied == b.ids_supplied && a.w_supplied == b.w_supplied;
+}
+
+static int decoder_iteration_graph(pgmoe_model *m, const float *x_in, int T, float *y_out,
+                                   const pgmoe_iteration_io &io, cudaStream_t s) {
     ++m->graph_clock;
     pgmoe_model::GraphEntry *victim = &m->graphs[0];
     for (auto &g : m->graphs) {
-        if (g.exec && g.x == x_in && g.y == y_out && g.T == T && g.ids == ids && g.w == w) {
+        if (g.exec && g.x == x_in && g.y == y_out && g.T == T && same_io(g.io, io)) {
             g.last_use = m->graph_clock;
             PG_CUDA(cudaGraphLaunch(g.exec, s));
             count_launch((int)g.launches);
@@ -989,7 +1079,7 @@ static int decoder_iteration_graph(pgmoe_model *m, const float *x_in, int T, flo
     if (!m->cap) PG_CUDA(cudaStreamCreateWithFlags(&m->cap, cudaStreamNonBlocking));
     const long long l0 = g_launches.load();
     PG_CUDA(cudaStreamBeginCapture(m->cap, cudaStreamCaptureModeThreadLocal));
-    const int st = decoder_iteration(m, x_in, T, y_out, ids, w, m->cap);
+    const int st = decoder_iteration(m, x_in, T, y_out, io, m->cap);
     victim->launches = g_launches.load() - l0;
     cudaGraph_t graph = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(m->cap, &graph);
@@ -1004,32 +1094,58 @@ static int decoder_iteration_graph(pgmoe_model *m, const float *x_in, int T, flo
     victim->x = x_in;
     victim->y = y_out;
     victim->T = T;
-    victim->ids = ids;
-    victim->w = w;
+    victim->io = io;
     victim->last_use = m->graph_clock;
     PG_CUDA(cudaGraphLaunch(victim->exec, s));
     return PGMOE_OK;
 }
 
-extern "C" int pgmoe_decoder_iteration(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
-                                       int32_t *ids_trace, float *w_trace, pgmoe_stream_t stream) {
+extern "C" int pgmoe_decoder_iteration_ex(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
+                                          const pgmoe_iteration_io *io_in, pgmoe_stream_t stream) {
     PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
     std::lock_guard<std::mutex> g(m->mu);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const pgmoe_iteration_io io = io_in ? *io_in : pgmoe_iteration_io{};
     if (m->placement == PGMOE_RESIDENT && m->use_graph && !m->timeline && T > 0 && T <= m->max_tokens &&
         m->e_local == m->cfg.num_experts)
-        return decoder_iteration_graph(m, x_in, T, y_out, ids_trace, w_trace, s);
-    return decoder_iteration(m, x_in, T, y_out, ids_trace, w_trace, s);
+        return decoder_iteration_graph(m, x_in, T, y_out, io, s);
+    return decoder_iteration(m, x_in, T, y_out, io, s);
 }
 
+extern "C" int pgmoe_decoder_iteration(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
+                                       int32_t *ids_trace, float *w_trace, pgmoe_stream_t stream) {
+    pgmoe_iteration_io io{};
+    io.ids_trace = ids_trace;
+    io.w_trace = w_trace;
+    return pgmoe_decoder_iteration_ex(m, x_in, T, y_out, &io, stream);
+}
+
+// Surfaces (and clears) a device-detected routing error of any ring buffer:
+// the error belongs to the iteration that raised it, not to later ones.
 static int check_all_routing(pgmoe_model *m) {
+    int first = PGMOE_OK;
+    std::string msg;
     for (auto &rb : m->routing) {
-        int32_t fb = 0, fl = 0;
-        int st = pgmoe_check_routing(&rb.r, &fb, &fl);
+        int32_t fb = 0;
+        int st = pgmoe_check_routing(&rb.r, &fb);
         m->stats.route_fallbacks = std::max<int64_t>(m->stats.route_fallbacks, fb);
-        if (st != PGMOE_OK) return st;
+        if (st != PGMOE_OK) {
+            if (first == PGMOE_OK) {
+                first = st;
+                msg = g_last_error;
+            }
+            PG_CUDA(cudaMemset(rb.r.status, 0, sizeof(int32_t)));
+        }
     }
-    return PGMOE_OK;
+    if (first != PGMOE_OK) g_last_error = msg;
+    return first;
+}
+
+extern "C" int pgmoe_model_check_routing(pgmoe_model *m) {
+    PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
+    std::lock_guard<std::mutex> g(m->mu);
+    PG_CUDA(cudaDeviceSynchronize());
+    return check_all_routing(m);
 }
 
 extern "C" int pgmoe_decoder_iteration_host(pgmoe_model *m, const float *x_in, int32_t T, float *y_out,
@@ -1091,6 +1207,7 @@ extern "C" int pgmoe_moe_block_forward(pgmoe_model *m, int32_t block, const floa
     const void *experts = bw.experts;
     int indexed = 0;
     if (m->placement == PGMOE_OFFLOADED) {  // on-demand fetch into slot 0
+        PG_CUDA(cudaStreamSynchronize(m->copy));  // no decoder migration still writing the slot
         int32_t nact = 0;
         PG_CUDA(cudaMemcpyAsync(m->routing[0].act_host, r_in->act, sizeof(int32_t) * (c.num_experts + 1),
                                 cudaMemcpyDeviceToHost, s));
@@ -1164,7 +1281,6 @@ extern "C" int pgmoe_model_stats(pgmoe_model *m, pgmoe_stats *out) {
         if (cudaMemcpy(st, rb.r.status, sizeof(st), cudaMemcpyDeviceToHost) == cudaSuccess) fb += st[1];
     }
     m->stats.route_fallbacks = fb;
-    m->stats.route_flips = 0;
     m->stats.fused_blocks = m->fused_blocks;
     m->stats.fused_routes = m->fused_routes;
     *out = m->stats;
