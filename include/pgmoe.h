@@ -51,7 +51,7 @@ typedef enum {
     PGMOE_E_INVARIANT = 10       /* InvariantError       (scheduler.py:127-145) */
 } pgmoe_status;
 
-typedef enum { PGMOE_F32 = 0, PGMOE_BF16 = 1 } pgmoe_dtype;
+typedef enum { PGMOE_F32 = 0, PGMOE_BF16 = 1, PGMOE_F64 = 2 /* gate weights of pgmoe_gate_forward_f64 only */ } pgmoe_dtype;
 typedef enum { PGMOE_RESIDENT = 0, PGMOE_OFFLOADED = 1 } pgmoe_placement;
 typedef enum { PGMOE_KERNEL_AUTO = 0, PGMOE_KERNEL_SIMT = 1, PGMOE_KERNEL_TCGEN05 = 2 } pgmoe_kernel;
 /* Expert migration policy of an offloaded model (scheduler.py:36-49).  The
@@ -94,6 +94,15 @@ PGMOE_API size_t pgmoe_route_workspace_bytes(int32_t T, int32_t E);
 PGMOE_API int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const void *gate_w,
                        int32_t wdtype, int32_t E, int32_t k, const pgmoe_routing *out,
                        void *workspace, pgmoe_stream_t stream);
+
+/* K1 at the reference's own precision: x fp64 [T][d] and gate_w fp64 [d][E]
+ * (moesim's init_model matrices and inputs are fp64 Python floats,
+ * core.py:200-211, :274-277).  Products are no longer exact in fp64, so
+ * the certification bound takes one more rounding (gamma_{d+1}); the serial
+ * fallback is the same __dadd_rn(__dmul_rn) loop.  Ids equal moesim's
+ * gate_forward bit-for-bit on unrounded inputs.  Same workspace as above. */
+PGMOE_API int pgmoe_gate_forward_f64(const double *x, int32_t T, int32_t d, const double *gate_w, int32_t E,
+                                     int32_t k, const pgmoe_routing *out, void *workspace, pgmoe_stream_t stream);
 
 /* K2 grouped expert FFN with fused combine.  Replaces expert_forward
  * (core.py:308-316) x k plus weighted_sum (linalg.py:45-51): for every

@@ -219,8 +219,12 @@ class DeviceRouting:
 
 def route(x: torch.Tensor, gate_w: torch.Tensor, k: int, out: DeviceRouting | None = None,
           stream=None) -> DeviceRouting:
-    """K1 on T tokens: x fp32 [T][d] (cuda), gate_w [d][E] fp32/bf16 (cuda)."""
+    """K1 on T tokens: x fp32 [T][d] (cuda), gate_w [d][E] fp32/bf16 (cuda);
+    or x and gate_w both fp64 — the reference's own precision
+    (pgmoe_gate_forward_f64)."""
     _require_cuda()
+    if x.dim() == 2 and x.is_cuda and x.dtype == torch.float64 and gate_w.dtype == torch.float64:
+        return _route64(x, gate_w, k, out, stream)
     if x.dim() != 2 or x.dtype != torch.float32 or not x.is_cuda:
         raise ShapeError("route expects x as a cuda float32 [T][d] tensor")
     d, E = gate_w.shape
@@ -235,6 +239,21 @@ def route(x: torch.Tensor, gate_w: torch.Tensor, k: int, out: DeviceRouting | No
     gate_w = gate_w.contiguous()
     _lib.check(_lib.load().pgmoe_gate_forward(_ptr(x), T, d, _ptr(gate_w), wdt, E, k, ctypes.byref(out.c),
                                               _ptr(out.workspace), _stream(stream)))
+    return out
+
+
+def _route64(x, gate_w, k, out, stream):
+    d, E = gate_w.shape
+    if k > E:
+        raise ConfigError(f"k={k} exceeds expert count {E}")
+    if x.shape[1] != d:
+        raise ShapeError(f"gate expects input of width {d}, got {x.shape[1]}")
+    T = x.shape[0]
+    out = out if out is not None else DeviceRouting(T, E, k, x.device)
+    x = x.contiguous()
+    gate_w = gate_w.contiguous()
+    _lib.check(_lib.load().pgmoe_gate_forward_f64(_ptr(x), T, d, _ptr(gate_w), E, k, ctypes.byref(out.c),
+                                                  _ptr(out.workspace), _stream(stream)))
     return out
 
 
@@ -498,43 +517,60 @@ def _wrap_device_ptr(ptr: int, numel: int, dtype: torch.dtype) -> torch.Tensor:
 # ------------------------------------------- drop-ins (reference API) -----
 
 _dev_cache: dict = {}
+# The decision type the drop-ins return: this module's RoutingDecision, or —
+# once dropin.install() points moesim at these functions — moesim's own.
+DECISION_TYPE = RoutingDecision
 
 
 def clear_cache() -> None:
     _dev_cache.clear()
 
 
-def _dev_matrix(mat) -> torch.Tensor:
-    """Device fp32 copy of a reference list-of-lists matrix (cached by id)."""
+def _dev_matrix(mat, dtype=torch.float32) -> torch.Tensor:
+    """Device copy of a reference list-of-lists matrix (cached by id and
+    dtype).  Torch tensors pass through in their own dtype."""
     if isinstance(mat, torch.Tensor):
         return mat.cuda() if not mat.is_cuda else mat
-    key = id(mat)
+    key = (id(mat), dtype)
     hit = _dev_cache.get(key)
     if hit is not None and hit[0] is mat:
         return hit[1]
-    t = torch.tensor(np.asarray(mat, dtype=np.float32), device="cuda")
+    npdt = np.float64 if dtype == torch.float64 else np.float32
+    t = torch.tensor(np.asarray(mat, dtype=npdt), device="cuda")
     _dev_cache[key] = (mat, t)
     return t
 
 
-def _dev_vec(x) -> torch.Tensor:
+def _dev_vec(x, dtype=torch.float32) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
-        return x.to(device="cuda", dtype=torch.float32).reshape(1, -1)
-    return torch.tensor(np.asarray(x, dtype=np.float32), device="cuda").reshape(1, -1)
+        return x.to(device="cuda", dtype=dtype).reshape(1, -1)
+    npdt = np.float64 if dtype == torch.float64 else np.float32
+    return torch.tensor(np.asarray(x, dtype=npdt), device="cuda").reshape(1, -1)
 
 
 def gate_forward(x, gate_weights, k: int) -> RoutingDecision:
-    """Drop-in for core.py:284-305 (one token) on the K1 kernel."""
-    G = _dev_matrix(gate_weights)
+    """Drop-in for core.py:284-305 (one token) on the K1 kernel.
+
+    The reference's inputs (Python floats, numpy float64, or fp64 tensors)
+    route at fp64 through pgmoe_gate_forward_f64, so ids equal moesim's
+    bit-for-bit on its own unrounded init_model weights; fp32 / bf16 tensors
+    route through the fp32 kernel (exact products)."""
+    if isinstance(gate_weights, torch.Tensor) and gate_weights.dtype != torch.float64:
+        G = _dev_matrix(gate_weights)
+        xv = _dev_vec(x)
+    else:
+        G = _dev_matrix(gate_weights, torch.float64)
+        xv = _dev_vec(x, torch.float64)
     E = G.shape[1] if G.dim() == 2 and G.shape[0] else 0
     if k > E:
         raise ConfigError(f"k={k} exceeds expert count {E}")
-    xv = _dev_vec(x)
     if G.shape[0] != xv.shape[1]:
         raise ShapeError(f"gate expects input of width {G.shape[0]}, got {xv.shape[1]}")
     r = route(xv, G, k)
     r.check()
-    return r.decisions()[0]
+    ids = r.ids.cpu().tolist()[0]
+    w = r.w.double().cpu().tolist()[0]
+    return DECISION_TYPE(tuple(ids), tuple(w))
 
 
 def expert_forward(x, expert) -> list:

@@ -40,7 +40,7 @@ constexpr int kMaxTiles = 8192;
 constexpr int kMaxSplits = 64;
 
 struct RouteParams {
-    const float *x;
+    const void *x;  // [T][d] fp32, or fp64 (the drop-in's reference-precision inputs)
     const void *G;
     int T, d, E, k;
     int tok;      // tokens per logits CTA
@@ -55,16 +55,20 @@ struct RouteParams {
 };
 
 // Phase 2: tokens [tok0, tok0+ntok) of tile `tile`, all splits present.
-template <typename GT>
+template <typename GT, typename XT>
 __device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, unsigned char *smem_raw) {
     const int d = p.d, E = p.E, k = p.k;
     const GT *G = static_cast<const GT *>(p.G);
+    const XT *X = static_cast<const XT *>(p.x);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double *logit = reinterpret_cast<double *>(smem_raw) + (size_t)warp * 2 * E;
     double *bound = logit + E;
     __shared__ double s_xsum[kSelectWarps];
     const double u = 1.1102230246251565e-16;  // 2^-53
-    const double gam = (double)d * u / (1.0 - (double)d * u);
+    // fp32/bf16 operands: products exact, d - 1 roundings on either side;
+    // fp64 operands: one more (the product), gamma_{d+1}
+    const double nd = (double)d + (std::is_same<GT, double>::value || std::is_same<XT, double>::value ? 1.0 : 0.0);
+    const double gam = nd * u / (1.0 - nd * u);
     const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
     const double bpad = 1e-300;  // products are exact in fp64: no underflow below ~1e-90
     // sum_i |x_i G_ij| <= (sum_i |x_i|) * max_i |G_ij|; the split CTAs
@@ -155,7 +159,7 @@ __device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, 
                     if (lg[j] + bd[j] >= minlow) cand |= 1u << q;
                 __syncwarp();
                 for (int j = lane, q = 0; j < E; j += 32, ++q)
-                    if (cand >> q & 1u) lg[j] = serial_logit<GT>(p.x + (size_t)tok * d, G, d, E, j);
+                    if (cand >> q & 1u) lg[j] = serial_logit<GT, XT>(X + (size_t)tok * d, G, d, E, j);
                 __syncwarp();
                 for (int s = 0; s < k; ++s) {
                     double bf = -INFINITY;
@@ -275,7 +279,7 @@ __device__ void permute_all(const RouteParams &p, unsigned char *smem_raw) {
 // tile / global last-arriver phases.  Products of fp32 activations and
 // fp32/bf16 gate values are exact in fp64, so every DFMA rounds once, like
 // one step of the reference's serial sum.
-template <typename GT, int TOK, bool VECLOAD>
+template <typename GT, typename XT, int TOK, bool VECLOAD>
 __global__ void __launch_bounds__(kLogitThreads)
 route_kernel(const RouteParams p_in) {
     constexpr int V = Vec<GT>::N;
@@ -314,7 +318,8 @@ route_kernel(const RouteParams p_in) {
     if (tid == 0) probe(p.probe, cta, 1);
     for (int i = tid; i < TOK * kn; i += kLogitThreads) {
         const int t = i / kn;
-        xd[i] = (t < ntok) ? (double)__ldg(p.x + (size_t)(t0 + t) * d + k0 + (i - t * kn)) : 0.0;
+        xd[i] = (t < ntok) ? (double)__ldg(static_cast<const XT *>(p.x) + (size_t)(t0 + t) * d + k0 + (i - t * kn))
+                           : 0.0;
     }
     __syncthreads();
     {   // sum |x_i| over this K slice, one warp per token (bounds the logit error)
@@ -354,7 +359,7 @@ route_kernel(const RouteParams p_in) {
 #pragma unroll
                     for (int v = 0; v < V; ++v) {
                         gd[u][v] = (j0 + v < E) ? gval(row, j0 + v) : 0.0;
-                        ga[u][v] = fabsf((float)gd[u][v]);
+                        ga[u][v] = (j0 + v < E) ? gabs_up(row, j0 + v) : 0.f;
                     }
                 }
             }
@@ -410,7 +415,7 @@ route_kernel(const RouteParams p_in) {
     if (!s_last) return;
     __threadfence();
     if (tid == 0) probe(p.probe, cta, 3);  // select start
-    select_tile<GT>(p, tile, t0, ntok, smem_raw);
+    select_tile<GT, XT>(p, tile, t0, ntok, smem_raw);
 
     // ---- phase 3: the last token tile permutes ----------------------------
     __syncthreads();
@@ -462,18 +467,20 @@ static size_t route_smem(int tok, int d, int splits, int E) {
     return std::max(std::max(a, b), std::max(c, e));
 }
 
-template <typename GT, int TOK>
+template <typename GT, typename XT, int TOK>
 static int launch_route(const RouteParams &p, cudaStream_t s) {
     constexpr int V = Vec<GT>::N;
     const size_t smem = route_smem<GT>(TOK, p.d, p.splits, p.E);
     PG_REQUIRE(smem <= 200 * 1024, PGMOE_E_CONFIG, "route: d=%d E=%d exceeds shared memory", p.d, p.E);
     const bool vec = (p.E % V == 0) && (reinterpret_cast<uintptr_t>(p.G) % 16 == 0);
-    auto kern = vec ? route_kernel<GT, TOK, true> : route_kernel<GT, TOK, false>;
-    static size_t attr[2] = {0, 0};
-    if (smem > attr[vec]) {
+    auto kern = vec ? route_kernel<GT, XT, TOK, true> : route_kernel<GT, XT, TOK, false>;
+    static size_t attr[64][2] = {};  // per device
+    const int dev = current_device();
+    PG_REQUIRE(dev >= 0 && dev < 64, PGMOE_E_CONFIG, "device ordinal %d unsupported", dev);
+    if (smem > attr[dev][vec]) {
         const size_t want = std::max<size_t>(smem, 64 * 1024);
         PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want));
-        attr[vec] = want;
+        attr[dev][vec] = want;
     }
     const dim3 grid((p.T + TOK - 1) / TOK, p.splits);
     PG_CUDA(launch_pdl(kern, grid, dim3(kLogitThreads), smem, s, p));
@@ -481,13 +488,13 @@ static int launch_route(const RouteParams &p, cudaStream_t s) {
     return PGMOE_OK;
 }
 
-template <typename GT>
+template <typename GT, typename XT = float>
 static int route_dispatch(RouteParams p, cudaStream_t s) {
     PG_REQUIRE((p.T + p.tok - 1) / p.tok <= kMaxTiles, PGMOE_E_CONFIG, "route: T=%d too large", p.T);
-    if (p.tok == 1) return launch_route<GT, 1>(p, s);
-    if (p.tok == 2) return launch_route<GT, 2>(p, s);
-    if (p.tok == 4) return launch_route<GT, 4>(p, s);
-    return launch_route<GT, 8>(p, s);
+    if (p.tok == 1) return launch_route<GT, XT, 1>(p, s);
+    if (p.tok == 2) return launch_route<GT, XT, 2>(p, s);
+    if (p.tok == 4) return launch_route<GT, XT, 4>(p, s);
+    return launch_route<GT, XT, 8>(p, s);
 }
 
 }  // namespace pgmoe
@@ -508,10 +515,10 @@ extern "C" size_t pgmoe_route_workspace_bytes(int32_t T, int32_t E) {
     return ws_head() + worst + 256;
 }
 
-extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const void *gate_w,
-                                  int32_t wdtype, int32_t E, int32_t k, const pgmoe_routing *out,
-                                  void *workspace, pgmoe_stream_t stream) {
+static int gate_forward_any(const void *x, bool x64, int32_t T, int32_t d, const void *gate_w, int32_t wdtype,
+                            int32_t E, int32_t k, const pgmoe_routing *out, void *workspace, pgmoe_stream_t stream) {
     PG_REQUIRE(out != nullptr && workspace != nullptr, PGMOE_E_CONFIG, "gate_forward: null buffers");
+    PG_REQUIRE(gate_w != nullptr && (x != nullptr || T == 0), PGMOE_E_CONFIG, "gate_forward: null inputs");
     PG_REQUIRE(k <= E, PGMOE_E_CONFIG, "k=%d exceeds expert count %d", k, E);
     PG_REQUIRE(k >= 1 && k <= 8, PGMOE_E_CONFIG, "top_k=%d unsupported (1..8)", k);
     PG_REQUIRE(E >= 1 && E <= 1024, PGMOE_E_CONFIG, "num_experts=%d unsupported (1..1024)", E);
@@ -543,10 +550,30 @@ extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const vo
     const size_t ncm = (size_t)((T + p.tok - 1) / p.tok) * p.splits * E;
     p.pxsum = reinterpret_cast<double *>(ws + ws_head() + ((n * 8 + ncm * 4 + 255) & ~(size_t)255));
     p.probe = probe_buffer(0, ((T + p.tok - 1) / p.tok) * p.splits);
+    if (x64) {
+        PG_REQUIRE(wdtype == PGMOE_F64, PGMOE_E_CONFIG, "fp64 inputs route with fp64 gate weights");
+        return route_dispatch<double, double>(p, s);
+    }
     if (wdtype == PGMOE_BF16) return route_dispatch<uint16_t>(p, s);
     if (wdtype == PGMOE_F32) return route_dispatch<float>(p, s);
     set_error("unknown weight dtype %d", wdtype);
     return PGMOE_E_CONFIG;
+}
+
+extern "C" int pgmoe_gate_forward(const float *x, int32_t T, int32_t d, const void *gate_w, int32_t wdtype,
+                                  int32_t E, int32_t k, const pgmoe_routing *out, void *workspace,
+                                  pgmoe_stream_t stream) {
+    PG_REQUIRE(wdtype == PGMOE_F32 || wdtype == PGMOE_BF16, PGMOE_E_CONFIG,
+               "fp32 activations route with fp32 / bf16 gate weights (fp64: pgmoe_gate_forward_f64)");
+    return gate_forward_any(x, false, T, d, gate_w, wdtype, E, k, out, workspace, stream);
+}
+
+extern "C" int pgmoe_gate_forward_f64(const double *x, int32_t T, int32_t d, const double *gate_w, int32_t E,
+                                      int32_t k, const pgmoe_routing *out, void *workspace,
+                                      pgmoe_stream_t stream) {
+    PG_REQUIRE((reinterpret_cast<uintptr_t>(gate_w) & 15) == 0 || E % 2 != 0, PGMOE_E_CONFIG,
+               "fp64 gate weights must be 16-byte aligned");
+    return gate_forward_any(x, true, T, d, gate_w, PGMOE_F64, E, k, out, workspace, stream);
 }
 
 extern "C" int pgmoe_check_routing(const pgmoe_routing *r, int32_t *fallbacks) {

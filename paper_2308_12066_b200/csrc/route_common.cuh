@@ -82,7 +82,22 @@ template <> struct Vec<float> {
     }
     __device__ __forceinline__ static double one(const float *p) { return __ldg(p); }
 };
+// fp64 gate weights (the reference's own init_model matrices, unrounded):
+// products are no longer exact, so the bound takes one more rounding
+// (gamma_{d+1}); |g| is rounded UP to fp32 for the column max.
+template <> struct Vec<double> {
+    static constexpr int N = 2;
+    __device__ __forceinline__ static void load(const double *p, double (&d)[2], float (&a)[2]) {
+        const double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+        d[0] = v.x; d[1] = v.y;
+        a[0] = __double2float_ru(fabs(v.x)); a[1] = __double2float_ru(fabs(v.y));
+    }
+    __device__ __forceinline__ static double one(const double *p) { return __ldg(p); }
+};
 template <typename GT> __device__ __forceinline__ double gval(const GT *G, size_t i) { return Vec<GT>::one(G + i); }
+template <typename GT> __device__ __forceinline__ float gabs_up(const GT *G, size_t i) {
+    return std::is_same<GT, double>::value ? __double2float_ru(fabs(gval(G, i))) : fabsf((float)gval(G, i));
+}
 // Two adjacent experts per load (the routing role's partial logits: 128
 // threads x 2 experts cover a token group, so each warp's dependent FP64
 // chain per gate row is half as long as with 4 experts per thread).
@@ -109,8 +124,8 @@ template <> struct Vec2<float> {
 // Serial fp64 logit in the reference order (linalg.py:35-37): out += x_i*G_ij.
 // Not inlined: the rare uncertified path would otherwise put NJ unrolled
 // copies of this loop into the routing role's instruction stream.
-template <typename GT>
-__device__ __noinline__ double serial_logit(const float *x, const GT *G, int d, int E, int j) {
+template <typename GT, typename XT>
+__device__ __noinline__ double serial_logit(const XT *x, const GT *G, int d, int E, int j) {
     double acc = 0.0;
     for (int i = 0; i < d; ++i) acc = __dadd_rn(acc, __dmul_rn((double)x[i], gval(G, (size_t)i * E + j)));
     return acc;
@@ -449,7 +464,7 @@ __device__ void router_select_token(const FusedRoute &r, const TileSums &ts, int
         const GT *G = static_cast<const GT *>(r.G);
 #pragma unroll
         for (int jj = 0; jj < NJ; ++jj)
-            if (cand >> jj & 1u) lg[jj] = serial_logit<GT>(r.x + (size_t)tok * d, G, d, E, lane + 32 * jj);
+            if (cand >> jj & 1u) lg[jj] = serial_logit<GT, float>(r.x + (size_t)tok * d, G, d, E, lane + 32 * jj);
         for (int s = 0; s < k; ++s) {
             double bf = -INFINITY;
             int bi = -1;

@@ -75,9 +75,12 @@ int device_sm_count() {
             q == cudaDriverEntryPointSuccess)
             get_res = reinterpret_cast<GetRes>(p);
     }
-    cudaFree(nullptr);  // make sure a context is current
     CUcontext ctx = nullptr;
     if (get_cur) get_cur(&ctx);
+    if (!ctx && get_cur) {  // no context yet: create the primary one (never reached during stream capture)
+        cudaFree(nullptr);
+        get_cur(&ctx);
+    }
     for (auto &e : cache)
         if (e.first == ctx) return e.second;
     int n = 0;

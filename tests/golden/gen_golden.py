@@ -212,6 +212,39 @@ def switch_fixture():
     return out
 
 
+def gate_f64_fixture():
+    """The reference's gate at ITS OWN precision: moesim's unrounded fp64
+    init_model weights and fp64 inputs (core.py:200-211, :274-277), Switch
+    Large-128 shapes, plus planted exact and 1-ulp near ties.  Pins the
+    drop-in's fp64 routing (pgmoe_gate_forward_f64)."""
+    out = []
+    large = moesim.ModelConfig(d_model=1024, d_ff=4096, num_blocks=24, num_experts=128, top_k=1, seed=0)
+    params = mcore.init_model(large)
+    dims = og.Dims(1024, 4096, 24, 128, 1)
+    for b in (0, 5, 22):
+        blk = params.blocks[b]
+        which = "gate" if b == 0 else "pre_gate"
+        G = blk.gate if b == 0 else blk.pre_gate
+        for t in range(6):
+            x = og.token_input(dims, t + 7 * b).tolist()  # fp64, unrounded
+            for k in (1, 2):
+                r = moesim.gate_forward(x, G, k)
+                out.append({"block": b, "which": which, "token": t + 7 * b, "k": k, "tie": None,
+                            "ids": list(r.expert_ids), "w": hxl(r.combine_weights)})
+    # near ties: column 9 := column 3 (exact tie), column 40 := column 3 with one
+    # element moved by one ulp; x chosen so that column 3 wins
+    G = [list(row) for row in params.blocks[5].pre_gate]
+    for i, row in enumerate(G):
+        row[9] = row[3]
+        row[40] = row[3] if i != 100 else float(np.nextafter(row[3], 1.0))
+    x = [0.05 if row[3] >= 0 else -0.05 for row in G]
+    for k in (1, 2, 3):
+        r = moesim.gate_forward(x, G, k)
+        out.append({"block": 5, "which": "pre_gate", "token": -1, "k": k, "tie": [3, 9, 40],
+                    "x": hxl(x), "ids": list(r.expert_ids), "w": hxl(r.combine_weights)})
+    return out
+
+
 def pgmoe1_fixture():
     """A PGMOE1 file written by the reference's own save_model (model_io.py:39-60)."""
     from moesim.model_io import save_model
@@ -238,7 +271,9 @@ def cache_fixture():
 
 
 def main():
-    pgmoe1_fixture()
+    only = sys.argv[1:]  # optional: names of the fixtures to (re)generate
+    if not only:
+        pgmoe1_fixture()
     fixtures = {
         "rng.json": rng_fixture,
         "linalg.json": linalg_fixture,
@@ -246,7 +281,10 @@ def main():
         "decoder_small.json": small_decoder_fixture,
         "switch.json": switch_fixture,
         "cache.json": cache_fixture,
+        "gate_f64.json": gate_f64_fixture,
     }
+    if only:
+        fixtures = {k: v for k, v in fixtures.items() if k in only}
     meta = {"generator": "tests/golden/gen_golden.py", "reference": "moesim " + moesim.__version__,
             "python": sys.version.split()[0]}
     for name, fn in fixtures.items():

@@ -163,3 +163,30 @@ def test_permutation_is_stable_counting_sort():
     assert hist.tolist() == np.bincount(flat, minlength=16).tolist()
     assert act.tolist() == [e for e in range(16) if hist[e] > 0]
     assert off[-1] == flat.size
+
+
+def gate_f64_case(c):
+    """(x fp64, G fp64, k) of a gate_f64.json case: moesim's unrounded
+    init_model weights (core.py:200-211) regenerated by the oracle's RNG."""
+    dims = og.Dims(1024, 4096, 24, 128, 1)
+    tag = og.TAG_GATE if c["which"] == "gate" else og.TAG_PRE_GATE
+    G = og.weights(og.derive_seed(0, tag, c["block"], -1), 1024, 128, "f64")
+    if c["tie"]:
+        G = G.copy()
+        G[:, 9] = G[:, 3]
+        G[:, 40] = G[:, 3]
+        G[100, 40] = np.nextafter(G[100, 3], 1.0)
+        x = fxa(c["x"])
+    else:
+        x = og.token_input(dims, c["token"])
+    return x, G, c["k"]
+
+
+def test_gate_fp64_switch_matches_reference():
+    """The reference's gate at its own precision (fp64 weights and inputs,
+    never rounded), Switch-Large shapes and planted near ties."""
+    for c in load("gate_f64.json"):
+        x, G, k = gate_f64_case(c)
+        ids, w, _ = og.gate_forward(x, G, k)
+        assert list(ids) == c["ids"]
+        assert [v.hex() for v in w] == c["w"]
