@@ -338,6 +338,10 @@ PGMOE_API int64_t pgmoe_launch_count(void);
  * launches taking consecutive rows (wrapping); nullptr disables.  Launches
  * enqueued (or graphs captured) while installed keep writing to it. */
 PGMOE_API int pgmoe_debug_set_probe(int32_t kind, void *device_buffer, int64_t rows);
+/* Debug only: create a green context of at least `min_sms` SMs on the current
+ * device and make it current on the calling thread (persistent kernels size
+ * their grid from the current context's SMs); *sms_out = SMs granted. */
+PGMOE_API int pgmoe_debug_green_context(int32_t min_sms, int32_t *sms_out);
 
 #ifdef __cplusplus
 }

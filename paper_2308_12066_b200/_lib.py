@@ -74,7 +74,7 @@ EXPORTS = (
     "pgmoe_cache_replay", "pgmoe_debug_set_probe", "pgmoe_model_set_fused_route",
     "pgmoe_ep_pack_send", "pgmoe_ep_local_routing_padded", "pgmoe_ep_pack_recv", "pgmoe_expert_forward_packed",
     "pgmoe_ep_unpermute_padded", "pgmoe_ep_slot_rows", "pgmoe_route_from_decisions", "pgmoe_decoder_iteration_ex",
-    "pgmoe_model_check_routing", "pgmoe_gate_forward_f64",
+    "pgmoe_model_check_routing", "pgmoe_gate_forward_f64", "pgmoe_debug_green_context",
 )
 
 _lib = None
@@ -100,6 +100,7 @@ def load():
         "pgmoe_check_routing": (i32, [P(Routing), P(i32)]),
         "pgmoe_route_from_decisions": (i32, [vp, vp, i32, i32, i32, P(Routing), vp]),
         "pgmoe_model_check_routing": (i32, [vp]),
+        "pgmoe_debug_green_context": (i32, [i32, P(i32)]),
         "pgmoe_gate_forward_f64": (i32, [vp, i32, i32, vp, i32, i32, P(Routing), vp, vp]),
         "pgmoe_decoder_iteration_ex": (i32, [vp, vp, i32, vp, P(IterationIO), vp]),
         "pgmoe_fill_weights": (i32, [vp, i32, ctypes.c_uint64, i32, i32, i32, i64, i64, vp]),

@@ -610,6 +610,49 @@ extern "C" int pgmoe_debug_set_probe(int32_t kind, void *device_buffer, int64_t 
     return PGMOE_OK;
 }
 
+// Debug: a green context of at least `min_sms` SMs (cuDevSmResourceSplitByCount)
+// made current on the calling thread, so the persistent kernels can be run on
+// a context with fewer co-resident CTAs than the device has SMs.
+extern "C" int pgmoe_debug_green_context(int32_t min_sms, int32_t *sms_out) {
+#define PG_DRV(name)                                                                                      \
+    decltype(&name) p_##name = nullptr;                                                                   \
+    {                                                                                                     \
+        void *fp = nullptr;                                                                               \
+        cudaDriverEntryPointQueryResult q;                                                                \
+        if (cudaGetDriverEntryPoint(#name, &fp, cudaEnableDefault, &q) != cudaSuccess ||                  \
+            q != cudaDriverEntryPointSuccess) {                                                           \
+            set_error("driver entry point %s unavailable", #name);                                       \
+            return PGMOE_E_CUDA;                                                                          \
+        }                                                                                                 \
+        p_##name = reinterpret_cast<decltype(&name)>(fp);                                                 \
+    }
+    PG_DRV(cuDeviceGetDevResource)
+    PG_DRV(cuDevSmResourceSplitByCount)
+    PG_DRV(cuDevResourceGenerateDesc)
+    PG_DRV(cuGreenCtxCreate)
+    PG_DRV(cuCtxFromGreenCtx)
+    PG_DRV(cuCtxSetCurrent)
+#undef PG_DRV
+    const CUdevice dev = (CUdevice)current_device();
+    CUdevResource input, result, remaining;
+    memset(&input, 0, sizeof(input));
+    memset(&result, 0, sizeof(result));
+    memset(&remaining, 0, sizeof(remaining));
+    unsigned int n = 1;
+    CUdevResourceDesc desc = nullptr;
+    CUgreenCtx g = nullptr;
+    CUcontext ctx = nullptr;
+    CUresult r = p_cuDeviceGetDevResource(dev, &input, CU_DEV_RESOURCE_TYPE_SM);
+    if (r == CUDA_SUCCESS) r = p_cuDevSmResourceSplitByCount(&result, &n, &input, &remaining, 0, (unsigned)min_sms);
+    if (r == CUDA_SUCCESS) r = p_cuDevResourceGenerateDesc(&desc, &result, 1);
+    if (r == CUDA_SUCCESS) r = p_cuGreenCtxCreate(&g, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM);
+    if (r == CUDA_SUCCESS) r = p_cuCtxFromGreenCtx(&ctx, g);
+    if (r == CUDA_SUCCESS) r = p_cuCtxSetCurrent(ctx);
+    PG_REQUIRE(r == CUDA_SUCCESS, PGMOE_E_CUDA, "green context of %d SMs failed (CUresult %d)", min_sms, (int)r);
+    if (sms_out) *sms_out = (int32_t)result.sm.smCount;
+    return PGMOE_OK;
+}
+
 // Workspaces of the standalone (model-less) tcgen05 entry points: split-K
 // tickets and partials, re-armed by each launch's last CTA, so calls that
 // share one must be stream-ordered.  Allocated once per process, under a

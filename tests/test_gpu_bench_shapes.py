@@ -193,20 +193,11 @@ import os, sys, numpy as np
 sys.path.insert(0, os.environ["ROOT"])
 mode = sys.argv[1]
 if mode == "green":
-    from cuda.bindings import driver as cu
-    def ok(r):
-        err = r[0] if isinstance(r, tuple) else r
-        assert int(err) == 0, r
-        return r[1:] if isinstance(r, tuple) and len(r) > 2 else (r[1] if isinstance(r, tuple) else None)
-    ok(cu.cuInit(0))
-    dev = ok(cu.cuDeviceGet(0))
-    res = ok(cu.cuDeviceGetDevResource(dev, cu.CUdevResourceType.CU_DEV_RESOURCE_TYPE_SM))
-    groups, n, rem = ok(cu.cuDevResourceSplitByCount(1, res, 0, int(sys.argv[2])))
-    desc = ok(cu.cuDevResourceGenerateDesc([groups[0]], 1))
-    g = ok(cu.cuGreenCtxCreate(desc, dev, cu.CUgreenCtxCreate_flags.CU_GREEN_CTX_DEFAULT_STREAM))
-    ctx = ok(cu.cuCtxFromGreenCtx(g))
-    ok(cu.cuCtxSetCurrent(ctx))
-    print("green context SMs:", groups[0].sm.smCount, flush=True)
+    import ctypes
+    from paper_2308_12066_b200 import _lib
+    n = ctypes.c_int32(0)
+    _lib.check(_lib.load().pgmoe_debug_green_context(int(sys.argv[2]), ctypes.byref(n)))
+    print("green context SMs:", n.value, flush=True)
 import paper_2308_12066_b200 as p
 cfg = p.ModelConfig(d_model=256, d_ff=2048, num_blocks=4, num_experts=64, top_k=1, activation_level=1, seed=2)
 m = p.DeviceModel(cfg, dtype="bf16", placement="resident", max_tokens=32)

@@ -220,7 +220,7 @@ def test_install_patches_a_moesim_shaped_package():
         h = dropin.install(name)
         assert sched.decoder_iteration is not orig["decoder_iteration"]
         d = core.gate_forward([0.3, -0.2, 0.1], [[0.1, 0.9], [0.4, -0.3], [0.2, 0.2]], 1)
-        assert type(d) is RoutingDecision and d.expert_ids == (0,)
+        assert type(d) is RoutingDecision and d.expert_ids == (1,)  # logits -0.03, 0.35
         with pytest.raises(errs.ShapeError, match="gate expects input of width 3, got 2"):
             core.gate_forward([0.3, -0.2], [[0.1, 0.9], [0.4, -0.3], [0.2, 0.2]], 1)
         params = Params(Cfg(32, 40, 3, 4, 1))
