@@ -27,6 +27,10 @@
 //   3. the last token tile builds the histogram, exclusive scan, stable
 //      permutation and active-expert list.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "route_common.cuh"
@@ -54,22 +58,27 @@ struct RouteParams {
     unsigned long long *probe;  // debug stamps [tiles*splits][kProbeSlots] or null
 };
 
+template <typename GT, typename XT>
+__device__ void select_tokens(const RouteParams &p, int tok0, int ntok, unsigned char *base);
+
+// fp32/bf16 operands: products exact, d - 1 roundings on either side;
+// fp64 operands: one more (the product), gamma_{d+1}
+template <typename GT, typename XT>
+__device__ __forceinline__ void bound_constants(int d, double *gam, double *bscale) {
+    const double u = 1.1102230246251565e-16;  // 2^-53
+    const double nd = (double)d + (std::is_same<GT, double>::value || std::is_same<XT, double>::value ? 1.0 : 0.0);
+    *gam = nd * u / (1.0 - nd * u);
+    *bscale = 2.0 * *gam / (1.0 - *gam) * 1.001;
+}
+
 // Phase 2: tokens [tok0, tok0+ntok) of tile `tile`, all splits present.
 template <typename GT, typename XT>
 __device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, unsigned char *smem_raw) {
-    const int d = p.d, E = p.E, k = p.k;
-    const GT *G = static_cast<const GT *>(p.G);
-    const XT *X = static_cast<const XT *>(p.x);
+    const int E = p.E;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double *logit = reinterpret_cast<double *>(smem_raw) + (size_t)warp * 2 * E;
-    double *bound = logit + E;
     __shared__ double s_xsum[kSelectWarps];
-    const double u = 1.1102230246251565e-16;  // 2^-53
-    // fp32/bf16 operands: products exact, d - 1 roundings on either side;
-    // fp64 operands: one more (the product), gamma_{d+1}
-    const double nd = (double)d + (std::is_same<GT, double>::value || std::is_same<XT, double>::value ? 1.0 : 0.0);
-    const double gam = nd * u / (1.0 - nd * u);
-    const double bscale = 2.0 * gam / (1.0 - gam) * 1.001;
+    double gam, bscale;
+    bound_constants<GT, XT>(p.d, &gam, &bscale);
     const double bpad = 1e-300;  // products are exact in fp64: no underflow below ~1e-90
     // sum_i |x_i G_ij| <= (sum_i |x_i|) * max_i |G_ij|; the split CTAs
     // wrote sum |x_i| of their slices.  All split partials are loaded in one
@@ -112,26 +121,52 @@ __device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, 
     }
     __syncthreads();
     if (tid == 0) probe(p.probe, blockIdx.y * gridDim.x + blockIdx.x, 7);  // partials reduced
+    select_tokens<GT, XT>(p, tok0, ntok, smem_raw);
+}
+
+// Certified selection + softmax of tokens [tok0, tok0 + ntok), one warp per
+// token, from shared memory: token w's fp64 logits at base + w * 2E and
+// their error bounds right after them (E doubles each).
+template <typename GT, typename XT>
+__device__ void select_tokens(const RouteParams &p, int tok0, int ntok, unsigned char *base) {
+    const int d = p.d, E = p.E, k = p.k;
+    const GT *G = static_cast<const GT *>(p.G);
+    const XT *X = static_cast<const XT *>(p.x);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // The softmax normaliser of the fast logits does not depend on the
+    // ranking: when there are idle warps, warp ntok + t computes token t's
+    // (max, sum exp) while warp t ranks; a token whose ranking needs the
+    // serial recompute (its logits change) redoes it itself.
+    __shared__ double s_mz[kSelectWarps][2];
+    const bool helpers = 2 * ntok <= kSelectWarps;
+    auto normaliser = [&](const double *lg, double &m, double &z) {  // softmax over all E (linalg.py:54-59)
+        m = -INFINITY;
+        for (int j = lane; j < E; j += 32) m = fmax(m, lg[j]);
+        m = warp_max(m);
+        z = 0.0;
+        for (int j = lane; j < E; j += 32) z += exp(lg[j] - m);
+        z = warp_sumd(z);
+    };
+    if (helpers && warp >= ntok && warp < 2 * ntok) {
+        double m, z;
+        normaliser(reinterpret_cast<const double *>(base) + (size_t)(warp - ntok) * 2 * E, m, z);
+        if (lane == 0) {
+            s_mz[warp - ntok][0] = m;
+            s_mz[warp - ntok][1] = z;
+        }
+    }
     const int tok = tok0 + warp;
+    double *lg = reinterpret_cast<double *>(base) + (size_t)warp * 2 * E;
+    double *bd = lg + E;
+    bool finite = true, certified = true;
+    int sel[8];
+    double minlow = INFINITY;
     if (warp < ntok) {  // tok < p.T follows
-        double *lg = logit;
-        double *bd = bound;
-        __syncwarp();
         // finite check (core.py:297)
-        bool finite = true;
         for (int j = lane; j < E; j += 32) finite &= (bool)isfinite(lg[j]);
         finite = __all_sync(0xffffffffu, finite);
-        if (!finite) {
-            if (lane == 0) atomicCAS(p.out.status, 0, (int)PGMOE_E_GATE_OVERFLOW);
-            for (int s = lane; s < k; s += 32) {
-                p.out.ids[(size_t)tok * k + s] = 0;
-                p.out.w[(size_t)tok * k + s] = 0.f;
-            }
-        } else {
-            int sel[8];
+        if (finite) {
             uint32_t taken = 0;  // bit q: expert lane + 32*q taken
-            bool certified = true;
-            double minlow = INFINITY;
             for (int s = 0; s < k; ++s) {
                 double bf = -INFINITY;
                 int bi = -1;
@@ -151,6 +186,17 @@ __device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, 
                 up = warp_max(up);
                 certified &= (low > up);
             }
+        }
+    }
+    if (helpers) __syncthreads();  // normalisers in shared memory; lg no longer read by helpers
+    if (warp < ntok) {
+        if (!finite) {
+            if (lane == 0) atomicCAS(p.out.status, 0, (int)PGMOE_E_GATE_OVERFLOW);
+            for (int s = lane; s < k; s += 32) {
+                p.out.ids[(size_t)tok * k + s] = 0;
+                p.out.w[(size_t)tok * k + s] = 0.f;
+            }
+        } else {
             if (!certified) {
                 // Candidates that could be in the reference top-k: recompute
                 // them in the reference's serial order.
@@ -176,13 +222,13 @@ __device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, 
                 if (lane == 0) atomicAdd(p.out.status + 1, 1);
             }
             if (lane == 0 && warp == 0) probe(p.probe, blockIdx.y * gridDim.x + blockIdx.x, 8);  // ranked
-            // softmax over all E (linalg.py:54-59), max-subtracted
-            double m = -INFINITY;
-            for (int j = lane; j < E; j += 32) m = fmax(m, lg[j]);
-            m = warp_max(m);
-            double z = 0.0;
-            for (int j = lane; j < E; j += 32) z += exp(lg[j] - m);
-            z = warp_sumd(z);
+            double m, z;
+            if (helpers && certified) {
+                m = s_mz[warp][0];
+                z = s_mz[warp][1];
+            } else {
+                normaliser(lg, m, z);
+            }
             for (int s = 0; s < k; ++s) {
                 const double pr = exp(lg[sel[s]] - m) / z;
                 if (lane == 0) {
@@ -193,7 +239,53 @@ __device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, 
             }
         }
     }
+}
 
+// Permutation of N = T*k <= 32 routed rows by one warp, straight from the
+// ids in registers (no shared-memory histogram, no block barriers): row r
+// goes to #{rows with a smaller expert} + #{earlier rows, same expert}, the
+// same stable order permute_all builds.
+__device__ void permute_warp(const RouteParams &p) {
+    const int E = p.E, N = p.T * p.k, lane = threadIdx.x & 31;
+    const bool v = lane < N;
+    const int e = v ? __ldcg(p.out.ids + lane) : 0x7fffffff;
+    const float w = v ? __ldcg(p.out.w + lane) : 0.f;
+    int ev[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) ev[l] = __shfl_sync(0xffffffffu, e, l);
+    int less = 0, before = 0;
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+        less += ev[l] < e;
+        before += (ev[l] == e) & (l < lane);
+    }
+    if (v) {
+        const int pos = less + before;
+        p.out.perm[pos] = lane;
+        if (p.out.inv) p.out.inv[lane] = pos;
+        p.out.w_perm[pos] = w;
+    }
+    int nact = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+        const int ex = e0 + lane;
+        int h = 0, lt = 0;
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {  // padding lanes hold INT_MAX: never counted
+            h += ev[l] == ex;
+            lt += ev[l] < ex;
+        }
+        const unsigned am = __ballot_sync(0xffffffffu, ex < E && h > 0);
+        if (ex < E) {
+            p.out.hist[ex] = h;
+            p.out.off[ex] = lt;
+            if (h > 0) p.out.act[nact + __popc(am & ((1u << lane) - 1u))] = ex;
+        }
+        nact += __popc(am);
+    }
+    if (lane == 0) {
+        p.out.off[E] = N;
+        *p.out.n_act = nact;
+    }
 }
 
 // Phase 3: histogram, exclusive scan, stable permutation, active list.
@@ -243,6 +335,7 @@ __device__ void permute_all(const RouteParams &p, unsigned char *smem_raw) {
         }
     }
     __syncthreads();
+    if (tid == 0) probe(p.probe, blockIdx.y * gridDim.x + blockIdx.x, 11);  // histogram + scan
     for (int e = tid; e < E; e += kSelectThreads) {
         int base = tot[e];
         for (int w = 0; w < kSelectWarps; ++w) {
@@ -429,7 +522,11 @@ route_kernel(const RouteParams p_in) {
     if (!s_last) return;
     __threadfence();
     if (tid == 0) probe(p.probe, cta, 5);  // permute start
-    permute_all(p, smem_raw);
+    if (p.T * p.k <= 32) {
+        if (threadIdx.x < 32) permute_warp(p);
+    } else {
+        permute_all(p, smem_raw);
+    }
     if (tid == 0) {
         *p.counter = 0;
         probe(p.probe, cta, 6);  // permute done
@@ -437,6 +534,272 @@ route_kernel(const RouteParams p_in) {
     __threadfence();
     __syncthreads();
     pdl_trigger();
+}
+
+// ---------------------------------------------------------------------------
+// K1, cluster form (E <= 256, fp32 / bf16 gates).  A token tile of TOK
+// tokens is one thread-block cluster of S CTAs; CTA `rank` owns gate rows
+// [rank*kn, (rank+1)*kn).  Its gate slice is static weight data, so it is
+// staged into shared memory BEFORE the programmatic-dependent-launch wait
+// (the load overlaps the previous kernel's tail).  Partial logits, column
+// maxima and sum|x| stay in each CTA's shared memory; rank 0 sums them over
+// the cluster through distributed shared memory in rank order
+// (deterministic), bounds, certifies / recomputes and selects.  No global
+// partials, no per-tile atomic ticket: the only global round trip left is
+// the permutation's ticket when the batch spans several tiles (a single
+// tile permutes straight from shared memory).
+// Same arithmetic contract as route_kernel: exact fp64 products, any
+// summation order within the certified bound, serial reference fallback.
+constexpr int kClusterMaxS = 16;
+
+constexpr size_t kClusterGBytes = 64 * 1024;  // gate slice per CTA
+
+struct ClusterLayout {
+    size_t r0, x, part, cm, xs, total;  // byte offsets in dynamic shared memory
+};
+__host__ __device__ inline ClusterLayout cluster_layout(int tok, int kn, int E, size_t gbytes) {
+    auto up = [](size_t v) { return (v + 15) & ~(size_t)15; };
+    ClusterLayout l;
+    size_t r0 = gbytes;                                         // gate slice
+    r0 = r0 > (size_t)tok * 2 * E * 8 ? r0 : (size_t)tok * 2 * E * 8;        // rank 0: logits + bounds
+    r0 = r0 > (size_t)(kSelectWarps + 1) * E * 4 ? r0 : (size_t)(kSelectWarps + 1) * E * 4;  // permutation
+    l.r0 = 0;
+    l.x = up(r0);
+    l.part = l.x + up((size_t)tok * kn * 8);
+    l.cm = l.part + up((size_t)tok * E * 8);
+    l.xs = l.cm + up((size_t)E * 4);
+    l.total = l.xs + up((size_t)tok * 8) + 16;
+    return l;
+}
+
+template <typename GT, int TOK>
+__global__ void __launch_bounds__(kLogitThreads) route_cluster_kernel(const RouteParams p_in) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ RouteParams p_sh;
+    if (threadIdx.x < sizeof(RouteParams) / 4)
+        reinterpret_cast<int *>(&p_sh)[threadIdx.x] = reinterpret_cast<const int *>(&p_in)[threadIdx.x];
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int S = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    __syncthreads();
+    const RouteParams &p = p_sh;
+    const int d = p.d, E = p.E, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tile = blockIdx.x / S;
+    const int t0 = tile * TOK, ntok = min(TOK, p.T - t0);
+    const int kn = d / S, k0 = rank * kn;
+    const ClusterLayout L = cluster_layout(TOK, kn, E, (size_t)kn * E * sizeof(GT));
+    GT *sG = reinterpret_cast<GT *>(smem_raw + L.r0);
+    double *sx = reinterpret_cast<double *>(smem_raw + L.x);
+    double *part = reinterpret_cast<double *>(smem_raw + L.part);
+    float *scm = reinterpret_cast<float *>(smem_raw + L.cm);
+    double *sxs = reinterpret_cast<double *>(smem_raw + L.xs);
+    const int cta = blockIdx.x;
+    if (tid == 0) {
+        probe(p.probe, cta, 0);
+        if (p.probe) p.probe[(size_t)cta * kProbeSlots + 12] = clock64();
+    }
+
+    // 1. gate rows [k0, k0 + kn): contiguous, 16-byte vectors, 8 in flight per thread
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(static_cast<const GT *>(p.G) + (size_t)k0 * E);
+        uint4 *dst = reinterpret_cast<uint4 *>(sG);
+        const int nv = (int)((size_t)kn * E * sizeof(GT) / 16);
+        for (int i0 = tid; i0 < nv; i0 += 8 * kLogitThreads) {
+            uint4 v[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int i = i0 + b * kLogitThreads;
+                if (i < nv) v[b] = __ldg(src + i);
+            }
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int i = i0 + b * kLogitThreads;
+                if (i < nv) dst[i] = v[b];
+            }
+        }
+    }
+    pdl_wait();  // x is produced by the previous kernel in the stream
+    if (tid == 0) probe(p.probe, cta, 1);
+    // 2. x slice (fp32 -> fp64, exact)
+    const float *X = static_cast<const float *>(p.x);
+    for (int i = tid; i < TOK * kn; i += kLogitThreads) {
+        const int t = i / kn;
+        sx[i] = t < ntok ? (double)__ldg(X + (size_t)(t0 + t) * d + k0 + (i - t * kn)) : 0.0;
+    }
+    __syncthreads();
+    if (warp < TOK) {  // sum |x_i| over the slice (bounds the logit error)
+        double v = 0.0;
+        for (int i = lane; i < kn; i += 32) v += fabs(sx[warp * kn + i]);
+        v = warp_sumd(v);
+        if (lane == 0) sxs[warp] = v;
+    }
+    if (tid == 0) probe(p.probe, cta, 10);  // x slice in shared memory
+    // 3. partial logits: thread (tg, j) owns expert j for tokens tg, tg + NTG, ...
+    {
+        const int NTG = max(1, kLogitThreads / E);
+        const int j = tid % E, tg = tid / E;
+        if (tg < NTG && tid < NTG * E) {
+            double acc[TOK];
+#pragma unroll
+            for (int tt = 0; tt < TOK; ++tt) acc[tt] = 0.0;
+            float cm = 0.f;
+            // batches of RB rows, loads first: one row's load -> convert ->
+            // FMA chain is ~100 cycles of latency, so rows must overlap
+            auto rows = [&](auto rb, int i) {
+                constexpr int RB = decltype(rb)::value;
+                float gf[RB];
+#pragma unroll
+                for (int b = 0; b < RB; ++b) gf[b] = WTraits<GT>::f32(sG[(size_t)(i + b) * E + j]);
+#pragma unroll
+                for (int b = 0; b < RB; ++b) {
+                    const double g = gf[b];
+                    cm = fmaxf(cm, fabsf(gf[b]));
+#pragma unroll
+                    for (int tt = 0; tt < TOK; ++tt) {
+                        const int t = tg + tt * NTG;
+                        if (t < TOK) acc[tt] = fma(sx[t * kn + i + b], g, acc[tt]);  // exact product, one rounding
+                    }
+                }
+            };
+            int i = 0;
+            for (; i + 8 <= kn; i += 8) rows(std::integral_constant<int, 8>{}, i);  // rows in order: same sums
+            for (; i < kn; ++i) rows(std::integral_constant<int, 1>{}, i);
+#pragma unroll
+            for (int tt = 0; tt < TOK; ++tt) {
+                const int t = tg + tt * NTG;
+                if (t < TOK) part[t * E + j] = acc[tt];
+            }
+            if (tg == 0) scm[j] = cm;
+        }
+    }
+    if (tid == 0) probe(p.probe, cta, 2);  // partial logits in shared memory
+    cl.sync();  // every CTA's partials visible cluster-wide
+    // 4. rank r owns the tile's tokens [r*c, (r+1)*c): sums over the cluster
+    //    in rank order (all S partials loaded first, then added: one round of
+    //    DSMEM latency), bounds -> [t][logit E | bound E] at r0
+    const int c = (TOK + S - 1) / S;
+    const int own0 = rank * c, nown = max(0, min(c, ntok - own0));
+    if (nown > 0) {
+        double gam, bscale;
+        bound_constants<GT, float>(d, &gam, &bscale);
+        __syncthreads();  // every thread is past its partial loop: r0 is free
+        double *lgs = reinterpret_cast<double *>(smem_raw + L.r0);
+        for (int q = tid; q < nown * E; q += kLogitThreads) {
+            const int tl = q / E, j = q - tl * E;
+            // one round of DSMEM loads: the S partials, column maxima and
+            // slice sums |x| (the latter redundantly per thread)
+            double pv[kClusterMaxS], xv[kClusterMaxS];
+            float cv[kClusterMaxS];
+#pragma unroll
+            for (int z = 0; z < kClusterMaxS; ++z) {
+                pv[z] = z < S ? cl.map_shared_rank(part, z)[(own0 + tl) * E + j] : 0.0;
+                cv[z] = z < S ? cl.map_shared_rank(scm, z)[j] : 0.f;
+                xv[z] = z < S ? cl.map_shared_rank(sxs, z)[own0 + tl] : 0.0;
+            }
+            double sum = 0.0, sx = 0.0;
+            float cm = 0.f;
+#pragma unroll
+            for (int z = 0; z < kClusterMaxS; ++z)  // fixed order: deterministic
+                if (z < S) {
+                    sum += pv[z];
+                    cm = fmaxf(cm, cv[z]);
+                    sx += xv[z];
+                }
+            lgs[tl * 2 * E + j] = sum;
+            lgs[tl * 2 * E + E + j] = bscale * (sx * (1.0 + 2.0 * gam)) * (double)cm + 1e-300;
+        }
+        __syncthreads();
+        if (tid == 0) probe(p.probe, cta, 3);  // cluster sums done
+        // 5. certified selection + softmax (one warp per token)
+        select_tokens<GT, float>(p, t0 + own0, nown, smem_raw + L.r0);
+        if (p.T > TOK) __threadfence();  // ids / weights visible GPU-wide before rank 0's ticket
+    }
+    cl.sync();  // the tile's ids / weights written; nobody reads remote shared memory any more
+    if (rank != 0) return;
+    if (tid == 0) probe(p.probe, cta, 4);  // tile selected
+    // 6. permutation: one tile -> straight away; several -> the last tile
+    //    through a global ticket
+    __shared__ int s_last;
+    if (p.T > TOK) {
+        if (tid == 0) s_last = (atomicAdd(p.counter, 1) == (int)(gridDim.x / S) - 1);
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+    }
+    if (tid == 0) probe(p.probe, cta, 5);
+    if (p.T * p.k <= 32) {
+        if (warp == 0) permute_warp(p);
+    } else {
+        permute_all(p, smem_raw + L.r0);
+    }
+    if (tid == 0) {
+        if (p.T > TOK) *p.counter = 0;
+        probe(p.probe, cta, 6);  // permutation written
+        if (p.probe) p.probe[(size_t)cta * kProbeSlots + 13] = clock64();
+    }
+    __threadfence();
+    __syncthreads();
+    pdl_trigger();
+}
+
+// Cluster size for T tokens: the smallest power of two that puts >= one CTA
+// on every SM (at most 16), with the gate slice <= 64 KB and d % S == 0.
+static int pick_cluster(int T, int d, int E, size_t gsz, int tok) {
+    const int tiles = (T + tok - 1) / tok;
+    int S = 1;
+    while (S < kClusterMaxS && (long long)tiles * S < kNumSMs) S <<= 1;
+    while (S < kClusterMaxS && (size_t)(d / S) * E * gsz > kClusterGBytes) S <<= 1;
+    while (S > 1 && d % S != 0) S >>= 1;
+    if (d % S != 0 || (size_t)(d / S) * E * gsz > kClusterGBytes) return 0;
+    return S;
+}
+
+template <typename GT, int TOK>
+static int launch_route_cluster(const RouteParams &p, int S, cudaStream_t s) {
+    auto kern = route_cluster_kernel<GT, TOK>;
+    const int kn = p.d / S;
+    const size_t smem = cluster_layout(TOK, kn, p.E, (size_t)kn * p.E * sizeof(GT)).total;
+    static unsigned long long attr_set[2] = {0, 0};  // per device: [0] smem + cluster attrs, [1] S = 16 usable
+    const int dev = current_device();
+    PG_REQUIRE(dev >= 0 && dev < 64, PGMOE_E_CONFIG, "device ordinal %d unsupported", dev);
+    if (!(attr_set[0] & (1ull << dev))) {
+        PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        PG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr_set[0] |= 1ull << dev;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(((p.T + TOK - 1) / TOK) * S));
+    cfg.blockDim = dim3(kLogitThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = (unsigned)S;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (S == kClusterMaxS && !(attr_set[1] & (1ull << dev))) {  // 16-CTA clusters are opt-in: check once
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            return launch_route_cluster<GT, TOK>(p, kClusterMaxS / 2, s);
+        }
+        attr_set[1] |= 1ull << dev;
+    }
+    PG_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+    count_launch();
+    return PGMOE_OK;
+}
+
+template <typename GT>
+static int route_cluster_dispatch(const RouteParams &p, int tok, int S, cudaStream_t s) {
+    if (tok == 1) return launch_route_cluster<GT, 1>(p, S, s);
+    if (tok == 2) return launch_route_cluster<GT, 2>(p, S, s);
+    if (tok == 4) return launch_route_cluster<GT, 4>(p, S, s);
+    return launch_route_cluster<GT, 8>(p, S, s);
 }
 
 static int pick_tok(int T) {
@@ -553,6 +916,23 @@ static int gate_forward_any(const void *x, bool x64, int32_t T, int32_t d, const
     if (x64) {
         PG_REQUIRE(wdtype == PGMOE_F64, PGMOE_E_CONFIG, "fp64 inputs route with fp64 gate weights");
         return route_dispatch<double, double>(p, s);
+    }
+    // cluster form unless the shape needs the split-partials kernel (E > 256,
+    // misaligned gate rows) or PGMOE_ROUTE_KERNEL=split forces it (A/B tests)
+    const char *force = getenv("PGMOE_ROUTE_KERNEL");
+    const size_t gsz = wdtype == PGMOE_BF16 ? 2 : 4;
+    if ((wdtype == PGMOE_BF16 || wdtype == PGMOE_F32) && E <= 256 && ((size_t)E * gsz) % 16 == 0 &&
+        (reinterpret_cast<uintptr_t>(gate_w) & 15) == 0 && !(force && strcmp(force, "split") == 0)) {
+        // measured (tools/route_bench.py): the cluster form wins at T <= 4 and
+        // T >= 128, the split form at 8..64 tokens (more CTAs select in parallel)
+        const bool want = (force && strcmp(force, "cluster") == 0) || T <= 4 || T >= 128;
+        const int tok = T <= 1 ? 1 : T <= 2 ? 2 : T <= 4 ? 4 : 8;
+        const int S = want ? pick_cluster(T, d, E, gsz, tok) : 0;
+        if (S > 0 && (T + tok - 1) / tok * S <= (1 << 20)) {
+            p.probe = probe_buffer(0, (T + tok - 1) / tok * S);
+            return wdtype == PGMOE_BF16 ? route_cluster_dispatch<uint16_t>(p, tok, S, s)
+                                        : route_cluster_dispatch<float>(p, tok, S, s);
+        }
     }
     if (wdtype == PGMOE_BF16) return route_dispatch<uint16_t>(p, s);
     if (wdtype == PGMOE_F32) return route_dispatch<float>(p, s);

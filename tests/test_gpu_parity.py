@@ -123,6 +123,37 @@ def test_route_near_ties_one_ulp_apart():
     _check_route(x, G, 2, r)
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("d,E,T", [(768, 64, 1), (768, 64, 3), (1024, 128, 8), (1024, 128, 9), (768, 128, 256),
+                                   (1024, 256, 65), (768, 8, 700), (512, 24, 64)])
+def test_route_cluster_kernel_equals_split_kernel(monkeypatch, dtype, d, E, T):
+    """K1's two forms (thread-block clusters reducing over DSMEM; split-K
+    partials through global memory) give identical routing buffers, and
+    both equal the reference (ties planted so the serial path runs too)."""
+    p = P()
+    G = og.weights(og.derive_seed(0, og.TAG_PRE_GATE, 7, -1), d, E, dtype)
+    x = tokens(d, T, seed=d + T)
+    if E > 16:  # duplicated columns: bit-equal logits the certified path cannot separate
+        G = G.copy()
+        G[:, 11] = G[:, 5]
+        x[::3] = (np.sign(G[:, 5].astype(np.float32) if G.dtype != np.uint16 else
+                          (G[:, 5].astype(np.uint32) << 16).view(np.float32)) * 0.05)[None, :]
+    xt = torch.from_numpy(x).cuda()
+    outs = []
+    for mode in ("cluster", "split"):
+        monkeypatch.setenv("PGMOE_ROUTE_KERNEL", mode)
+        r = p.route(xt, as_torch_w(G), 1)
+        st = r.check()
+        outs.append((r, st))
+    a, b = outs[0][0], outs[1][0]
+    for name in ("ids", "w", "hist", "off", "act"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+    n = T
+    assert torch.equal(a.perm[:n], b.perm[:n]) and torch.equal(a.w_perm[:n], b.w_perm[:n])
+    assert outs[0][1]["fallbacks"] == outs[1][1]["fallbacks"]
+    _check_route(x, G, 1, a)
+
+
 def test_route_golden_reference_gate_large():
     """Reference outputs (moesim.gate_forward) on the Large-128 gate shape."""
     p = P()
