@@ -274,6 +274,18 @@ PGMOE_API int pgmoe_model_set_kernel(pgmoe_model *m, int32_t kernel);
  * launch, overlapped with its expert GEMMs (default on).  0 restores the
  * separate K1 launch; routing and outputs are identical either way. */
 PGMOE_API int pgmoe_model_set_fused_route(pgmoe_model *m, int32_t enabled);
+/* Resident top-1 decoding at small batches (T <= max_tokens, at most 64):
+ * ONE persistent launch per decoder iteration runs every block — expert
+ * up/down, combine, dense and the next block's pre-gate — with K split over
+ * 8-CTA thread-block clusters and the partials summed in distributed shared
+ * memory (decode_tc.cu).  Replaces the per-block launches of
+ * decoder_iteration's block loop (core.py:361-380); routing is identical, block
+ * outputs equal the per-block path within the bf16 tolerance (different
+ * split-K grouping).  enabled = 0 restores the per-block launches; max_tokens
+ * = 0 keeps the current threshold (default 1, PGMOE_DECODE_MAX_T). */
+PGMOE_API int pgmoe_model_set_decode(pgmoe_model *m, int32_t enabled, int32_t max_tokens);
+/* Decoder iterations served by the persistent small-batch launch so far. */
+PGMOE_API int64_t pgmoe_model_decode_iterations(pgmoe_model *m);
 
 /* decoder_iteration (core.py:342-383) for T tokens, device buffers.
  * x_in / y_out: fp32 [T][d] device.  ids_trace / w_trace (optional, device):

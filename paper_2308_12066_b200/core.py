@@ -365,6 +365,15 @@ class DeviceModel:
         """Resident top-1: compute each pre-gate inside the block launch (default)."""
         _lib.check(self._L.pgmoe_model_set_fused_route(self._h, 1 if enabled else 0))
 
+    def set_decode(self, enabled: bool, max_tokens: int = 0) -> None:
+        """Resident top-1 at T <= max_tokens (default 1): one persistent launch
+        per decoder iteration (pgmoe_model_set_decode)."""
+        _lib.check(self._L.pgmoe_model_set_decode(self._h, 1 if enabled else 0, int(max_tokens)))
+
+    @property
+    def decode_iterations(self) -> int:
+        return int(self._L.pgmoe_model_decode_iterations(self._h))
+
     # -- weights (BlockParams `loaded` hook, core.py:185-211) --
     def _mat_shape(self, name):
         c = self.config

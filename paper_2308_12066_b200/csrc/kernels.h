@@ -20,6 +20,8 @@ int expert_ffn_tc(const float *x, int T, int d, int f, int k, const void *expert
 int dense_tc(const float *yw, int T, int d, int k, const void *dense_w, float *y, void *workspace,
              size_t ws_bytes, cudaStream_t s);
 bool tc_supported(int d, int f);
+// xb[r] = bf16(x[perm[r] / k]): the up-projection operand in routing order
+int tc_pack_rows(const float *x, const int *perm, int n, int d, int k, uint16_t *xb, cudaStream_t s);
 // Fused-operand variants used by the runtime: bf16 activations packed once
 // (xb), bf16 hidden (hb), and for top-1 the bf16 mix written by the down
 // projection's epilogue so the dense layer reads it directly.

@@ -580,6 +580,51 @@ static __device__ __noinline__ void router_permute(const FusedRoute &r, int rt, 
     }
 }
 
+// The same permutation for N = T*k <= 32 rows by ONE warp (lane = row), with
+// no shared-memory histogram and no barriers: row r goes to #{rows of a
+// smaller expert} + #{earlier rows of its expert} — the stable order
+// router_permute builds.
+static __device__ __noinline__ void router_permute_small(const FusedRoute &r, int lane, const int *ids_src,
+                                                         const float *w_src) {
+    const int E = r.E, N = r.T * r.k;
+    const bool v = lane < N;
+    const int e = v ? ids_src[lane] : 0x7fffffff;
+    const float wv = v ? w_src[lane] : 0.f;
+    int less = 0, before = 0;
+    for (int l = 0; l < N; ++l) {
+        const int el = __shfl_sync(0xffffffffu, e, l);
+        less += el < e;
+        before += (el == e) & (l < lane);
+    }
+    if (v) {
+        const int pos = less + before;
+        r.out.perm[pos] = lane;
+        if (r.out.inv) r.out.inv[lane] = pos;
+        r.out.w_perm[pos] = wv;
+    }
+    int nact = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+        const int ex = e0 + lane;
+        int h = 0, lt = 0;
+        for (int l = 0; l < N; ++l) {
+            const int el = __shfl_sync(0xffffffffu, e, l);
+            h += el == ex;
+            lt += el < ex;
+        }
+        const unsigned am = __ballot_sync(0xffffffffu, ex < E && h > 0);
+        if (ex < E) {
+            r.out.hist[ex] = h;
+            r.out.off[ex] = lt;
+            if (h > 0) r.out.act[nact + __popc(am & ((1u << lane) - 1u))] = ex;
+        }
+        nact += __popc(am);
+    }
+    if (lane == 0) {
+        r.out.off[E] = N;
+        *r.out.n_act = nact;
+    }
+}
+
 // The whole routing role (64 threads, rt = 0..63) for one CTA.
 template <typename GT, int NJ>
 __device__ void router_role(const FusedRoute &r, int rt, float *xs, int *s_flag, unsigned long long *pr) {
@@ -630,7 +675,11 @@ __device__ void router_role(const FusedRoute &r, int rt, float *xs, int *s_flag,
         router_sync();
         if (!*s_flag) continue;
         if (!single) __threadfence();
-        router_permute(r, rt, reinterpret_cast<int *>(xs), single ? s_ids : r.out.ids, single ? s_w : r.out.w);
+        if (r.T * r.k <= 32) {
+            if (w == 0) router_permute_small(r, lane, single ? s_ids : r.out.ids, single ? s_w : r.out.w);
+        } else {
+            router_permute(r, rt, reinterpret_cast<int *>(xs), single ? s_ids : r.out.ids, single ? s_w : r.out.w);
+        }
         __threadfence();
         router_sync();
         if (rt == 0) probe(pr, blockIdx.x, 29);  // permutation written

@@ -21,6 +21,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "decode.h"
 #include "expert_cache.h"
 #include "kernels.h"
 #include "rng.h"
@@ -187,6 +188,13 @@ struct pgmoe_model {
     unsigned long long graph_clock = 0;
     int64_t fused_blocks = 0;  // blocks whose dense layer ran inside the expert launch
     int64_t fused_routes = 0;  // pre-gates computed inside the block launch
+    // small batches (T <= decode_max_t): one persistent launch per decoder
+    // iteration (decode_tc.cu); per-block descriptors built at creation
+    bool decode = true;          // pgmoe_model_set_decode / PGMOE_DECODE=0
+    int decode_max_t = 1;        // PGMOE_DECODE_MAX_T (measured: the per-block launches win from T = 2)
+    DecodeBlock *dec_blocks = nullptr;
+    int *dec_sync = nullptr;
+    int64_t decode_iters = 0;
     bool fuse_route = true;    // resident: route inside the block launch (pgmoe_model_set_fused_route)
     long long fuse_max_t = 0;  // largest T routed inside the block launch (0: d_ff / 8; PGMOE_FUSE_MAX_T)
     // fused: launches chained on the previous dense phase instead of its
@@ -464,6 +472,46 @@ static FusedRoute fused_route_args(pgmoe_model *m, const float *x, int T, const 
     return r;
 }
 
+// Small batches: block 0's gate (K1) and operand pack, then ONE persistent
+// launch runs every block (decode_tc.cu), the pre-gates included.
+static int decode_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, const pgmoe_iteration_io &io,
+                            cudaStream_t s) {
+    const auto &c = m->cfg;
+    const int nb = c.num_blocks;
+    PG_CUDA(cudaMemsetAsync(m->dec_sync, 0, (size_t)nb * kDecodeSyncInts * 4, s));
+    PG_TRY(route_into(m, x_in, T, m->blocks[0].gate, 0, false, s, "gate", 0, io, 0));
+    PG_TRY(tc_pack_rows(x_in, m->routing[0].r.perm, T, c.d_model, 1, m->xb, s));
+    DecodeArgs a{};
+    a.T = T;
+    a.d = c.d_model;
+    a.f = c.d_ff;
+    a.E = c.num_experts;
+    a.nb = nb;
+    a.blocks = m->dec_blocks;
+    a.sync = m->dec_sync;
+    a.x_in = x_in;
+    a.y_out = y_out;
+    a.xb = m->xb;
+    a.hb = m->hb;
+    a.mixb = m->mixb;
+    a.route = fused_route_args(m, x_in, T, m->blocks[0].pre_gate, m->routing[1].r, 0);
+    a.experts = m->blocks[0].experts;
+    a.nrec = nb * c.num_experts;
+    a.rec_bytes = m->rec_bytes;
+    a.pool = m->dev_pool;
+    a.pool_rows = (long long)(m->dev_pool_bytes / (2 * (size_t)c.d_model));
+    a.x_trace = io.x_trace;
+    a.ids_trace = io.ids_trace;
+    a.w_trace = io.w_trace;
+    tl_begin(m, "compute", "experts", 0, s);  // every block's experts, dense layers and pre-gates: one launch
+    PG_TRY(decode_iteration_tc(a, s));
+    tl_end(m, s);
+    m->fused_blocks += nb;
+    m->fused_routes += nb - 1;
+    m->decode_iters++;
+    return PGMOE_OK;
+}
+
 int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, const pgmoe_iteration_io &io,
                       cudaStream_t s) {
     const auto &c = m->cfg;
@@ -507,6 +555,9 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, co
     const bool fuse_route = !off && !io.ids_supplied && use_tc(m) && c.top_k == 1 && L == 1 && m->fuse_route &&
                             fused_route_supported(c.num_experts) &&
                             (long long)T <= (m->fuse_max_t > 0 ? m->fuse_max_t : c.d_ff / 8);
+    if (m->decode && m->dec_blocks && !off && !io.ids_supplied && use_tc(m) && m->fuse_route &&
+        T <= m->decode_max_t && decode_supported(T, c.d_model, c.d_ff, c.num_experts, c.top_k, L, nb))
+        return decode_iteration(m, x_in, T, y_out, io, s);
     const float *cur = x_in;
     // Chained block launches (fused routing): each launch waits for its
     // predecessor's dense phase through a device counter instead of for its
@@ -838,6 +889,32 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
     if (const char *e = getenv("PGMOE_CHAIN")) m->chain_launches = (e[0] != '0');
     if (const char *e = getenv("PGMOE_FUSED_ROUTE")) m->fuse_route = (e[0] == '1');
     if (const char *e = getenv("PGMOE_FUSE_MAX_T")) m->fuse_max_t = atoll(e);
+    if (const char *e = getenv("PGMOE_DECODE")) m->decode = (e[0] != '0');
+    if (const char *e = getenv("PGMOE_DECODE_MAX_T")) m->decode_max_t = std::max(0, std::min(kDecodeMaxT, atoi(e)));
+    if (placement == PGMOE_RESIDENT && wdtype == PGMOE_BF16 && m->e_local == c.num_experts &&
+        decode_supported(1, (int)d, (int)f, c.num_experts, (int)k, c.activation_level, (int)nb) &&
+        m->dev_pool_bytes % (2 * d) == 0) {
+        std::vector<DecodeBlock> db(nb);
+        for (size_t b = 0; b < nb; ++b) {
+            const pgmoe_routing &r = m->routing[b % 2].r;
+            DecodeBlock &x = db[b];
+            x.act = r.act; x.n_act = r.n_act; x.hist = r.hist; x.off = r.off; x.perm = r.perm; x.inv = r.inv;
+            x.w_perm = r.w_perm; x.ids = r.ids; x.w = r.w;
+            x.next_inv = b + 1 < nb ? m->routing[(b + 1) % 2].r.inv : nullptr;
+            x.wrec0 = (int)(b * E);
+            x.dense_row0 = (int)((static_cast<unsigned char *>(m->blocks[b].dense) - m->dev_pool) / (2 * d));
+            x.has_pre_gate = has_pre_gate(c, (int)b) ? 1 : 0;
+            x.x = b >= 1 ? m->act_buf[(b - 1) & 1] : nullptr;
+            x.y = b + 1 < nb ? m->act_buf[b & 1] : nullptr;
+            x.pre_gate = m->blocks[b].pre_gate;
+            x.out = m->routing[(b + 1) % 2].r;
+        }
+        if (cudaMalloc(&m->dec_blocks, nb * sizeof(DecodeBlock)) != cudaSuccess ||
+            cudaMemcpy(m->dec_blocks, db.data(), nb * sizeof(DecodeBlock), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMalloc(&m->dec_sync, nb * kDecodeSyncInts * 4) != cudaSuccess ||
+            cudaMemset(m->dec_sync, 0, nb * kDecodeSyncInts * 4) != cudaSuccess)
+            return fail(PGMOE_E_OOM);
+    }
     cudaEventCreate(&m->t0);
     m->stats.pinned_hbm_bytes = (int64_t)pinned;
     m->stats.slot_capacity_bytes = (int64_t)m->slot_capacity;
@@ -877,6 +954,8 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     if (m->host_pool) cudaFreeHost(m->host_pool);
     cudaFree(m->slots);
     cudaFree(m->route_ws);
+    cudaFree(m->dec_blocks);
+    cudaFree(m->dec_sync);
     cudaFree(m->tc_ws);
     cudaFree(m->epoch);
     cudaFree(m->act_buf[0]);
@@ -996,6 +1075,18 @@ extern "C" int pgmoe_model_set_fused_route(pgmoe_model *m, int32_t enabled) {
     m->fuse_route = enabled != 0;
     return PGMOE_OK;
 }
+
+extern "C" int pgmoe_model_set_decode(pgmoe_model *m, int32_t enabled, int32_t max_tokens) {
+    PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
+    PG_REQUIRE(max_tokens >= 0 && max_tokens <= kDecodeMaxT, PGMOE_E_CONFIG,
+               "decode kernel serves 1..%d tokens per iteration", kDecodeMaxT);
+    drop_graphs(m);
+    m->decode = enabled != 0;
+    if (max_tokens > 0) m->decode_max_t = max_tokens;
+    return PGMOE_OK;
+}
+
+extern "C" int64_t pgmoe_model_decode_iterations(pgmoe_model *m) { return m ? m->decode_iters : 0; }
 
 extern "C" int pgmoe_model_init_weights(pgmoe_model *m) {
     const auto &c = m->cfg;
