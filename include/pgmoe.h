@@ -286,6 +286,12 @@ PGMOE_API int pgmoe_model_set_fused_route(pgmoe_model *m, int32_t enabled);
 PGMOE_API int pgmoe_model_set_decode(pgmoe_model *m, int32_t enabled, int32_t max_tokens);
 /* Decoder iterations served by the persistent small-batch launch so far. */
 PGMOE_API int64_t pgmoe_model_decode_iterations(pgmoe_model *m);
+/* Low-latency small-batch decoder (decode_ll.cu, T <= 8): one persistent
+ * launch per decoder iteration whose phases exchange flag-in-word (LL)
+ * stores; takes precedence over pgmoe_model_set_decode's kernel for
+ * T <= max_tokens.  Same contract as decoder_iteration (core.py:342-383). */
+PGMOE_API int pgmoe_model_set_ll_decode(pgmoe_model *m, int32_t enabled, int32_t max_tokens);
+PGMOE_API int64_t pgmoe_model_ll_decode_iterations(pgmoe_model *m);
 
 /* decoder_iteration (core.py:342-383) for T tokens, device buffers.
  * x_in / y_out: fp32 [T][d] device.  ids_trace / w_trace (optional, device):

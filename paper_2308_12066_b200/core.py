@@ -370,6 +370,16 @@ class DeviceModel:
         per decoder iteration (pgmoe_model_set_decode)."""
         _lib.check(self._L.pgmoe_model_set_decode(self._h, 1 if enabled else 0, int(max_tokens)))
 
+    def set_ll_decode(self, enabled: bool, max_tokens: int = 0) -> None:
+        """Resident, T <= max_tokens (<= 8): the low-latency decoder — one
+        persistent launch per decoder iteration whose phases exchange LL
+        (flag-in-word) stores (pgmoe_model_set_ll_decode)."""
+        _lib.check(self._L.pgmoe_model_set_ll_decode(self._h, 1 if enabled else 0, int(max_tokens)))
+
+    @property
+    def ll_decode_iterations(self) -> int:
+        return int(self._L.pgmoe_model_ll_decode_iterations(self._h))
+
     @property
     def decode_iterations(self) -> int:
         return int(self._L.pgmoe_model_decode_iterations(self._h))

@@ -48,6 +48,28 @@ struct DecodeArgs {
 };
 
 bool decode_supported(int T, int d, int f, int E, int k, int L, int nb);
+
+// Low-latency small-batch decoder (decode_ll.cu): LL-word exchanges between
+// row-split phases, T <= kLLMaxT tokens.
+constexpr int kLLMaxT = 8;
+struct LLDecodeArgs {
+    int T, d, f, E, nb;
+    const DecodeBlock *blocks;
+    const void *experts;  // resident expert records [nb][E]
+    size_t rec_bytes;
+    const uint16_t *pool; // weight pool holding every dense matrix (DecodeBlock::dense_row0)
+    const float *x_in;
+    float *y_out;
+    void *ws;             // ll_decode_ws_bytes(max T), prepared once by ll_decode_prepare
+    size_t ws_bytes;
+    float *x_trace;       // optional traces (as DecodeArgs)
+    int32_t *ids_trace;
+    float *w_trace;
+};
+bool ll_decode_supported(int T, int d, int f, int E, int k, int L, int nb);
+size_t ll_decode_ws_bytes(int T, int d, int f, int E, int nb);
+int ll_decode_prepare(void *ws, cudaStream_t s);
+int ll_decode_iteration(const LLDecodeArgs &a, cudaStream_t s);
 int decode_iteration_tc(const DecodeArgs &a, cudaStream_t s);
 
 }  // namespace pgmoe

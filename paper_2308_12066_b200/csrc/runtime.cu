@@ -195,6 +195,12 @@ struct pgmoe_model {
     DecodeBlock *dec_blocks = nullptr;
     int *dec_sync = nullptr;
     int64_t decode_iters = 0;
+    // low-latency decoder (decode_ll.cu) for T <= ll_max_t: LL-word phase exchanges
+    bool ll_decode = true;       // pgmoe_model_set_ll_decode / PGMOE_LLDECODE=0
+    int ll_max_t = kLLMaxT;      // PGMOE_LLDECODE_MAX_T
+    void *ll_ws = nullptr;
+    size_t ll_ws_bytes = 0;
+    int64_t ll_iters = 0;
     bool fuse_route = true;    // resident: route inside the block launch (pgmoe_model_set_fused_route)
     long long fuse_max_t = 0;  // largest T routed inside the block launch (0: d_ff / 8; PGMOE_FUSE_MAX_T)
     // fused: launches chained on the previous dense phase instead of its
@@ -512,6 +518,38 @@ static int decode_iteration(pgmoe_model *m, const float *x_in, int T, float *y_o
     return PGMOE_OK;
 }
 
+// Small batches, low-latency form: block 0's gate (K1), then ONE persistent
+// launch (decode_ll.cu) whose phases exchange LL words.
+static int ll_decode_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, const pgmoe_iteration_io &io,
+                               cudaStream_t s) {
+    const auto &c = m->cfg;
+    PG_TRY(route_into(m, x_in, T, m->blocks[0].gate, 0, false, s, "gate", 0, io, 0));
+    LLDecodeArgs a{};
+    a.T = T;
+    a.d = c.d_model;
+    a.f = c.d_ff;
+    a.E = c.num_experts;
+    a.nb = c.num_blocks;
+    a.blocks = m->dec_blocks;
+    a.experts = m->blocks[0].experts;
+    a.rec_bytes = m->rec_bytes;
+    a.pool = reinterpret_cast<const uint16_t *>(m->dev_pool);
+    a.x_in = x_in;
+    a.y_out = y_out;
+    a.ws = m->ll_ws;
+    a.ws_bytes = m->ll_ws_bytes;
+    a.x_trace = io.x_trace;
+    a.ids_trace = io.ids_trace;
+    a.w_trace = io.w_trace;
+    tl_begin(m, "compute", "experts", 0, s);  // every block's experts, dense layers and pre-gates: one launch
+    PG_TRY(ll_decode_iteration(a, s));
+    tl_end(m, s);
+    m->fused_blocks += c.num_blocks;
+    m->fused_routes += c.num_blocks - 1;
+    m->ll_iters++;
+    return PGMOE_OK;
+}
+
 int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, const pgmoe_iteration_io &io,
                       cudaStream_t s) {
     const auto &c = m->cfg;
@@ -555,6 +593,9 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, co
     const bool fuse_route = !off && !io.ids_supplied && use_tc(m) && c.top_k == 1 && L == 1 && m->fuse_route &&
                             fused_route_supported(c.num_experts) &&
                             (long long)T <= (m->fuse_max_t > 0 ? m->fuse_max_t : c.d_ff / 8);
+    if (m->ll_decode && m->ll_ws && !off && !io.ids_supplied && use_tc(m) && m->fuse_route && T <= m->ll_max_t &&
+        ll_decode_supported(T, c.d_model, c.d_ff, c.num_experts, c.top_k, L, nb))
+        return ll_decode_iteration(m, x_in, T, y_out, io, s);
     if (m->decode && m->dec_blocks && !off && !io.ids_supplied && use_tc(m) && m->fuse_route &&
         T <= m->decode_max_t && decode_supported(T, c.d_model, c.d_ff, c.num_experts, c.top_k, L, nb))
         return decode_iteration(m, x_in, T, y_out, io, s);
@@ -914,7 +955,19 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
             cudaMalloc(&m->dec_sync, nb * kDecodeSyncInts * 4) != cudaSuccess ||
             cudaMemset(m->dec_sync, 0, nb * kDecodeSyncInts * 4) != cudaSuccess)
             return fail(PGMOE_E_OOM);
+        if (ll_decode_supported(1, (int)d, (int)f, c.num_experts, (int)k, c.activation_level, (int)nb)) {
+            const int tmax = std::min(max_tokens, kLLMaxT);
+            m->ll_ws_bytes = ll_decode_ws_bytes(tmax, (int)d, (int)f, c.num_experts, (int)nb);
+            if (cudaMalloc(&m->ll_ws, m->ll_ws_bytes) != cudaSuccess ||
+                cudaMemset(m->ll_ws, 0, m->ll_ws_bytes) != cudaSuccess)
+                return fail(PGMOE_E_OOM);
+            m->ll_max_t = tmax;
+            if ((st = ll_decode_prepare(m->ll_ws, nullptr)) != PGMOE_OK)
+                return fail(st);
+        }
     }
+    if (const char *e = getenv("PGMOE_LLDECODE")) m->ll_decode = (e[0] != '0');
+    if (const char *e = getenv("PGMOE_LLDECODE_MAX_T")) m->ll_max_t = std::max(0, std::min(m->ll_max_t, atoi(e)));
     cudaEventCreate(&m->t0);
     m->stats.pinned_hbm_bytes = (int64_t)pinned;
     m->stats.slot_capacity_bytes = (int64_t)m->slot_capacity;
@@ -956,6 +1009,7 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     cudaFree(m->route_ws);
     cudaFree(m->dec_blocks);
     cudaFree(m->dec_sync);
+    cudaFree(m->ll_ws);
     cudaFree(m->tc_ws);
     cudaFree(m->epoch);
     cudaFree(m->act_buf[0]);
@@ -1087,6 +1141,18 @@ extern "C" int pgmoe_model_set_decode(pgmoe_model *m, int32_t enabled, int32_t m
 }
 
 extern "C" int64_t pgmoe_model_decode_iterations(pgmoe_model *m) { return m ? m->decode_iters : 0; }
+
+extern "C" int pgmoe_model_set_ll_decode(pgmoe_model *m, int32_t enabled, int32_t max_tokens) {
+    PG_REQUIRE(m != nullptr, PGMOE_E_CONFIG, "null model");
+    PG_REQUIRE(max_tokens >= 0 && max_tokens <= kLLMaxT, PGMOE_E_CONFIG,
+               "low-latency decoder serves 1..%d tokens per iteration", kLLMaxT);
+    drop_graphs(m);
+    m->ll_decode = enabled != 0;
+    if (max_tokens > 0) m->ll_max_t = max_tokens;
+    return PGMOE_OK;
+}
+
+extern "C" int64_t pgmoe_model_ll_decode_iterations(pgmoe_model *m) { return m ? m->ll_iters : 0; }
 
 extern "C" int pgmoe_model_init_weights(pgmoe_model *m) {
     const auto &c = m->cfg;

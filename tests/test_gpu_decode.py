@@ -22,6 +22,7 @@ def _model(dims, T, placement="resident"):
     cfg = p.ModelConfig(d_model=dims.d_model, d_ff=dims.d_ff, num_blocks=dims.num_blocks,
                         num_experts=dims.num_experts, top_k=1, activation_level=1, seed=dims.seed)
     m = p.DeviceModel(cfg, dtype="bf16", placement=placement, max_tokens=T)
+    m.set_ll_decode(False)  # this file tests decode_tc.cu (the LL decoder: test_gpu_lldecode.py)
     m.set_decode(True, min(T, 64))  # the kernel serves up to 64 tokens (default threshold: 1)
     return m
 

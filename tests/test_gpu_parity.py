@@ -331,6 +331,7 @@ def test_fused_routing_equals_separate_launch_and_offloaded(E, T):
     dims = og.Dims(256, 2048, 5, E, 1, seed=7)  # the routing role is fused while T <= d_ff / 8
     x0 = torch.from_numpy(tokens(256, T)).cuda()
     fused = _device_model(dims, "bf16", "resident", max_tokens=T)
+    fused.set_ll_decode(False)
     fused.set_decode(False)  # the per-block launches (the persistent small-batch launch: test_gpu_decode.py)
     sep = _device_model(dims, "bf16", "resident", max_tokens=T)
     sep.set_fused_route(False)
