@@ -87,11 +87,12 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("PGMOE_LIB_PATH", LIB_PATH)  # A/B of library builds (tools/)
+    if not os.path.exists(path):
         raise errors.DeviceError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2308_12066_b200.build` "
+            f"{path} is missing: build it with `python -m paper_2308_12066_b200.build` "
             "(there is no CPU fallback)")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
     P = ctypes.POINTER
     sig = {

@@ -47,7 +47,7 @@ using tc::smem_u32;
 constexpr int kThreads = 384;
 constexpr int kCW0 = 2, kCWarps = 8, kCThreads = kCWarps * 32;  // compute warps
 constexpr int kRW0 = 10, kRThreads = 64;                        // reducer warps
-constexpr int kSlots = 3;
+constexpr int kMaxSlots = 6;  // weight-slice ring: as many slots as shared memory allows (>= 3)
 constexpr int kSlotBytes = 33792;
 constexpr int kDRows = 16;  // dense rows per dense CTA
 constexpr int kMaxE = 128;
@@ -60,6 +60,7 @@ struct Piece {
 
 struct Params {
     int T, d, f, E, nb, nd;           // nd: dense CTAs (d / kDRows)
+    int nslots;                       // weight-slice ring slots
     const DecodeBlock *blocks;
     const unsigned char *experts;     // records [nb][E]: W1 [f][d] then W2 [d][f]
     size_t rec_bytes;
@@ -110,6 +111,36 @@ __device__ __forceinline__ double poll_ll_f64(const unsigned long long *p, uint3
     while ((uint32_t)(a >> 32) != flag || (uint32_t)(b >> 32) != flag) ld_ll2(p, a, b);
     return __hiloint2double((int)(uint32_t)b, (int)(uint32_t)a);
 }
+// Poll U word pairs (one 16-byte load each) until every flag matches.  All
+// pending loads are re-issued together, so a batch waits about one round
+// trip after its data lands instead of one per word.
+template <int U, typename Addr>
+__device__ __forceinline__ void poll2(Addr addr, uint32_t valid, uint32_t flag, unsigned long long (&a)[U],
+                                      unsigned long long (&b)[U]) {
+    uint32_t pend = valid;
+    while (pend) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (pend >> u & 1u) ld_ll2(addr(u), a[u], b[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if ((pend >> u & 1u) && (uint32_t)(a[u] >> 32) == flag && (uint32_t)(b[u] >> 32) == flag)
+                pend &= ~(1u << u);
+    }
+}
+template <int U, typename Addr>
+__device__ __forceinline__ void poll1(Addr addr, uint32_t valid, uint32_t flag, unsigned long long (&a)[U]) {
+    uint32_t pend = valid;
+    while (pend) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (pend >> u & 1u) a[u] = ld_ll(addr(u));
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if ((pend >> u & 1u) && (uint32_t)(a[u] >> 32) == flag) pend &= ~(1u << u);
+    }
+}
+
 __device__ __forceinline__ void st_ll_f64(unsigned long long *p, double v, uint32_t flag) {
     const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
     st_ll2(p, ll_word((uint32_t)bits, flag), ll_word((uint32_t)(bits >> 32), flag));
@@ -132,9 +163,16 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// Device-side stamps (tools/probe_ll.py) exist only in a -DPGMOE_LL_PROBE
+// build: at T = 1 the launch is sensitive to every extra instruction on its
+// serial path (a handful of disabled stamps measured +4 us per block).
+#ifdef PGMOE_LL_PROBE
 __device__ __forceinline__ void dprobe(const Params &p, int b, int k) {
     if (p.probe && b < 5) p.probe[(size_t)blockIdx.x * kProbeSlots + 1 + 8 * b + k] = gtimer();
 }
+#else
+__device__ __forceinline__ void dprobe(const Params &, int, int) {}
+#endif
 __device__ __forceinline__ void csync() { named_sync(1, kCThreads); }
 __device__ __forceinline__ void rsync() { named_sync(2, kRThreads); }
 
@@ -143,7 +181,7 @@ __device__ __forceinline__ void rsync() { named_sync(2, kRThreads); }
 // Returns through `out` (thread ct < mt*128 owns output (ct / 8, ct % 8) of
 // its m-tile); rows past nrows repeat the last row (results discarded).
 __device__ __forceinline__ void piece_gemv(const unsigned char *A, int apitch, int nrows, const unsigned char *B,
-                                           int bpitch, int K, float *red, int ct, float &out, int &orow, int &otok) {
+                                           int bpitch, int brows, int K, float *red, int ct, float &out, int &orow, int &otok) {
     const int w = ct >> 5, lane = ct & 31, g = lane >> 2, t4 = lane & 3;
     const int mt = nrows > 16 ? 2 : 1, S = kCWarps / mt;
     const int m = w / S, s = w - m * S;
@@ -151,7 +189,7 @@ __device__ __forceinline__ void piece_gemv(const unsigned char *A, int apitch, i
     const int r0 = min(m * 16 + g, nrows - 1), r1 = min(m * 16 + g + 8, nrows - 1);
     const unsigned char *a0p = A + (size_t)r0 * apitch + t4 * 4;
     const unsigned char *a1p = A + (size_t)r1 * apitch + t4 * 4;
-    const unsigned char *bp = B + (size_t)g * bpitch + t4 * 4;
+    const unsigned char *bp = B + (size_t)min(g, brows - 1) * bpitch + t4 * 4;  // staged rows only
     float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
     for (int ks = k0; ks < k1; ++ks) {
@@ -199,35 +237,32 @@ __device__ __forceinline__ void stage(unsigned char *act, int K, int ng, const i
     for (int i0 = ct; i0 < n_all; i0 += U * kCThreads) {
         unsigned long long a[U], b[U];
         int n[U], k[U];
+        uint32_t valid = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = i0 + u * kCThreads;
-            n[u] = i / npair;
-            k[u] = 2 * (i - n[u] * npair);
-            if (i < n_all) {
-                const int t = tok ? tok[n[u]] : n[u];
-                if (plain) {
+            n[u] = min(i, n_all - 1) / npair;
+            k[u] = 2 * (min(i, n_all - 1) - n[u] * npair);
+            if (i < n_all) valid |= 1u << u;
+        }
+        if (plain) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (valid >> u & 1u) {
+                    const int t = tok ? tok[n[u]] : n[u];
                     const float2 v = __ldcg(reinterpret_cast<const float2 *>(plain + (size_t)t * plain_stride + k[u]));
                     a[u] = __float_as_uint(v.x);
                     b[u] = __float_as_uint(v.y);
-                } else {
-                    ld_ll2(ll + (size_t)t * ll_stride + k[u], a[u], b[u]);
                 }
-            }
+        } else {
+            poll2<U>([&](int u) { return ll + (size_t)(tok ? tok[n[u]] : n[u]) * ll_stride + k[u]; }, valid, flag, a, b);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = i0 + u * kCThreads;
-            if (i < n_all) {
-                if (!plain) {
-                    const unsigned long long *q = ll + (size_t)(tok ? tok[n[u]] : n[u]) * ll_stride + k[u];
-                    while ((uint32_t)(a[u] >> 32) != flag || (uint32_t)(b[u] >> 32) != flag) ld_ll2(q, a[u], b[u]);
-                }
+        for (int u = 0; u < U; ++u)
+            if (valid >> u & 1u)
                 *reinterpret_cast<uint32_t *>(act + (size_t)n[u] * apitch + k[u] * 2) =
                     (uint32_t)bf16_bits(__uint_as_float((uint32_t)a[u])) |
                     ((uint32_t)bf16_bits(__uint_as_float((uint32_t)b[u])) << 16);
-            }
-        }
     }
     csync();
 }
@@ -272,11 +307,12 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
     const int c = blockIdx.x, G = gridDim.x;
     const int dpitch = d * 2 + 16;
     // ---- shared memory layout ------------------------------------------
+    const int kSlots = p.nslots;
     unsigned char *slots = smem_raw;                                    // kSlots x kSlotBytes
-    unsigned char *dbuf = slots + kSlots * kSlotBytes;                  // kDRows x dpitch
+    unsigned char *dbuf = slots + (size_t)kSlots * kSlotBytes;          // kDRows x dpitch
     uint16_t *gsl = reinterpret_cast<uint16_t *>(dbuf + kDRows * dpitch);  // kDRows x E pre-gate rows
-    unsigned char *act = reinterpret_cast<unsigned char *>(gsl + kDRows * E);  // 8 x (max(d,f) * 2 + 16)
-    float *red = reinterpret_cast<float *>(act + 8 * (size_t)(f * 2 + 16));    // kCWarps x 128
+    unsigned char *act = reinterpret_cast<unsigned char *>(gsl + kDRows * E);  // T x (max(d,f) * 2 + 16)
+    float *red = reinterpret_cast<float *>(act + (size_t)((T + 1) & ~1) * (f * 2 + 16));  // kCWarps x 128
     float *ytile = red + kCWarps * 128;                                         // kDRows x 8
     float *rx = ytile + kDRows * 8;                                             // reducer: x [d]
     double *rlg = reinterpret_cast<double *>(rx + d);                           // [kRThreads] chunk sums
@@ -300,7 +336,9 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
         mbar_init(dfull, 1);
         mbar_init(dempty, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#ifdef PGMOE_LL_PROBE
         if (p.probe) p.probe[(size_t)c * kProbeSlots] = gtimer();
+#endif
     }
     __syncthreads();
     const bool dense_cta = c < p.nd;
@@ -361,41 +399,44 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                 reinterpret_cast<float *>(sched)[kLLMaxT + lane] = w;
             }
             __syncwarp();
-            if (lane == 0) {
-                dprobe(p, b, 0);
-                // active experts ascending; tokens of each in ascending order (stable)
-                int ex[kLLMaxT], na = 0;
-                for (int t = 0; t < T; ++t) {
-                    const int e = sched[t];
-                    int pos = 0;
-                    bool seen = false;
-                    for (int a = 0; a < na; ++a) {
-                        seen |= ex[a] == e;
-                        pos += ex[a] < e;
-                    }
-                    if (!seen) {
-                        for (int a = na; a > pos; --a) ex[a] = ex[a - 1];
-                        ex[pos] = e;
-                        ++na;
-                    }
+            // every lane walks the same schedule; lane 0 publishes the piece
+            // descriptors and arms the barriers, the lanes issue one row copy each
+            if (lane == 0) dprobe(p, b, 0);
+            // active experts ascending; tokens of each in ascending order (stable)
+            int ex[kLLMaxT], na = 0;
+            for (int t = 0; t < T; ++t) {
+                const int e = sched[t];
+                int pos = 0;
+                bool seen = false;
+                for (int a = 0; a < na; ++a) {
+                    seen |= ex[a] == e;
+                    pos += ex[a] < e;
                 }
-                const unsigned char *recs = p.experts + (size_t)b * E * p.rec_bytes;
-                for (int ph = 0; ph < 2; ++ph) {
-                    const int R = ph == 0 ? f : d, K = ph == 0 ? d : f;
-                    const int pitch = K * 2 + 16, prow = min(kSlotBytes / pitch, 32);
-                    const long long N = (long long)na * R;
-                    const long long lo = N * c / G, hi = N * (c + 1) / G;
-                    long long r = lo;
-                    do {
-                        const int slot = pc % kSlots;
-                        if (pc >= kSlots) mbar_wait(&empty[slot], ((pc / kSlots) - 1) & 1);
-                        Piece &pd = desc[slot];
-                        pd.b = b;
-                        pd.phase = ph;
-                        if (r < hi) {
-                            const int a = (int)(r / R), rr = (int)(r - (long long)a * R);
-                            const int n = (int)min((long long)min(R - rr, prow), hi - r);
-                            const int e = ex[a];
+                if (!seen) {
+                    for (int a = na; a > pos; --a) ex[a] = ex[a - 1];
+                    ex[pos] = e;
+                    ++na;
+                }
+            }
+            const unsigned char *recs = p.experts + (size_t)b * E * p.rec_bytes;
+            for (int ph = 0; ph < 2; ++ph) {
+                const int R = ph == 0 ? f : d, K = ph == 0 ? d : f;
+                const int pitch = K * 2 + 16, prow = min(kSlotBytes / pitch, 32);
+                const long long N = (long long)na * R;
+                const long long lo = N * c / G, hi = N * (c + 1) / G;
+                long long r = lo;
+                do {
+                    const int slot = pc % kSlots;
+                    if (pc >= kSlots) mbar_wait(&empty[slot], ((pc / kSlots) - 1) & 1);
+                    Piece &pd = desc[slot];
+                    if (r < hi) {
+                        const int a = (int)(r / R), rr = (int)(r - (long long)a * R);
+                        const int n = (int)min((long long)min(R - rr, prow), hi - r);
+                        const int e = ex[a];
+                        r += n;
+                        if (lane == 0) {
+                            pd.b = b;
+                            pd.phase = ph;
                             pd.e = e;
                             pd.row0 = rr;
                             pd.nrows = n;
@@ -407,24 +448,26 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                                     ++ng;
                                 }
                             pd.ng = ng;
-                            r += n;
                             pd.end = r >= hi;
-                            const unsigned char *src = recs + (size_t)e * p.rec_bytes +
-                                                       (ph == 0 ? (size_t)rr * d * 2
-                                                                : (size_t)f * d * 2 + (size_t)rr * f * 2);
                             mbar_expect_tx(&full[slot], (uint32_t)(n * K * 2));
-                            for (int i = 0; i < n; ++i)
-                                bulk_g2s(slots + (size_t)slot * kSlotBytes + i * pitch, src + (size_t)i * K * 2,
-                                         K * 2, &full[slot], pol);
-                        } else {  // no rows of this phase here: an empty marker piece
-                            pd.nrows = 0;
-                            pd.ng = 0;
-                            pd.end = 1;
-                            mbar_arrive(&full[slot]);
                         }
-                        ++pc;
-                    } while (r < hi);
-                }
+                        __syncwarp();
+                        const unsigned char *src = recs + (size_t)e * p.rec_bytes +
+                                                   (ph == 0 ? (size_t)rr * d * 2 : (size_t)f * d * 2 + (size_t)rr * f * 2);
+                        for (int i = lane; i < n; i += 32)
+                            bulk_g2s(slots + (size_t)slot * kSlotBytes + i * pitch, src + (size_t)i * K * 2, K * 2,
+                                     &full[slot], pol);
+                    } else if (lane == 0) {  // no rows of this phase here: an empty marker piece
+                        pd.b = b;
+                        pd.phase = ph;
+                        pd.nrows = 0;
+                        pd.ng = 0;
+                        pd.end = 1;
+                        mbar_arrive(&full[slot]);
+                    }
+                    __syncwarp();
+                    ++pc;
+                } while (r < hi);
             }
             __syncwarp();
         }
@@ -473,17 +516,15 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                 double s = 0.0;
                 for (int q0 = qp0; q0 < qp1; q0 += 16) {
                     unsigned long long lo[16], hi[16];
+                    uint32_t valid = 0;
 #pragma unroll
                     for (int u = 0; u < 16; ++u)
-                        if (q0 + u < qp1) ld_ll2(base + (((size_t)(q0 + u) * T + t) * W + j) * 2, lo[u], hi[u]);
+                        if (q0 + u < qp1) valid |= 1u << u;
+                    poll2<16>([&](int u) { return base + (((size_t)(q0 + u) * T + t) * W + j) * 2; }, valid, fin, lo,
+                              hi);
 #pragma unroll
                     for (int u = 0; u < 16; ++u)
-                        if (q0 + u < qp1) {
-                            const unsigned long long *qq = base + (((size_t)(q0 + u) * T + t) * W + j) * 2;
-                            while ((uint32_t)(lo[u] >> 32) != fin || (uint32_t)(hi[u] >> 32) != fin)
-                                ld_ll2(qq, lo[u], hi[u]);
-                            s += __hiloint2double((int)(uint32_t)hi[u], (int)(uint32_t)lo[u]);
-                        }
+                        if (valid >> u & 1u) s += __hiloint2double((int)(uint32_t)hi[u], (int)(uint32_t)lo[u]);
                 }
                 rlg[kc * 16 + jj] = s;
             }
@@ -503,54 +544,48 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                 for (int i = rt; i < d; i += kRThreads) rx[i] = __ldcg(p.x_in + (size_t)t * d + i);
             } else {
                 const unsigned long long *xq = p.llx + ((size_t)par * T + t) * d;
-                for (int i0 = rt; i0 < d; i0 += 12 * kRThreads) {
-                    unsigned long long v[12];
+                for (int i0 = rt; i0 < d; i0 += 16 * kRThreads) {
+                    unsigned long long v[16];
+                    uint32_t valid = 0;
 #pragma unroll
-                    for (int u = 0; u < 12; ++u)
-                        if (i0 + u * kRThreads < d) v[u] = ld_ll(xq + i0 + u * kRThreads);
+                    for (int u = 0; u < 16; ++u)
+                        if (i0 + u * kRThreads < d) valid |= 1u << u;
+                    poll1<16>([&](int u) { return xq + i0 + u * kRThreads; }, valid, fin, v);
 #pragma unroll
-                    for (int u = 0; u < 12; ++u)
-                        if (i0 + u * kRThreads < d) {
-                            while ((uint32_t)(v[u] >> 32) != fin) v[u] = ld_ll(xq + i0 + u * kRThreads);
-                            rx[i0 + u * kRThreads] = __uint_as_float((uint32_t)v[u]);
-                        }
+                    for (int u = 0; u < 16; ++u)
+                        if (valid >> u & 1u) rx[i0 + u * kRThreads] = __uint_as_float((uint32_t)v[u]);
                 }
             }
-            double sx = 0.0, gx = 0.0;
-            if (rt < nd) {
-                sx = poll_ll_f64(base + (((size_t)rt * T + t) * W + E) * 2, fin);
-                gx = poll_ll_f64(base + (((size_t)rt * T + t) * W + E + 1) * 2, fin);
-            }
-            rsx[rt] = sx;
-            rgx[rt] = gx;
-            {
+            {   // the producers' sum|x| / max|G| words and the E logits: one batch
+                unsigned long long lo[4], hi[4];
+                const unsigned long long *pq = base + (((size_t)rt * T + t) * W + E) * 2;
                 const unsigned long long *lq = p.lllog + ((size_t)par * T + t) * E * 2;
-                unsigned long long lo[2], hi[2];
+                auto addr = [&](int u) { return u < 2 ? pq + 2 * u : lq + (rt + (u - 2) * kRThreads) * 2; };
+                uint32_t pend = (rt < nd ? 3u : 0u) | (rt < E ? 4u : 0u) | (rt + kRThreads < E ? 8u : 0u);
+                const uint32_t valid = pend;
+                while (pend) {
 #pragma unroll
-                for (int u = 0; u < 2; ++u)
-                    if (rt + u * kRThreads < E) ld_ll2(lq + (rt + u * kRThreads) * 2, lo[u], hi[u]);
+                    for (int u = 0; u < 4; ++u)
+                        if (pend >> u & 1u) ld_ll2(addr(u), lo[u], hi[u]);
 #pragma unroll
-                for (int u = 0; u < 2; ++u)
-                    if (rt + u * kRThreads < E) {
-                        while ((uint32_t)(lo[u] >> 32) != fout || (uint32_t)(hi[u] >> 32) != fout)
-                            ld_ll2(lq + (rt + u * kRThreads) * 2, lo[u], hi[u]);
-                        rsel[rt + u * kRThreads] = __hiloint2double((int)(uint32_t)hi[u], (int)(uint32_t)lo[u]);
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t fl = u < 2 ? fin : fout;
+                        if ((pend >> u & 1u) && (uint32_t)(lo[u] >> 32) == fl && (uint32_t)(hi[u] >> 32) == fl)
+                            pend &= ~(1u << u);
                     }
-            }
-            rsync();
-            if (rt == 0) {
-                double s = 0.0, g = 0.0;
-                for (int k = 0; k < nd; ++k) {
-                    s += rsx[k];
-                    g = fmax(g, rgx[k]);
                 }
-                rsx[kRThreads] = s;
-                rgx[0] = g;
+                rsx[rt] = (valid & 1u) ? __hiloint2double((int)(uint32_t)hi[0], (int)(uint32_t)lo[0]) : 0.0;
+                rgx[rt] = (valid & 2u) ? __hiloint2double((int)(uint32_t)hi[1], (int)(uint32_t)lo[1]) : 0.0;
+                if (valid & 4u) rsel[rt] = __hiloint2double((int)(uint32_t)hi[2], (int)(uint32_t)lo[2]);
+                if (valid & 8u) rsel[rt + kRThreads] = __hiloint2double((int)(uint32_t)hi[3], (int)(uint32_t)lo[3]);
             }
-            rsync();
-            for (int j = rt; j < E; j += kRThreads) rcm[j] = (float)rgx[0];  // exact: a bf16 magnitude
             rsync();
             if (rt < 32) {
+                const double sxt = warp_sumd(rsx[rt] + rsx[rt + 32]);
+                const double gxt = warp_max(fmax(rgx[rt], rgx[rt + 32]));
+                for (int j = rt; j < E; j += 32) rcm[j] = (float)gxt;  // exact: a bf16 magnitude
+                if (rt == 0) rsx[kRThreads] = sxt;
+                __syncwarp();
                 TileSums ts;
                 ts.lgs = rsel;
                 ts.cms = rcm;
@@ -624,7 +659,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                         if (first && ct == 0) dprobe(p, b, ph == 0 ? 1 : 3);
                         first = false;
                     }
-                    piece_gemv(slots + (size_t)slot * kSlotBytes, K * 2 + 16, nrows, act, K * 2 + 16, K, red, ct,
+                    piece_gemv(slots + (size_t)slot * kSlotBytes, K * 2 + 16, nrows, act, K * 2 + 16, ng, K, red, ct,
                                out, orow, otok);
                     if (orow >= 0 && orow < nrows && otok < ng) {
                         const int t = my_t;
@@ -648,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
             mbar_wait(dfull, dfill & 1);
             stage(act, d, T, nullptr, p.llmix, d, nullptr, 0, fl, ct);
             if (ct == 0) dprobe(p, b, 6);
-            piece_gemv(dbuf, dpitch, kDRows, act, d * 2 + 16, d, red, ct, out, orow, otok);
+            piece_gemv(dbuf, dpitch, kDRows, act, d * 2 + 16, T, d, red, ct, out, orow, otok);
             if (orow >= 0 && otok < T) {
                 const int row = dr0 + orow;
                 ytile[orow * 8 + otok] = out;
@@ -678,16 +713,26 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
             p.ctr[0] = epoch + 1 > 0x3FFFFFFu ? 1u : epoch + 1;
             __threadfence();
         }
+#ifdef PGMOE_LL_PROBE
         if (p.probe) p.probe[(size_t)c * kProbeSlots + 41] = gtimer();
+#endif
     }
 }
 
-size_t smem_bytes(int d, int f, int E) {
-    size_t s = (size_t)kSlots * kSlotBytes + (size_t)kDRows * (d * 2 + 16) + (size_t)kDRows * E * 2 +
-               8 * (size_t)(f * 2 + 16) + (size_t)kCWarps * 128 * 4 + kDRows * 8 * 4 + (size_t)d * 4 +
-               (kRThreads + kMaxE) * 8 + kMaxE * 4 + (2 * kRThreads + 1) * 8 + kSlots * sizeof(Piece) + 16 +
-               (2 * kSlots + 2) * 8 + 2 * kLLMaxT * 4 + 64;
-    return s;
+// Shared memory of a launch: the weight ring (nslots), the dense slice, the
+// staged activations of T tokens (mma B rows past T are never read: columns
+// repeat the last staged token) and small per-role buffers.
+size_t smem_bytes(int T, int d, int f, int E, int nslots) {
+    return (size_t)nslots * kSlotBytes + (size_t)kDRows * (d * 2 + 16) + (size_t)kDRows * E * 2 +
+           (size_t)((T + 1) & ~1) * (f * 2 + 16) + (size_t)kCWarps * 128 * 4 + kDRows * 8 * 4 + (size_t)d * 4 +
+           (kRThreads + kMaxE) * 8 + kMaxE * 4 + (2 * kRThreads + 1) * 8 + nslots * sizeof(Piece) + 16 +
+           (2 * nslots + 2) * 8 + 2 * kLLMaxT * 4 + 64;
+}
+constexpr size_t kSmemCap = 226 * 1024;
+int pick_slots(int T, int d, int f, int E) {
+    int n = kMaxSlots;
+    while (n > 3 && smem_bytes(T, d, f, E, n) > kSmemCap) --n;
+    return n;
 }
 
 }  // namespace ll
@@ -695,7 +740,7 @@ size_t smem_bytes(int d, int f, int E) {
 bool ll_decode_supported(int T, int d, int f, int E, int k, int L, int nb) {
     return T >= 1 && T <= kLLMaxT && k == 1 && L == 1 && d % ll::kDRows == 0 && d % 16 == 0 && f % 16 == 0 &&
            (E == 64 || E == 128) && nb >= 2 && nb <= kDecodeMaxBlocks && d * 2 + 16 <= ll::kSlotBytes &&
-           f * 2 + 16 <= ll::kSlotBytes && ll::smem_bytes(d, f, E) <= 226 * 1024 &&
+           f * 2 + 16 <= ll::kSlotBytes && ll::smem_bytes(kLLMaxT, d, f, E, 3) <= ll::kSmemCap &&
            d / ll::kDRows <= ll::kRThreads &&
            d / ll::kDRows + kLLMaxT * (E / 16) <= device_sm_count();
 }
@@ -725,7 +770,8 @@ int ll_decode_prepare(void *ws, cudaStream_t s) {
 
 int ll_decode_iteration(const LLDecodeArgs &a, cudaStream_t s) {
     using namespace ll;
-    const size_t smem = smem_bytes(a.d, a.f, a.E);
+    const int nslots = pick_slots(a.T, a.d, a.f, a.E);
+    const size_t smem = smem_bytes(a.T, a.d, a.f, a.E, nslots);
     static size_t attr_smem[64] = {0};  // per device: dynamic shared memory the attribute allows
     static int grid_dev[64] = {0};
     const int dev = current_device();
@@ -750,6 +796,7 @@ int ll_decode_iteration(const LLDecodeArgs &a, cudaStream_t s) {
     p.E = a.E;
     p.nb = a.nb;
     p.nd = nd;
+    p.nslots = nslots;
     p.blocks = a.blocks;
     p.experts = static_cast<const unsigned char *>(a.experts);
     p.rec_bytes = a.rec_bytes;
