@@ -342,9 +342,13 @@ def run_ours(args, rank: int, world: int):
     # ---- profile pass: per-kernel CUDA events on the compute / copy streams
     prof_steps = max(1, min(args.steps, 3))
     model.set_timeline(True)
+    ll0, dec0 = model.ll_decode_iterations, model.decode_iterations
     for _ in range(prof_steps):
         model.decoder_iteration(x)
     torch.cuda.synchronize()
+    # which launch served the iteration: the low-latency decoder (decode_ll.cu), the
+    # persistent tcgen05 decoder (decode_tc.cu) or one block launch per block (ffn_tc.cu)
+    served = ("ll" if model.ll_decode_iterations > ll0 else "decode" if model.decode_iterations > dec0 else "blocks")
     tl = model.timeline()
     model.set_timeline(False)
     # the profile pass runs the host loop (no graph replay), so its stats say
@@ -492,8 +496,13 @@ def run_ours(args, rank: int, world: int):
                            "bound": bound, "t_hbm_ms": round(bounds["hbm"] * 1e3, 4),
                            "t_tensor_ms": round(bounds["tensor"] * 1e3, 4),
                            "t_pcie_ms": round(bounds["pcie"] * 1e3, 4), "n_act_avg": round(nact_avg, 2)},
-        "roofline": {"bound": "hbm", "kernel": "K2 up+down" + (" + K3 dense" if fused else "") +
-                     (" + next block's K1 routing" if routed_in_launch else "") + (", one launch" if fused else ""),
+        "roofline": {"bound": "hbm",
+                     "kernel": ({"ll": "ll_decode_kernel (decode_ll.cu): every block's up+down+dense and pre-gates, "
+                                       "one launch per decoder iteration",
+                                 "decode": "decode_kernel (decode_tc.cu): every block, one launch per iteration"}
+                                .get(served) or ("K2 up+down" + (" + K3 dense" if fused else "") +
+                                                 (" + next block's K1 routing" if routed_in_launch else "") +
+                                                 (", one launch" if fused else ""))),
                      "achieved": round(ffn_gbs, 1) if ffn_gbs else None, "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(ffn_gbs / hbm_peak, 4) if ffn_gbs else None,
                      "traffic": ncu_traffic("ffn", workload_name(args.preset, args.placement, T) +

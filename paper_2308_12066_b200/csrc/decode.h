@@ -60,6 +60,8 @@ struct LLDecodeArgs {
     const uint16_t *pool; // weight pool holding every dense matrix (DecodeBlock::dense_row0)
     const float *x_in;
     float *y_out;
+    const void *gate0;        // block 0's conventional gate (bf16 [d][E]): routed inside the launch
+    pgmoe_routing gate0_out;  // where its decision goes (the routing block 0 consumes)
     void *ws;             // ll_decode_ws_bytes(max T), prepared once by ll_decode_prepare
     size_t ws_bytes;
     float *x_trace;       // optional traces (as DecodeArgs)

@@ -67,10 +67,13 @@ struct Params {
     const uint16_t *pool;             // weight pool: dense(b) = pool + blocks[b].dense_row0 * d
     const float *x_in;
     float *y_out;
+    const uint16_t *gate0;            // block 0's conventional gate [d][E] (core.py:362-366)
+    pgmoe_routing gate0_out;          // the decision it writes (block 0 consumes it)
     unsigned long long *llx;          // [2][T][d]
     unsigned long long *llh;          // [T][f]
     unsigned long long *llmix;        // [T][d]
-    unsigned long long *llpart;       // [2][nd][T][E + 2] x 2 words (fp64 halves): logits, sum|x|, max|G|
+    unsigned long long *llpart;       // [2][nd][T][E + 2] x 2 words (fp64 halves): logits, sum|x|, max|G|;
+                                      // gate g (0: block 0's gate, b + 1: block b's pre-gate) uses [g & 1]
     unsigned long long *lllog;        // [2][T][E] x 2 words: the reducers' logits
     unsigned long long *lldec;        // [nb][kLLMaxT] x 2 words (id, weight)
     unsigned *ctr;                    // [0] epoch (>= 1), [1] CTAs finished
@@ -81,7 +84,9 @@ struct Params {
     unsigned long long *probe;
 };
 
-__device__ __forceinline__ uint32_t flag_of(uint32_t epoch, int b) { return (epoch << 6) + (uint32_t)(b + 1); }
+// flag of the words produced during block b (b = -1: the launch prologue; -2:
+// block 0's conventional gate): never 0, the value of fresh memory
+__device__ __forceinline__ uint32_t flag_of(uint32_t epoch, int b) { return (epoch << 7) + (uint32_t)(b + 2); }
 __device__ __forceinline__ unsigned long long ll_word(uint32_t payload, uint32_t flag) {
     return ((unsigned long long)flag << 32) | payload;
 }
@@ -311,7 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
     unsigned char *slots = smem_raw;                                    // kSlots x kSlotBytes
     unsigned char *dbuf = slots + (size_t)kSlots * kSlotBytes;          // kDRows x dpitch
     uint16_t *gsl = reinterpret_cast<uint16_t *>(dbuf + kDRows * dpitch);  // kDRows x E pre-gate rows
-    unsigned char *act = reinterpret_cast<unsigned char *>(gsl + kDRows * E);  // T x (max(d,f) * 2 + 16)
+    uint16_t *gsl0 = gsl + kDRows * E;                                     // block 0's gate rows (fill 0)
+    unsigned char *act = reinterpret_cast<unsigned char *>(gsl0 + kDRows * E);  // T x (max(d,f) * 2 + 16)
     float *red = reinterpret_cast<float *>(act + (size_t)((T + 1) & ~1) * (f * 2 + 16));  // kCWarps x 128
     float *ytile = red + kCWarps * 128;                                         // kDRows x 8
     float *rx = ytile + kDRows * 8;                                             // reducer: x [d]
@@ -349,14 +355,16 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
         if (lane == 0 && dense_cta) {
             uint64_t pol;
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-            // fill 0: the first pre-gate's rows (block 0 input = x_in); fill
+            // fill 0: block 0's gate and pre-gate rows (both on x_in); fill
             // b+1: dense(b) rows + pre-gate(b+1) rows
             for (int fl = 0; fl <= nb; ++fl) {
                 const int b = fl - 1;
                 const bool has_d = b >= 0;
                 const bool has_g = fl < nb && p.blocks[fl].has_pre_gate;
                 if (fl > 0) mbar_wait(dempty, (fl - 1) & 1);
-                const uint32_t bytes = (has_d ? kDRows * d * 2 : 0) + (has_g ? kDRows * E * 2 : 0);
+                const bool has_g0 = fl == 0;
+                const uint32_t bytes = (has_d ? kDRows * d * 2 : 0) + (has_g ? kDRows * E * 2 : 0) +
+                                       (has_g0 ? kDRows * E * 2 : 0);
                 if (bytes == 0) {
                     mbar_arrive(dfull);
                     continue;
@@ -369,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                 if (has_g)
                     bulk_g2s(gsl, static_cast<const uint16_t *>(p.blocks[fl].pre_gate) + (size_t)dr0 * E,
                              kDRows * E * 2, dfull, pol);
+                if (has_g0) bulk_g2s(gsl0, p.gate0 + (size_t)dr0 * E, kDRows * E * 2, dfull, pol);
             }
         }
         return;
@@ -382,16 +391,14 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         int pc = 0;  // pieces issued
         for (int b = 0; b < nb; ++b) {
-            // the decision block b consumes: K1 (b = 0) or the reducers (LL)
+            // the decision block b consumes, from the reducers (LL words): block 0's
+            // gate (b = 0) or block b-1's pre-gate
             if (lane < T) {
                 int id;
                 float w;
-                if (b == 0) {
-                    id = __ldcg(p.blocks[0].ids + lane);
-                    w = __ldcg(p.blocks[0].w + lane);
-                } else {
+                {
                     const unsigned long long *q = p.lldec + ((size_t)b * kLLMaxT + lane) * 2;
-                    const uint32_t fl = flag_of(epoch, b - 1);
+                    const uint32_t fl = flag_of(epoch, b == 0 ? -2 : b - 1);
                     id = (int)poll_ll(q, fl);
                     w = __uint_as_float(poll_ll(q + 1, fl));
                 }
@@ -494,21 +501,22 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
         r.gam = p.gam;
         r.bscale = p.bscale;
         r.x = rx - (size_t)t * d;  // serial fallback reads x[tok * d + i]: this token's copy in shared memory
-        if (selector && p.ids_trace && rt == 0) {
-            p.ids_trace[t] = __ldcg(p.blocks[0].ids + t);
-            p.w_trace[t] = __ldcg(p.blocks[0].w + t);
-        }
         if (selector && p.x_trace)
             for (int i = rt; i < d; i += kRThreads) p.x_trace[(size_t)t * d + i] = __ldcg(p.x_in + (size_t)t * d + i);
         const int W = E + 2, nd = p.nd;
         // thread (expert jj of 16, producer chunk k of 4)
         const int jj = rt % 16, kc = rt / 16, NK = kRThreads / 16;
         const int qp0 = nd * kc / NK, qp1 = nd * (kc + 1) / NK;
-        for (int b = 0; b + 1 < nb; ++b) {
-            const DecodeBlock &bd = p.blocks[b];
-            if (!bd.has_pre_gate) continue;
-            const uint32_t fin = flag_of(epoch, b - 1), fout = flag_of(epoch, b);
-            const int par = b & 1;
+        // gate g: 0 = block 0's conventional gate on x_in (core.py:362-366), g = b + 1 =
+        // block b's pre-gate on block b's input (core.py:327-329); decision for block g
+        for (int g = 0; g < nb; ++g) {
+            const int b = g - 1;  // the block whose pre-gate this is (-1: block 0's gate)
+            if (g > 0 && !p.blocks[b].has_pre_gate) continue;
+            // partials: written in the prologue (g <= 1) or by dense(g - 2); decision: flag of block b
+            const uint32_t fin = flag_of(epoch, g <= 1 ? -1 : g - 2), fout = flag_of(epoch, g == 0 ? -2 : b);
+            const int par = g & 1;
+            const void *Gm = g == 0 ? static_cast<const void *>(p.gate0) : p.blocks[b].pre_gate;
+            const pgmoe_routing rout = g == 0 ? p.gate0_out : p.blocks[b].out;
             const unsigned long long *base = p.llpart + (size_t)par * nd * T * W * 2;
             // 1. this CTA's 16 experts: partials of its producer chunk, in order
             {
@@ -540,10 +548,10 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
             }
             // 2. selector: this token's block input (the serial fallback's
             //    operand), the producers' sum|x| / max|G|, the E logits
-            if (b == 0) {
+            if (g <= 1) {
                 for (int i = rt; i < d; i += kRThreads) rx[i] = __ldcg(p.x_in + (size_t)t * d + i);
             } else {
-                const unsigned long long *xq = p.llx + ((size_t)par * T + t) * d;
+                const unsigned long long *xq = p.llx + ((size_t)(b & 1) * T + t) * d;
                 for (int i0 = rt; i0 < d; i0 += 16 * kRThreads) {
                     unsigned long long v[16];
                     uint32_t valid = 0;
@@ -590,17 +598,17 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                 ts.lgs = rsel;
                 ts.cms = rcm;
                 ts.sxs = rsx + kRThreads;
-                r.G = bd.pre_gate;
-                r.out = bd.out;
+                r.G = Gm;
+                r.out = rout;
                 if (E == 64) router_select_token<uint16_t, 2>(r, ts, 0, t, lane, s_ids, s_w);
                 else router_select_token<uint16_t, 4>(r, ts, 0, t, lane, s_ids, s_w);
                 __syncwarp();
                 if (lane == 0) {
-                    unsigned long long *qd = p.lldec + ((size_t)(b + 1) * kLLMaxT + t) * 2;
+                    unsigned long long *qd = p.lldec + ((size_t)g * kLLMaxT + t) * 2;
                     st_ll2(qd, ll_word((uint32_t)s_ids[0], fout), ll_word(__float_as_uint(s_w[0]), fout));
                     if (p.ids_trace) {
-                        p.ids_trace[(size_t)(b + 1) * T + t] = s_ids[0];
-                        p.w_trace[(size_t)(b + 1) * T + t] = s_w[0];
+                        p.ids_trace[(size_t)g * T + t] = s_ids[0];
+                        p.w_trace[(size_t)g * T + t] = s_w[0];
                     }
                     dprobe(p, b, 5);
                 }
@@ -615,19 +623,18 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
     int pc = 0, dfill = 0;
     float out;
     int orow, otok;
-    if (dense_cta && p.blocks[0].has_pre_gate) {  // the first pre-gate on x_in (fill 0)
+    if (dense_cta) {  // prologue (fill 0): block 0's gate and block 0's pre-gate, both on x_in
         mbar_wait(dfull, 0);
         for (int i = ct; i < kDRows * 8; i += kCThreads) {
             const int rr = i >> 3, t = i & 7;
             ytile[i] = t < T ? __ldcg(p.x_in + (size_t)t * d + dr0 + rr) : 0.f;
         }
         csync();
-        pregate_partials(p, ytile, gsl, red, c, 0, flag_of(epoch, -1), ct);
-        csync();
-        if (ct == 0) mbar_arrive(dempty);
-        dfill = 1;
-    } else if (dense_cta) {
-        mbar_wait(dfull, 0);
+        pregate_partials(p, ytile, gsl0, red, c, 0, flag_of(epoch, -1), ct);
+        if (p.blocks[0].has_pre_gate) {
+            csync();  // red is reused
+            pregate_partials(p, ytile, gsl, red, c, 1, flag_of(epoch, -1), ct);
+        }
         csync();
         if (ct == 0) mbar_arrive(dempty);
         dfill = 1;
@@ -695,7 +702,8 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                 }
             }
             csync();
-            if (b + 1 < nb && p.blocks[b + 1].has_pre_gate) pregate_partials(p, ytile, gsl, red, c, (b + 1) & 1, fl, ct);
+            if (b + 1 < nb && p.blocks[b + 1].has_pre_gate)  // gate g = b + 2
+                pregate_partials(p, ytile, gsl, red, c, b & 1, fl, ct);
             csync();
             if (ct == 0) {
                 mbar_arrive(dempty);
@@ -710,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
         __threadfence();
         if (atomicAdd(p.ctr + 1, 1u) == (unsigned)G - 1) {
             p.ctr[1] = 0;
-            p.ctr[0] = epoch + 1 > 0x3FFFFFFu ? 1u : epoch + 1;
+            p.ctr[0] = epoch + 1 > 0x1FFFFFFu ? 1u : epoch + 1;
             __threadfence();
         }
 #ifdef PGMOE_LL_PROBE
@@ -723,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
 // staged activations of T tokens (mma B rows past T are never read: columns
 // repeat the last staged token) and small per-role buffers.
 size_t smem_bytes(int T, int d, int f, int E, int nslots) {
-    return (size_t)nslots * kSlotBytes + (size_t)kDRows * (d * 2 + 16) + (size_t)kDRows * E * 2 +
+    return (size_t)nslots * kSlotBytes + (size_t)kDRows * (d * 2 + 16) + (size_t)2 * kDRows * E * 2 +
            (size_t)((T + 1) & ~1) * (f * 2 + 16) + (size_t)kCWarps * 128 * 4 + kDRows * 8 * 4 + (size_t)d * 4 +
            (kRThreads + kMaxE) * 8 + kMaxE * 4 + (2 * kRThreads + 1) * 8 + nslots * sizeof(Piece) + 16 +
            (2 * nslots + 2) * 8 + 2 * kLLMaxT * 4 + 64;
@@ -803,6 +811,8 @@ int ll_decode_iteration(const LLDecodeArgs &a, cudaStream_t s) {
     p.pool = a.pool;
     p.x_in = a.x_in;
     p.y_out = a.y_out;
+    p.gate0 = static_cast<const uint16_t *>(a.gate0);
+    p.gate0_out = a.gate0_out;
     char *w = static_cast<char *>(a.ws);
     size_t off[6];
     const size_t need = ll_ws_layout(a.T, a.d, a.f, a.E, a.nb, off);

@@ -518,13 +518,14 @@ static int decode_iteration(pgmoe_model *m, const float *x_in, int T, float *y_o
     return PGMOE_OK;
 }
 
-// Small batches, low-latency form: block 0's gate (K1), then ONE persistent
-// launch (decode_ll.cu) whose phases exchange LL words.
+// Small batches, low-latency form: ONE persistent launch per decoder iteration
+// (decode_ll.cu), block 0's gate included; its phases exchange LL words.
 static int ll_decode_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, const pgmoe_iteration_io &io,
                                cudaStream_t s) {
     const auto &c = m->cfg;
-    PG_TRY(route_into(m, x_in, T, m->blocks[0].gate, 0, false, s, "gate", 0, io, 0));
     LLDecodeArgs a{};
+    a.gate0 = m->blocks[0].gate;  // block 0's gate is routed inside the launch too: one launch per iteration
+    a.gate0_out = m->routing[0].r;
     a.T = T;
     a.d = c.d_model;
     a.f = c.d_ff;
