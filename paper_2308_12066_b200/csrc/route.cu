@@ -555,8 +555,14 @@ constexpr int kClusterMaxS = 16;
 constexpr size_t kClusterGBytes = 64 * 1024;  // gate slice per CTA
 
 struct ClusterLayout {
-    size_t r0, x, part, cm, xs, total;  // byte offsets in dynamic shared memory
+    size_t r0, x, part, cm, xs, ext, total;  // byte offsets in dynamic shared memory
 };
+// register blocking of the partial-logit loop: a thread owns 2 experts x TB tokens
+__host__ __device__ constexpr int cl_tb(int tok) { return tok < 4 ? tok : 4; }
+__host__ __device__ inline int cl_row_slices(int tok, int E) {
+    const int units = (E / 2) * (tok / cl_tb(tok));
+    return units >= kLogitThreads ? 1 : kLogitThreads / units;
+}
 __host__ __device__ inline ClusterLayout cluster_layout(int tok, int kn, int E, size_t gbytes) {
     auto up = [](size_t v) { return (v + 15) & ~(size_t)15; };
     ClusterLayout l;
@@ -568,7 +574,9 @@ __host__ __device__ inline ClusterLayout cluster_layout(int tok, int kn, int E, 
     l.part = l.x + up((size_t)tok * kn * 8);
     l.cm = l.part + up((size_t)tok * E * 8);
     l.xs = l.cm + up((size_t)E * 4);
-    l.total = l.xs + up((size_t)tok * 8) + 16;
+    l.ext = l.xs + up((size_t)tok * 8);  // row slices > 0: partial logits + column maxima
+    const int rs = cl_row_slices(tok, E);
+    l.total = l.ext + up((size_t)(rs - 1) * tok * E * 8) + up((size_t)rs * E * 4) + 16;
     return l;
 }
 
@@ -620,56 +628,99 @@ __global__ void __launch_bounds__(kLogitThreads) route_cluster_kernel(const Rout
     }
     pdl_wait();  // x is produced by the previous kernel in the stream
     if (tid == 0) probe(p.probe, cta, 1);
-    // 2. x slice (fp32 -> fp64, exact)
+    // 2. x slice (fp32 -> fp64, exact), row-major [i][TOK]: a row's tokens are adjacent
     const float *X = static_cast<const float *>(p.x);
-    for (int i = tid; i < TOK * kn; i += kLogitThreads) {
-        const int t = i / kn;
-        sx[i] = t < ntok ? (double)__ldg(X + (size_t)(t0 + t) * d + k0 + (i - t * kn)) : 0.0;
+    for (int q = tid; q < TOK * kn; q += kLogitThreads) {
+        const int t = q / kn, i = q - t * kn;
+        sx[i * TOK + t] = t < ntok ? (double)__ldg(X + (size_t)(t0 + t) * d + k0 + i) : 0.0;
     }
     __syncthreads();
     if (warp < TOK) {  // sum |x_i| over the slice (bounds the logit error)
         double v = 0.0;
-        for (int i = lane; i < kn; i += 32) v += fabs(sx[warp * kn + i]);
+        for (int i = lane; i < kn; i += 32) v += fabs(sx[i * TOK + warp]);
         v = warp_sumd(v);
         if (lane == 0) sxs[warp] = v;
     }
     if (tid == 0) probe(p.probe, cta, 10);  // x slice in shared memory
-    // 3. partial logits: thread (tg, j) owns expert j for tokens tg, tg + NTG, ...
+    // 3. partial logits, register-blocked: thread (row slice rs, token group tg,
+    //    expert pair jp) owns experts 2jp, 2jp+1 for tokens [TB tg, TB tg + TB) over
+    //    its rows; per row one gate-pair load and TB/2 16-byte (broadcast) x loads
+    //    feed 2 TB independent DFMA chains (the per-DFMA shared-memory load of the
+    //    one-expert form kept the loop MIO-bound).  Row slices are added in slice
+    //    order: deterministic, and any order is inside the certified bound.
     {
-        const int NTG = max(1, kLogitThreads / E);
-        const int j = tid % E, tg = tid / E;
-        if (tg < NTG && tid < NTG * E) {
-            double acc[TOK];
+        constexpr int TB = cl_tb(TOK), NTG = TOK / TB;
+        const int NP = E / 2, units = NP * NTG, RS = cl_row_slices(TOK, E);
+        const int u = tid % units, rs = tid / units;
+        const int jp = u % NP, tg = u / NP;
+        double *ext = reinterpret_cast<double *>(smem_raw + L.ext);
+        float *cmx = reinterpret_cast<float *>(smem_raw + L.ext + (((size_t)(RS - 1) * TOK * E * 8 + 15) & ~(size_t)15));
+        if (rs < RS) {
+            double acc[TB][2];
 #pragma unroll
-            for (int tt = 0; tt < TOK; ++tt) acc[tt] = 0.0;
-            float cm = 0.f;
-            // batches of RB rows, loads first: one row's load -> convert ->
-            // FMA chain is ~100 cycles of latency, so rows must overlap
-            auto rows = [&](auto rb, int i) {
-                constexpr int RB = decltype(rb)::value;
-                float gf[RB];
+            for (int tt = 0; tt < TB; ++tt) acc[tt][0] = acc[tt][1] = 0.0;
+            float cm0 = 0.f, cm1 = 0.f;
+            const int i0 = kn * rs / RS, i1 = kn * (rs + 1) / RS;
+            const GT *gp = sG + 2 * jp;
+            const double *xp = sx + TB * tg;
+            auto row = [&](int i) {
+                GT g2[2];
+                if constexpr (sizeof(GT) == 2) {
+                    const uint32_t w = *reinterpret_cast<const uint32_t *>(gp + (size_t)i * E);
+                    g2[0] = (GT)(w & 0xffffu);
+                    g2[1] = (GT)(w >> 16);
+                } else {
+                    const float2 w = *reinterpret_cast<const float2 *>(gp + (size_t)i * E);
+                    g2[0] = reinterpret_cast<const GT &>(w.x);
+                    g2[1] = reinterpret_cast<const GT &>(w.y);
+                }
+                const float f0 = WTraits<GT>::f32(g2[0]), f1 = WTraits<GT>::f32(g2[1]);
+                cm0 = fmaxf(cm0, fabsf(f0));
+                cm1 = fmaxf(cm1, fabsf(f1));
+                const double d0 = f0, d1 = f1;
+                double xv[TB];
+                if constexpr (TB == 4) {
+                    const double2 a = *reinterpret_cast<const double2 *>(xp + (size_t)i * TOK);
+                    const double2 b = *reinterpret_cast<const double2 *>(xp + (size_t)i * TOK + 2);
+                    xv[0] = a.x; xv[1] = a.y; xv[2] = b.x; xv[3] = b.y;
+                } else {
 #pragma unroll
-                for (int b = 0; b < RB; ++b) gf[b] = WTraits<GT>::f32(sG[(size_t)(i + b) * E + j]);
+                    for (int tt = 0; tt < TB; ++tt) xv[tt] = xp[(size_t)i * TOK + tt];
+                }
 #pragma unroll
-                for (int b = 0; b < RB; ++b) {
-                    const double g = gf[b];
-                    cm = fmaxf(cm, fabsf(gf[b]));
-#pragma unroll
-                    for (int tt = 0; tt < TOK; ++tt) {
-                        const int t = tg + tt * NTG;
-                        if (t < TOK) acc[tt] = fma(sx[t * kn + i + b], g, acc[tt]);  // exact product, one rounding
-                    }
+                for (int tt = 0; tt < TB; ++tt) {
+                    acc[tt][0] = fma(xv[tt], d0, acc[tt][0]);  // exact product, one rounding
+                    acc[tt][1] = fma(xv[tt], d1, acc[tt][1]);
                 }
             };
-            int i = 0;
-            for (; i + 8 <= kn; i += 8) rows(std::integral_constant<int, 8>{}, i);  // rows in order: same sums
-            for (; i < kn; ++i) rows(std::integral_constant<int, 1>{}, i);
+            int i = i0;
+            for (; i + 4 <= i1; i += 4) {
 #pragma unroll
-            for (int tt = 0; tt < TOK; ++tt) {
-                const int t = tg + tt * NTG;
-                if (t < TOK) part[t * E + j] = acc[tt];
+                for (int b = 0; b < 4; ++b) row(i + b);
             }
-            if (tg == 0) scm[j] = cm;
+            for (; i < i1; ++i) row(i);
+            double *dst = rs == 0 ? part : ext + (size_t)(rs - 1) * TOK * E;
+#pragma unroll
+            for (int tt = 0; tt < TB; ++tt) {
+                dst[(TB * tg + tt) * E + 2 * jp] = acc[tt][0];
+                dst[(TB * tg + tt) * E + 2 * jp + 1] = acc[tt][1];
+            }
+            if (tg == 0) {
+                cmx[rs * E + 2 * jp] = cm0;
+                cmx[rs * E + 2 * jp + 1] = cm1;
+            }
+        }
+        __syncthreads();
+        if (RS > 1)
+            for (int q = tid; q < TOK * E; q += kLogitThreads) {
+                double v = part[q];
+                for (int z = 1; z < RS; ++z) v += ext[(size_t)(z - 1) * TOK * E + q];
+                part[q] = v;
+            }
+        for (int j = tid; j < E; j += kLogitThreads) {
+            float m = cmx[j];
+            for (int z = 1; z < RS; ++z) m = fmaxf(m, cmx[z * E + j]);
+            scm[j] = m;
         }
     }
     if (tid == 0) probe(p.probe, cta, 2);  // partial logits in shared memory
@@ -788,6 +839,25 @@ static int launch_route_cluster(const RouteParams &p, int S, cudaStream_t s) {
             return launch_route_cluster<GT, TOK>(p, kClusterMaxS / 2, s);
         }
         attr_set[1] |= 1ull << dev;
+    }
+    // one wave: a tile that has to wait for a free cluster costs a whole
+    // launch (measured: Large-128 T=128, 32 tiles of 8 CTAs, 12 us later);
+    // halve the cluster (each CTA then owns twice the gate rows) until every
+    // tile is co-resident
+    if (S > 1) {
+        static int max_clusters[64][kClusterMaxS + 1] = {};  // per device, per S (0: not queried)
+        int &mc = max_clusters[dev][S];
+        if (mc == 0) {
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                n = 1 << 30;  // unknown: keep the form
+            }
+            mc = std::max(n, 1);
+        }
+        const int tiles = (p.T + TOK - 1) / TOK;
+        const size_t half_g = (size_t)(p.d / (S / 2)) * p.E * sizeof(GT);
+        if (tiles > mc && p.d % (S / 2) == 0 && half_g <= kClusterGBytes) return launch_route_cluster<GT, TOK>(p, S / 2, s);
     }
     PG_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
     count_launch();

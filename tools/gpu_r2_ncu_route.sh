@@ -1,6 +1,6 @@
 #!/bin/bash
+# ncu source-level capture of one K1 cluster-form launch (Large-128, T=256)
 cd "$GRAFT_REPO_ROOT"
-OUT=gpurun_out/r2ncu; mkdir -p $OUT
-for c in "large128 1" "large128 256"; do set -- $c
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:route -s 3 -c 1 -o $OUT/route_$1_T$2 python tools/route_one.py $1 $2 > $OUT/route_$1_T$2.log 2>&1
-done
+OUT=gpurun_out/r2ncu${TAG}; rm -rf $OUT; mkdir -p $OUT
+timeout -s KILL 300 ncu --section SourceCounters --section WarpStateStats --section SpeedOfLight --warp-sampling-interval 0 --clock-control none --import-source on -k regex:route_cluster -s 3 -c 1 -o $OUT/route_T256 python tools/route_one.py large128 256 > $OUT/log.txt 2>&1
+ncu -i $OUT/route_T256.ncu-rep --page source --csv --print-source cuda,sass > $OUT/source.csv 2>> $OUT/log.txt
