@@ -38,49 +38,90 @@ __global__ void unpermute_kernel(const float *__restrict__ back, const int *__re
     }
 }
 
-// Receiver routing: rows arrive grouped by source rank, each source's rows
-// grouped by local expert ascending.  Regroup by local expert (sources in
-// rank order inside an expert) — the same stable order a single GPU would
-// produce for the concatenated batch.  cnt: [P][El].  One CTA.
+// Exclusive scan of v[0, n) in place by the whole CTA (256 threads, n <= 256 * 16);
+// returns the total.  Each thread scans a contiguous chunk, chunk totals go
+// through a warp scan and a scan of the 8 warp totals.
+__device__ int block_exclusive_scan(int *v, int n, int *warp_tot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (n + 255) / 256, i0 = min(n, tid * per), i1 = min(n, i0 + per);
+    int run = 0;
+    for (int i = i0; i < i1; ++i) run += v[i];
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    int base = 0, total = 0;
+    for (int w = 0; w < 8; ++w) {
+        if (w < warp) base += warp_tot[w];
+        total += warp_tot[w];
+    }
+    int acc = base + incl - run;
+    for (int i = i0; i < i1; ++i) {
+        const int x = v[i];
+        v[i] = acc;
+        acc += x;
+    }
+    __syncthreads();
+    return total;
+}
+
+// Receiver-side routing of expert-parallel dispatch: rows arrive grouped by
+// source rank p (ascending), inside a source grouped by local expert e (the
+// sender's K1 permutation is expert-grouped), so local expert e's rows are
+// [source 0's e rows, source 1's e rows, ...] — in (source, sender position)
+// = global token order within an expert, i.e. the permutation a single GPU
+// would build for the concatenated batch.  cnt: [P][El].  One CTA of 256
+// threads; counts, offsets and the active list are parallel scans (the
+// per-source offset tables of a serial version cost ~20 us per block).
 // src_stride > 0: source p's rows start at row p * src_stride (fixed-size,
 // padded exchange) instead of right after source p-1's.
 // cnt_stride: ints between sources' count rows (El when contiguous).
-__global__ void ep_local_routing_kernel(const int *__restrict__ cnt, int cnt_stride, int P, int El, int src_stride,
-                                        pgmoe_routing r) {
+__global__ void __launch_bounds__(256) ep_local_routing_kernel(const int *__restrict__ cnt, int cnt_stride, int P,
+                                                               int El, int src_stride, pgmoe_routing r) {
     extern __shared__ int sm[];
-    int *src_base = sm;          // [P] first received row of source p
-    int *src_off = sm + P;       // [P][El] offset of expert e inside source p's rows
-    if (threadIdx.x == 0) {
-        int run = 0;
-        for (int p = 0; p < P; ++p) {
-            if (src_stride > 0) run = p * src_stride;
-            src_base[p] = run;
-            int o = 0;
-            for (int e = 0; e < El; ++e) {
-                src_off[p * El + e] = o;
-                o += cnt[p * cnt_stride + e];
-            }
-            run += o;
-        }
-        int off = 0, nact = 0;
-        for (int e = 0; e < El; ++e) {
-            int h = 0;
-            for (int p = 0; p < P; ++p) h += cnt[p * cnt_stride + e];
-            r.hist[e] = h;
-            r.off[e] = off;
-            if (h > 0) r.act[nact++] = e;
-            off += h;
-        }
-        r.off[El] = off;
+    int *src_base = sm;               // [P]     first received row of source p
+    int *src_off = sm + P;            // [P][El] offset of expert e inside source p's rows (scan of cnt)
+    int *hist = src_off + P * El;     // [El]    -> exclusive scan: off
+    int *actf = hist + El;            // [El]    active flags -> exclusive scan: position in act
+    int *wt = actf + El;              // [8]     scan scratch
+    const int tid = threadIdx.x;
+    for (int i = tid; i < P * El; i += blockDim.x) src_off[i] = __ldg(cnt + (size_t)(i / El) * cnt_stride + i % El);
+    __syncthreads();
+    for (int e = tid; e < El; e += blockDim.x) {
+        int h = 0;
+        for (int p = 0; p < P; ++p) h += src_off[p * El + e];
+        hist[e] = h;
+        actf[e] = h > 0;
+        r.hist[e] = h;
+    }
+    __syncthreads();
+    int run = 0;
+    for (int p = 0; p < P; ++p) {  // per-source exclusive scans over the experts
+        const int tot = block_exclusive_scan(src_off + p * El, El, wt);
+        if (tid == 0) src_base[p] = src_stride > 0 ? p * src_stride : run;
+        run += tot;
+    }
+    const int total = block_exclusive_scan(hist, El, wt);
+    const int nact = block_exclusive_scan(actf, El, wt);
+    for (int e = tid; e < El; e += blockDim.x) {
+        r.off[e] = hist[e];
+        if ((e + 1 < El ? hist[e + 1] : total) > hist[e]) r.act[actf[e]] = e;  // active: a non-empty range
+    }
+    if (tid == 0) {
+        r.off[El] = total;
         *r.n_act = nact;
     }
     __syncthreads();
     // perm[pos] = received row; one warp per expert
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = tid >> 5, lane = tid & 31;
     for (int e = warp; e < El; e += blockDim.x >> 5) {
-        int pos = r.off[e];
+        int pos = hist[e];
         for (int p = 0; p < P; ++p) {
-            const int c = cnt[p * cnt_stride + e];
+            const int c = __ldg(cnt + (size_t)p * cnt_stride + e);
             const int base = src_base[p] + src_off[p * El + e];
             for (int i = lane; i < c; i += 32) {
                 r.perm[pos + i] = base + i;
@@ -218,8 +259,8 @@ extern "C" int32_t pgmoe_ep_slot_rows(int32_t cap, int32_t El, int32_t d) { retu
 extern "C" int pgmoe_ep_local_routing_padded(const uint16_t *recv, int32_t P, int32_t El, int32_t cap, int32_t d,
                                              const pgmoe_routing *out, pgmoe_stream_t stream) {
     PG_REQUIRE(P >= 1 && El >= 1 && cap >= 1 && d >= 1, PGMOE_E_CONFIG, "bad EP shape P=%d El=%d cap=%d", P, El, cap);
-    const size_t smem = (size_t)(P + P * El) * 4;
-    PG_REQUIRE(smem <= 48 * 1024, PGMOE_E_CONFIG, "EP routing table too large");
+    const size_t smem = (size_t)(P + P * El + 2 * El + 8) * 4;
+    PG_REQUIRE(smem <= 48 * 1024 && El <= 256 * 16, PGMOE_E_CONFIG, "EP routing table too large");
     const int slot = cap + ep_header_rows(El, d);
     // counts of source p: the header of its slot (slot * d bf16 = slot * d / 2 ints apart)
     const int *cnt = reinterpret_cast<const int *>(recv + (size_t)cap * d);
@@ -258,8 +299,8 @@ extern "C" int pgmoe_unpermute_combine(const float *back, const int32_t *perm, c
 extern "C" int pgmoe_ep_local_routing(const int32_t *recv_cnt, int32_t P, int32_t El, const pgmoe_routing *out,
                                       pgmoe_stream_t stream) {
     PG_REQUIRE(P >= 1 && El >= 1, PGMOE_E_CONFIG, "bad EP shape P=%d El=%d", P, El);
-    const size_t smem = (size_t)(P + P * El) * 4;
-    PG_REQUIRE(smem <= 48 * 1024, PGMOE_E_CONFIG, "EP routing table too large");
+    const size_t smem = (size_t)(P + P * El + 2 * El + 8) * 4;
+    PG_REQUIRE(smem <= 48 * 1024 && El <= 256 * 16, PGMOE_E_CONFIG, "EP routing table too large");
     ep_local_routing_kernel<<<1, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(recv_cnt, El, P, El, 0, *out);
     PG_CUDA(cudaGetLastError());
     count_launch();

@@ -38,7 +38,7 @@ import torch.distributed as dist
 
 from . import _lib
 from .core import DeviceRouting, ModelConfig, _ptr, _stream
-from .errors import ConfigError, ShapeError
+from .errors import DeviceError, ConfigError, ShapeError
 
 
 def expert_range(E: int, P: int, rank: int) -> tuple[int, int]:
@@ -154,6 +154,8 @@ class EPDecoder:
         self.use_graph = os.environ.get("PGMOE_EP_GRAPH", "1") != "0"
         self._graphs: dict = {}
         self.replayed_kernels = 0  # our kernels launched by graph replays (benchmark evidence)
+        self._side = torch.cuda.Stream()  # the pre-gates (off the critical path)
+        self._rbufs: dict = {}
         # fixed-size exchange buffers (tcgen05 path): slot of cap rows per peer
         self.packed = dtype == "bf16" and kernel != "simt" and config.d_model % 128 == 0 \
             and config.d_ff % 128 == 0 and config.d_ff >= config.d_model
@@ -262,13 +264,13 @@ class EPDecoder:
             key = (x.data_ptr(), tuple(x.shape))
             entry = self._graphs.get(key)
             if entry is None:
+                # a capture failure is an error, not a silent switch to eager
+                # execution (PGMOE_EP_GRAPH=0 selects eager launches explicitly)
                 try:
                     entry = self._capture(x)
-                except Exception as e:  # noqa: BLE001 - capture unsupported: run the same work eagerly
-                    import warnings
-                    warnings.warn(f"EP graph capture failed ({e}); running eagerly")
-                    self.use_graph = False
-                    return self._iteration(x, trace)
+                except Exception as e:  # noqa: BLE001
+                    raise DeviceError(f"EP CUDA-graph capture failed: {e} (set PGMOE_EP_GRAPH=0 for eager "
+                                      "launches)") from e
                 if len(self._graphs) >= 4:
                     self._graphs.pop(next(iter(self._graphs)))
                 self._graphs[key] = entry
@@ -291,18 +293,43 @@ class EPDecoder:
             y, _ = self._iteration(x, False)
         return g, y, self._L.pgmoe_launch_count() - n0  # our kernels per replay
 
+    def _rbuf(self, T: int, slot: int) -> DeviceRouting:
+        """Routing buffers reused across blocks and iterations (a fresh
+        DeviceRouting zero-fills nine tensors: nine extra launches per block)."""
+        key = (T, slot)
+        r = self._rbufs.get(key)
+        if r is None:
+            r = self._rbufs[key] = DeviceRouting(T, self.config.num_experts, self.config.top_k)
+        return r
+
     def _iteration(self, x: torch.Tensor, trace: bool = False):
+        """The decoder loop (core.py:342-383).  Pre-gating at work: block b's
+        pre-gate reads only block b's input, so it runs on a side stream
+        concurrently with block b's exchange and expert FFN and is off the
+        critical path (the consumer waits on its event one block later)."""
         from .core import route
         c = self.config
+        main = torch.cuda.current_stream()
         pending: dict = {}
         ids = []
+        T = x.shape[0]
         for b in range(c.num_blocks):
             if c.has_conv_gate(b):
-                r_in = route(x, self.model.matrix("gate", b), c.top_k)
+                r_in = route(x, self.model.matrix("gate", b), c.top_k, out=self._rbuf(T, 2))
             else:
-                r_in = pending.pop(b)
+                r_in, done = pending.pop(b)
+                main.wait_event(done)
             if c.has_pre_gate(b):
-                pending[b + c.activation_level] = route(x, self.model.matrix("pre_gate", b), c.top_k)
+                ready = torch.cuda.Event()
+                ready.record(main)  # block b's input is written (and block b-1 is done with its routing)
+                self._side.wait_event(ready)
+                with torch.cuda.stream(self._side):
+                    r = route(x, self.model.matrix("pre_gate", b), c.top_k,
+                              out=self._rbuf(T, (b + c.activation_level) % (c.activation_level + 1)))
+                    done = torch.cuda.Event()
+                    done.record(self._side)
+                x.record_stream(self._side)
+                pending[b + c.activation_level] = (r, done)
             if trace:
                 ids.append(r_in.ids.clone())
             x = self.block(b, x, r_in)
