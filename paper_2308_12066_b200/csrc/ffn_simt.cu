@@ -171,13 +171,195 @@ gemv_grouped_kernel(GemvParams p) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tiled grouped GEMM for many tokens per expert (fp32 weights, T*k >= 64):
+// the GEMV above re-reads every weight row once per 4 tokens; here a 64-row
+// x 32-token output tile stages 64 x 32 weight and 32 x 32 token elements
+// per k-step in shared memory (transposed, so a thread's 4 rows and 2
+// tokens are vector loads) and each thread accumulates a 4 x 2 register
+// tile in K order (fp32, like the GEMV).  Units (expert, row tile, token
+// tile) are spread over a persistent grid; token tiles of an expert follow
+// its routing order (off/hist), so the epilogues (ReLU, combine weight +
+// un-permute, dense slot sum) are the GEMV's.
+constexpr int TBN = 32, TBK = 32;
+
+// BM = 64 or 32 weight rows per tile (32 when 64-row tiles would leave SMs
+// idle: the down projection has only d / 64 row tiles per expert).  The next
+// k-step's tiles are loaded into registers while the current one is
+// multiplied (one global round trip per k-step hidden behind 32 FMA rounds).
+template <typename WT, int BM>
+__global__ void __launch_bounds__(256) sgemm_grouped_kernel(GemvParams p) {
+    constexpr int RM = BM / 16;            // rows per thread (16 thread rows)
+    constexpr int WL = BM * TBK / 4 / 256;  // weight float4 loads per thread per k-step (2 or 1)
+    __shared__ __align__(16) float As[TBK][BM + 4];
+    __shared__ __align__(16) float Bs[TBK][TBN + 4];
+    __shared__ int tile0[1025];  // prefix of tiles per expert group
+    __shared__ int wtot[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int groups = (p.mode == kDense) ? 1 : *p.n_act;
+    const int mtiles = (p.M + BM - 1) / BM;
+    {   // tiles per group (4 groups per thread, loaded in parallel), exclusive scan
+        int cnt[4], run = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int g = 4 * tid + q;
+            const int ntok = g < groups ? (p.mode == kDense ? p.T : __ldg(p.hist + __ldg(p.act + g))) : 0;
+            cnt[q] = mtiles * ((ntok + TBN - 1) / TBN);
+            run += cnt[q];
+        }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wtot[warp] = incl;
+        __syncthreads();
+        int base = 0;
+        for (int w = 0; w < warp; ++w) base += wtot[w];
+        int acc = base + incl - run;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int g = 4 * tid + q;
+            if (g <= groups) tile0[g] = acc;
+            acc += cnt[q];
+        }
+    }
+    __syncthreads();
+    const int total = tile0[groups];
+    const int tx = tid % 16, ty = tid / 16;  // thread tile: rows RM ty .. +RM-1, tokens 2 tx .. +1
+    for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        int lo = 0, hi = groups - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (tile0[mid] <= u) lo = mid;
+            else hi = mid - 1;
+        }
+        const int g = lo, l = u - tile0[g];
+        const int nt = l / mtiles, mt = l - nt * mtiles;
+        int e = 0, tok0 = 0, ntok = p.T;
+        const unsigned char *rec = p.W + p.w_offset;
+        if (p.mode != kDense) {
+            e = p.act[g];
+            tok0 = p.off[e];
+            ntok = p.hist[e];
+            rec += (size_t)(p.indexed_by_act ? g : e) * p.expert_stride;
+        }
+        const WT *Wm = reinterpret_cast<const WT *>(rec);
+        const int m0 = mt * BM, n0 = nt * TBN;
+        float acc[RM][2];
+#pragma unroll
+        for (int r = 0; r < RM; ++r) acc[r][0] = acc[r][1] = 0.f;
+        // loaders: weights BM rows x 32 k (WL float4 per thread), tokens 32 x 32 (1 float4)
+        const int bn = tid / 8, bk = (tid % 8) * 4;
+        const int col = n0 + bn;
+        const float *srow[8];
+        int ns = 0;
+        if (col < ntok) {
+            if (p.mode == kUp) {
+                srow[0] = p.src + (size_t)(p.perm[tok0 + col] / p.k) * p.K;
+                ns = 1;
+            } else if (p.mode == kDown) {
+                srow[0] = p.src + (size_t)(tok0 + col) * p.K;
+                ns = 1;
+            } else {
+                for (int q = 0; q < p.k && q < 8; ++q) srow[q] = p.src + ((size_t)col * p.k + q) * p.K;
+                ns = p.k < 8 ? p.k : 8;
+            }
+        }
+        float4 wv[WL], xv;
+        auto fetch = [&](int k0) {
+#pragma unroll
+            for (int h = 0; h < WL; ++h) {
+                const int idx = tid + h * 256, wr = idx / 8, wk = (idx % 8) * 4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (m0 + wr < p.M) {
+                    if constexpr (sizeof(WT) == 4) {
+                        v = __ldg(reinterpret_cast<const float4 *>(Wm + (size_t)(m0 + wr) * p.K + k0 + wk));
+                    } else {
+                        const uint2 b2 = __ldg(reinterpret_cast<const uint2 *>(Wm + (size_t)(m0 + wr) * p.K + k0 + wk));
+                        v = make_float4(__uint_as_float(b2.x << 16), __uint_as_float(b2.x & 0xffff0000u),
+                                        __uint_as_float(b2.y << 16), __uint_as_float(b2.y & 0xffff0000u));
+                    }
+                }
+                wv[h] = v;
+            }
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < ns; ++q) {  // kDense: the k slot rows summed in routing order
+                const float4 a4 = __ldg(reinterpret_cast<const float4 *>(srow[q] + k0 + bk));
+                v.x += a4.x; v.y += a4.y; v.z += a4.z; v.w += a4.w;
+            }
+            xv = v;
+        };
+        fetch(0);
+        for (int k0 = 0; k0 < p.K; k0 += TBK) {
+#pragma unroll
+            for (int h = 0; h < WL; ++h) {
+                const int idx = tid + h * 256, wr = idx / 8, wk = (idx % 8) * 4;
+                As[wk][wr] = wv[h].x;
+                As[wk + 1][wr] = wv[h].y;
+                As[wk + 2][wr] = wv[h].z;
+                As[wk + 3][wr] = wv[h].w;
+            }
+            Bs[bk][bn] = xv.x;
+            Bs[bk + 1][bn] = xv.y;
+            Bs[bk + 2][bn] = xv.z;
+            Bs[bk + 3][bn] = xv.w;
+            __syncthreads();
+            if (k0 + TBK < p.K) fetch(k0 + TBK);  // in flight while this step multiplies
+#pragma unroll 8
+            for (int kk = 0; kk < TBK; ++kk) {
+                float av[RM];
+                if constexpr (RM == 4) {
+                    const float4 a4 = *reinterpret_cast<const float4 *>(&As[kk][4 * ty]);
+                    av[0] = a4.x; av[1] = a4.y; av[2] = a4.z; av[3] = a4.w;
+                } else {
+                    const float2 a2 = *reinterpret_cast<const float2 *>(&As[kk][RM * ty]);
+                    av[0] = a2.x; av[1] = a2.y;
+                }
+                const float2 b = *reinterpret_cast<const float2 *>(&Bs[kk][2 * tx]);
+#pragma unroll
+                for (int r = 0; r < RM; ++r) {
+                    acc[r][0] = fmaf(av[r], b.x, acc[r][0]);
+                    acc[r][1] = fmaf(av[r], b.y, acc[r][1]);
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int r = 0; r < RM; ++r)
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) {
+                const int m = m0 + RM * ty + r, cc = n0 + 2 * tx + c2;
+                if (m >= p.M || cc >= ntok) continue;
+                const float v = acc[r][c2];
+                if (p.mode == kUp) {
+                    p.dst[(size_t)(tok0 + cc) * p.M + m] = v > 0.f ? v : 0.f;  // relu, linalg.py:41-42
+                } else if (p.mode == kDown) {
+                    const int rr = tok0 + cc;
+                    p.dst[(size_t)p.perm[rr] * p.M + m] = p.w_perm[rr] * v;  // combine weight
+                } else {
+                    p.dst[(size_t)cc * p.M + m] = v;
+                }
+            }
+    }
+}
+
 template <typename WT>
 static int launch_gemv(const GemvParams &p, cudaStream_t s) {
     const bool vec = (p.K % 8 == 0) && (p.w_offset % 16 == 0) && (p.expert_stride % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(p.W) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(p.src) % 16 == 0);
     const int grid = kNumSMs * 4;
-    if (vec) gemv_grouped_kernel<WT, true><<<grid, 256, 0, s>>>(p);
+    // many tokens per launch: the tiled kernel reads each weight tile once per
+    // 32 tokens instead of once per 4 (fp32: 236 GB/s -> see DESIGN §5)
+    const bool tiled = vec && p.K % TBK == 0 && (long long)p.T * (p.mode == kDense ? 1 : p.k) >= 64 &&
+                       (p.mode == kDense || p.expert_stride % 16 == 0);
+    // 32-row tiles when 64-row tiles would not give every SM two units (estimate: T*k tokens spread
+    // over min(T*k, E) groups is unknown here; the row count decides)
+    if (tiled && p.M / 64 * 8 < 2 * kNumSMs) sgemm_grouped_kernel<WT, 32><<<grid, 256, 0, s>>>(p);
+    else if (tiled) sgemm_grouped_kernel<WT, 64><<<grid, 256, 0, s>>>(p);
+    else if (vec) gemv_grouped_kernel<WT, true><<<grid, 256, 0, s>>>(p);
     else gemv_grouped_kernel<WT, false><<<grid, 256, 0, s>>>(p);
     PG_CUDA(cudaGetLastError());
     count_launch();
