@@ -591,7 +591,8 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, co
     // (~E·d·f weight bytes): measured crossover T ≈ f/8 (Base-64 fused
     // better through T=384, separate at 512; Large-128 fused through 768,
     // even at 1024; tools/gpu_env_sweep.sh VAR=PGMOE_FUSE_MAX_T).
-    const bool fuse_route = !off && !io.ids_supplied && use_tc(m) && c.top_k == 1 && L == 1 && m->fuse_route &&
+    // (any lookahead L >= 1: block b's launch routes block b+L into ring entry (b+L) % (L+1))
+    const bool fuse_route = !off && !io.ids_supplied && use_tc(m) && c.top_k == 1 && L >= 1 && m->fuse_route &&
                             fused_route_supported(c.num_experts) &&
                             (long long)T <= (m->fuse_max_t > 0 ? m->fuse_max_t : c.d_ff / 8);
     if (m->ll_decode && m->ll_ws && !off && !io.ids_supplied && use_tc(m) && m->fuse_route && T <= m->ll_max_t &&

@@ -321,6 +321,38 @@ def test_offloaded_equals_resident_and_ledger(dtype):
     off.close()
 
 
+@pytest.mark.parametrize("L", [2, 3])
+def test_fused_routing_with_deeper_lookahead(L):
+    """Lookahead L >= 2 (core.py:73-89: block b's pre-gate decides block b+L):
+    the routing computed inside block b's launch goes to ring entry (b+L) %
+    (L+1) while the dense epilogue packs block b+1's operand from the entry
+    an earlier launch filled.  Outputs and decisions equal the separate-K1
+    schedule and the offloaded one bitwise, and the teacher-forced oracle."""
+    dims = og.Dims(256, 2048, 6, 64, 1, activation_level=L, seed=11)
+    T = 24
+    xn = tokens(256, T, seed=L)
+    x0 = torch.from_numpy(xn).cuda()
+    fused = _device_model(dims, "bf16", "resident", max_tokens=T)
+    sep = _device_model(dims, "bf16", "resident", max_tokens=T)
+    sep.set_fused_route(False)
+    off = _device_model(dims, "bf16", "offloaded", max_tokens=T)
+    outs = []
+    for m in (fused, sep, off):
+        m.reset_stats()
+        for _ in range(2):
+            y, ids, w = m.decoder_iteration(x0, trace=True)
+        torch.cuda.synchronize()
+        outs.append((y.clone(), ids.clone(), w.clone()))
+    assert fused.stats()["fused_routes"] > 0 and sep.stats()["fused_routes"] == 0
+    for y, ids, w in outs[1:]:
+        assert torch.equal(outs[0][1], ids) and torch.equal(outs[0][2], w)
+        assert torch.equal(outs[0][0], y)
+    om = og.OracleModel(dims, "bf16")
+    _teacher_forced_chain(fused, om, xn, TOL["bf16"])
+    for m in (fused, sep, off):
+        m.close()
+
+
 @pytest.mark.parametrize("E,T", [(64, 1), (64, 10), (64, 40), (128, 33), (128, 256), (256, 17)])
 def test_fused_routing_equals_separate_launch_and_offloaded(E, T):
     """Resident top-1 decoding computes each pre-gate inside the block's
