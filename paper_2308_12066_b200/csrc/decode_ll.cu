@@ -829,7 +829,22 @@ int ll_decode_iteration(const LLDecodeArgs &a, cudaStream_t s) {
     p.ids_trace = a.ids_trace;
     p.w_trace = a.w_trace;
     p.probe = probe_buffer(1, G);
-    PG_CUDA(launch_pdl(ll_decode_kernel, dim3(G), dim3(kThreads), smem, s, p));
+    // Cooperative: every CTA polls words other CTAs write, so the launch must
+    // be all-or-nothing co-resident (another persistent kernel on a second
+    // stream must not hold part of the SMs while this one spins on the rest).
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    PG_CUDA(cudaLaunchKernelEx(&cfg, ll_decode_kernel, p));
     count_launch();
     return PGMOE_OK;
 }

@@ -138,3 +138,31 @@ def test_ll_decode_serial_fallback_on_planted_tie():
     assert m.stats()["route_fallbacks"] > 0, "the tie must take the serial recompute"
     m.check_routing()
     m.close()
+
+
+def test_ll_decode_gate_overflow_surfaces_as_reference_error():
+    """A non-finite pre-gate logit inside the launch (core.py:297): the
+    reducer flags it on the routing buffer and check_routing raises the
+    reference's GateOverflowError with its message; the next clean launch
+    runs normally."""
+    from paper_2308_12066_b200 import errors
+    dims = og.Dims(256, 512, 3, 64, 1, seed=6)
+    m = _model(dims, 2)
+    x = torch.from_numpy(_tokens(256, 2, seed=3)).cuda()
+    m.decoder_iteration(x)
+    torch.cuda.synchronize()
+    m.check_routing()
+    g = m.get_matrix("pre_gate", 1)
+    g_bad = g.copy()
+    g_bad[:, 5] = 0x7F80  # +inf (bf16)
+    m.set_matrix("pre_gate", 1, -1, g_bad)
+    m.decoder_iteration(x)  # a graph replay of the LL launch (counted once, at capture)
+    torch.cuda.synchronize()
+    assert m.ll_decode_iterations >= 1
+    with pytest.raises(errors.GateOverflowError, match="numerical overflow in gate"):
+        m.check_routing()
+    m.set_matrix("pre_gate", 1, -1, g)
+    m.decoder_iteration(x)
+    torch.cuda.synchronize()
+    m.check_routing()
+    m.close()
