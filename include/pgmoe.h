@@ -292,6 +292,11 @@ PGMOE_API int64_t pgmoe_model_decode_iterations(pgmoe_model *m);
  * T <= max_tokens.  Same contract as decoder_iteration (core.py:342-383). */
 PGMOE_API int pgmoe_model_set_ll_decode(pgmoe_model *m, int32_t enabled, int32_t max_tokens);
 PGMOE_API int64_t pgmoe_model_ll_decode_iterations(pgmoe_model *m);
+/* Device %globaltimer stamps (ns) of the last resident decoder iteration that
+ * ran chained block launches: out[b+1] = when block b's dense layer completed
+ * (out[0] unused).  Consecutive differences are the reference's block
+ * latencies (scheduler.py:374-397), measured on graph-replayed iterations. */
+PGMOE_API int pgmoe_model_block_stamps(pgmoe_model *m, int64_t *out, int32_t n);
 
 /* decoder_iteration (core.py:342-383) for T tokens, device buffers.
  * x_in / y_out: fp32 [T][d] device.  ids_trace / w_trace (optional, device):

@@ -76,7 +76,7 @@ EXPORTS = (
     "pgmoe_ep_unpermute_padded", "pgmoe_ep_slot_rows", "pgmoe_route_from_decisions", "pgmoe_decoder_iteration_ex",
     "pgmoe_model_check_routing", "pgmoe_gate_forward_f64", "pgmoe_debug_green_context",
     "pgmoe_model_set_decode", "pgmoe_model_decode_iterations",
-    "pgmoe_model_set_ll_decode", "pgmoe_model_ll_decode_iterations",
+    "pgmoe_model_set_ll_decode", "pgmoe_model_ll_decode_iterations", "pgmoe_model_block_stamps",
 )
 
 _lib = None
@@ -142,6 +142,7 @@ def load():
         "pgmoe_model_decode_iterations": (i64, [vp]),
         "pgmoe_model_set_ll_decode": (i32, [vp, i32, i32]),
         "pgmoe_model_ll_decode_iterations": (i64, [vp]),
+        "pgmoe_model_block_stamps": (i32, [vp, vp, i32]),
         "pgmoe_ep_pack_send": (i32, [vp, P(Routing), i32, i32, i32, i32, i32, i32, vp, vp]),
         "pgmoe_ep_local_routing_padded": (i32, [vp, i32, i32, i32, i32, P(Routing), vp]),
         "pgmoe_ep_slot_rows": (i32, [i32, i32, i32]),

@@ -97,6 +97,7 @@ struct Params {
     // parity buffers, so a launch never touches what its predecessor re-arms.
     int *epoch;                 // null: not chained
     int epoch_wait, epoch_set;
+    unsigned long long *stamps;  // chained: stamps[epoch_set] = %globaltimer at dense-phase completion
 };
 
 struct PhaseSched {
@@ -719,6 +720,10 @@ block_gemm_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant_
                         __threadfence();
                         asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.epoch), "r"(p.epoch_set)
                                      : "memory");
+                        // the reference's block latency is the time between consecutive
+                        // blocks' dense-layer ends (scheduler.py:374-397): stamp it on the
+                        // device, so graph-replayed timed iterations report it unperturbed
+                        if (p.stamps) p.stamps[p.epoch_set] = gtimer();
                     }
                 }
             }
@@ -1020,6 +1025,7 @@ int block_tc(const float *x, int T, int d, int f, int k, const void *experts, si
         p.epoch = chain->epoch;
         p.epoch_wait = chain->epoch_wait;
         p.epoch_set = chain->epoch_set;
+        p.stamps = chain->stamps;
         parity = chain->parity & 1;
     }
     // N tile: 64 tokens (8 weight stages) while the average expert holds at

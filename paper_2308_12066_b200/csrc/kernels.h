@@ -37,6 +37,7 @@ struct LaunchChain {
     int epoch_wait;   // > 0: wait for *epoch >= epoch_wait; 0: for the previous launch to complete (PDL)
     int epoch_set;
     int parity;       // alternates between consecutive block launches
+    unsigned long long *stamps;  // [epoch_set] %globaltimer when the launch's dense phase completes (or null)
 };
 int block_tc(const float *x, int T, int d, int f, int k, const void *experts, size_t stride, int indexed_by_act,
              const pgmoe_routing *r, uint16_t *xb, uint16_t *hb, float *yw, uint16_t *mixb, bool xb_ready,

@@ -649,7 +649,8 @@ int decoder_iteration(pgmoe_model *m, const float *x_in, int T, float *y_out, co
         const bool fuse_next = use_tc(m) && b + 1 < nb && !has_conv_gate(c, b + 1);
         const pgmoe_routing *next_r = fuse_next ? &m->routing[(b + 1) % R].r : nullptr;
         const int indexed = (off && !prefetch_all) ? 1 : 0;
-        LaunchChain lc{m->epoch, b > 0 ? b : 0, b + 1, b & 1};
+        LaunchChain lc{m->epoch, b > 0 ? b : 0, b + 1, b & 1,
+                       reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(m->epoch) + 256)};
         if (use_tc(m) && c.top_k == 1) {
             // one launch: up, down(+combine), dense — phases behind grid barriers
             tl_begin(m, "compute", "experts", b, s);
@@ -927,7 +928,8 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
     m->tc_ws_bytes = 64ull << 20;
     if (cudaMalloc(&m->tc_ws, m->tc_ws_bytes) != cudaSuccess || cudaMemset(m->tc_ws, 0, m->tc_ws_bytes) != cudaSuccess)
         return fail(PGMOE_E_OOM);
-    if (cudaMalloc(&m->epoch, 256) != cudaSuccess || cudaMemset(m->epoch, 0, 256) != cudaSuccess)
+    // [0] launch-chain epoch; bytes 256..: dense-end stamps per block (pgmoe_model_block_stamps)
+    if (cudaMalloc(&m->epoch, 1024) != cudaSuccess || cudaMemset(m->epoch, 0, 1024) != cudaSuccess)
         return fail(PGMOE_E_OOM);
     if (const char *e = getenv("PGMOE_CHAIN")) m->chain_launches = (e[0] != '0');
     if (const char *e = getenv("PGMOE_FUSED_ROUTE")) m->fuse_route = (e[0] == '1');
@@ -1155,6 +1157,14 @@ extern "C" int pgmoe_model_set_ll_decode(pgmoe_model *m, int32_t enabled, int32_
 }
 
 extern "C" int64_t pgmoe_model_ll_decode_iterations(pgmoe_model *m) { return m ? m->ll_iters : 0; }
+
+extern "C" int pgmoe_model_block_stamps(pgmoe_model *m, int64_t *out, int32_t n) {
+    PG_REQUIRE(m != nullptr && out != nullptr, PGMOE_E_CONFIG, "null argument");
+    PG_REQUIRE(n >= 0 && n <= 96, PGMOE_E_CONFIG, "at most 96 stamps");
+    PG_CUDA(cudaDeviceSynchronize());
+    PG_CUDA(cudaMemcpy(out, reinterpret_cast<char *>(m->epoch) + 256, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    return PGMOE_OK;
+}
 
 extern "C" int pgmoe_model_init_weights(pgmoe_model *m) {
     const auto &c = m->cfg;

@@ -234,3 +234,31 @@ def test_persistent_kernel_on_fewer_sms(tmp_path, mode):
     assert np.array_equal(np.load(str(ref) + ".ids.npy"), np.load(str(out) + ".ids.npy"))
     a, b = np.load(ref), np.load(out)
     assert np.max(np.abs(a - b)) <= BF16_TOL * np.max(np.abs(a))
+
+
+def test_block_end_stamps_of_chained_launches():
+    """Chained resident block launches stamp when each block's dense layer
+    completes (pgmoe_model_block_stamps); the bench derives the reference's
+    block latency (scheduler.py:374-397) from them on graph-replayed
+    iterations.  Stamps are per block, increasing, and span less than the
+    event-timed iteration."""
+    import ctypes
+    p = P()
+    from paper_2308_12066_b200 import _lib
+    cfg = p.ModelConfig(d_model=256, d_ff=2048, num_blocks=5, num_experts=64, top_k=1, activation_level=1)
+    m = p.DeviceModel(cfg, dtype="bf16", placement="resident", max_tokens=24)
+    x = p.token_inputs(cfg, 24)
+    y = torch.empty_like(x)
+    for _ in range(3):  # eager, capture, replay
+        m.decoder_iteration(x, out=y)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    m.decoder_iteration(x, out=y)
+    b.record()
+    torch.cuda.synchronize()
+    st = np.zeros(cfg.num_blocks + 1, dtype=np.int64)
+    _lib.check(_lib.load().pgmoe_model_block_stamps(m._h, ctypes.c_void_p(st.ctypes.data), cfg.num_blocks + 1))
+    d = np.diff(st[1:])
+    assert (st[1:] > 0).all() and (d > 0).all(), st
+    assert (st[-1] - st[1]) / 1e6 < a.elapsed_time(b)
+    m.close()
