@@ -1,5 +1,5 @@
 # per-block latency (bench clock, graph replay) vs one knob:
-#   VAR=PGMOE_INFLIGHT VALS="6 8" bash tools/gpu_env_sweep.sh
+#   VAR=PGMOE_INFLIGHT VALS="6 8" bash tools/gpu/gpu_env_sweep.sh
 OUT=gpurun_out/envsw; rm -rf $OUT; mkdir -p $OUT
 B64=${B64:-1,8,64,128,256}; L128=${L128:-1,64,256}
 for v in $VALS; do

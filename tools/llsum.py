@@ -1,4 +1,4 @@
-"""Summarise a tools/gpu_r2_ll.sh output directory."""
+"""Summarise a tools/gpu/gpu_r2_ll.sh output directory."""
 import glob
 import json
 import sys

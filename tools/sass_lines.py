@@ -1,4 +1,4 @@
-"""Aggregate ncu per-SASS warp samples (tools/gpu_ncu_source.sh) by CUDA
+"""Aggregate ncu per-SASS warp samples (tools/gpu/gpu_ncu_source.sh) by CUDA
 source line, using nvdisasm --print-line-info of the same build.
 
   python tools/sass_lines.py SASS_CSV KERNEL_SYMBOL [--file route_common] [--top 40]
