@@ -48,7 +48,7 @@ constexpr int kThreads = 384;
 constexpr int kCW0 = 2, kCWarps = 8, kCThreads = kCWarps * 32;  // compute warps
 constexpr int kRW0 = 10, kRThreads = 64;                        // reducer warps
 constexpr int kMaxSlots = 6;  // weight-slice ring: as many slots as shared memory allows (>= 3)
-constexpr int kSlotBytes = 33792;
+constexpr int kSlotBytes = 33792;  // the smallest ring slot (one row of K = 4096 needs 8208 B)
 constexpr int kDRows = 16;  // dense rows per dense CTA
 constexpr int kMaxE = 128;
 
@@ -60,7 +60,7 @@ struct Piece {
 
 struct Params {
     int T, d, f, E, nb, nd;           // nd: dense CTAs (d / kDRows)
-    int nslots;                       // weight-slice ring slots
+    int nslots, slot_bytes;           // weight-slice ring: slots x bytes (pick_ring)
     const DecodeBlock *blocks;
     const unsigned char *experts;     // records [nb][E]: W1 [f][d] then W2 [d][f]
     size_t rec_bytes;
@@ -313,8 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
     const int dpitch = d * 2 + 16;
     // ---- shared memory layout ------------------------------------------
     const int kSlots = p.nslots;
-    unsigned char *slots = smem_raw;                                    // kSlots x kSlotBytes
-    unsigned char *dbuf = slots + (size_t)kSlots * kSlotBytes;          // kDRows x dpitch
+    const int kSlotB = p.slot_bytes;
+    unsigned char *slots = smem_raw;                                    // kSlots x kSlotB
+    unsigned char *dbuf = slots + (size_t)kSlots * kSlotB;              // kDRows x dpitch
     uint16_t *gsl = reinterpret_cast<uint16_t *>(dbuf + kDRows * dpitch);  // kDRows x E pre-gate rows
     uint16_t *gsl0 = gsl + kDRows * E;                                     // block 0's gate rows (fill 0)
     unsigned char *act = reinterpret_cast<unsigned char *>(gsl0 + kDRows * E);  // T x (max(d,f) * 2 + 16)
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
             const unsigned char *recs = p.experts + (size_t)b * E * p.rec_bytes;
             for (int ph = 0; ph < 2; ++ph) {
                 const int R = ph == 0 ? f : d, K = ph == 0 ? d : f;
-                const int pitch = K * 2 + 16, prow = min(kSlotBytes / pitch, 32);
+                const int pitch = K * 2 + 16, prow = min(kSlotB / pitch, 32);
                 const long long N = (long long)na * R;
                 const long long lo = N * c / G, hi = N * (c + 1) / G;
                 long long r = lo;
@@ -462,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                         const unsigned char *src = recs + (size_t)e * p.rec_bytes +
                                                    (ph == 0 ? (size_t)rr * d * 2 : (size_t)f * d * 2 + (size_t)rr * f * 2);
                         for (int i = lane; i < n; i += 32)
-                            bulk_g2s(slots + (size_t)slot * kSlotBytes + i * pitch, src + (size_t)i * K * 2, K * 2,
+                            bulk_g2s(slots + (size_t)slot * kSlotB + i * pitch, src + (size_t)i * K * 2, K * 2,
                                      &full[slot], pol);
                     } else if (lane == 0) {  // no rows of this phase here: an empty marker piece
                         pd.b = b;
@@ -666,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                         if (first && ct == 0) dprobe(p, b, ph == 0 ? 1 : 3);
                         first = false;
                     }
-                    piece_gemv(slots + (size_t)slot * kSlotBytes, K * 2 + 16, nrows, act, K * 2 + 16, ng, K, red, ct,
+                    piece_gemv(slots + (size_t)slot * kSlotB, K * 2 + 16, nrows, act, K * 2 + 16, ng, K, red, ct,
                                out, orow, otok);
                     if (orow >= 0 && orow < nrows && otok < ng) {
                         const int t = my_t;
@@ -730,17 +731,37 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
 // Shared memory of a launch: the weight ring (nslots), the dense slice, the
 // staged activations of T tokens (mma B rows past T are never read: columns
 // repeat the last staged token) and small per-role buffers.
-size_t smem_bytes(int T, int d, int f, int E, int nslots) {
-    return (size_t)nslots * kSlotBytes + (size_t)kDRows * (d * 2 + 16) + (size_t)2 * kDRows * E * 2 +
+size_t smem_bytes(int T, int d, int f, int E, int nslots, int slot_bytes = kSlotBytes) {
+    return (size_t)nslots * slot_bytes + (size_t)kDRows * (d * 2 + 16) + (size_t)2 * kDRows * E * 2 +
            (size_t)((T + 1) & ~1) * (f * 2 + 16) + (size_t)kCWarps * 128 * 4 + kDRows * 8 * 4 + (size_t)d * 4 +
            (kRThreads + kMaxE) * 8 + kMaxE * 4 + (2 * kRThreads + 1) * 8 + nslots * sizeof(Piece) + 16 +
            (2 * nslots + 2) * 8 + 2 * kLLMaxT * 4 + 64;
 }
 constexpr size_t kSmemCap = 226 * 1024;
-int pick_slots(int T, int d, int f, int E) {
-    int n = kMaxSlots;
-    while (n > 3 && smem_bytes(T, d, f, E, n) > kSmemCap) --n;
-    return n;
+// The ring: bigger slots mean fewer, larger pieces (each piece pays a fixed
+// K-split reduction, two barriers and an epilogue).  Rule: the largest slot
+// (65, 48, 33 KB) that still leaves at least 2 slots.  Measured (A/B of
+// PGMOE_LL_SLOT_KB on one box, us per block, 33 KB -> chosen): Base-64
+// T=1 10.6 -> 9.4, T=2 13.3 -> 11.8, T=4 18.6 -> 15.7, T=8 32.5 -> 28.3;
+// Large-128 T=1 11.8 -> 10.1, T=2 16.9 -> 13.2, T=4 25.4 -> 20.6, T=8
+// 51.9 -> 47.6 (48 KB: 64 KB slots do not fit twice there).
+void pick_ring(int T, int d, int f, int E, int *nslots, int *slot_bytes) {
+    static const int sizes[3] = {65536 + 1024, 49152, kSlotBytes};
+    int force = 0;
+    if (const char *e = getenv("PGMOE_LL_SLOT_KB")) force = atoi(e) * 1024;
+    for (int i = 0; i < 3; ++i) {
+        int sb = sizes[i];
+        if (force && sb != (force >= 60 * 1024 ? sizes[0] : force >= 40 * 1024 ? sizes[1] : sizes[2])) continue;
+        int n = kMaxSlots;
+        while (n > 2 && smem_bytes(T, d, f, E, n, sb) > kSmemCap) --n;
+        if (smem_bytes(T, d, f, E, n, sb) <= kSmemCap) {
+            *nslots = n;
+            *slot_bytes = sb;
+            return;
+        }
+    }
+    *nslots = 3;
+    *slot_bytes = kSlotBytes;
 }
 
 }  // namespace ll
@@ -778,8 +799,9 @@ int ll_decode_prepare(void *ws, cudaStream_t s) {
 
 int ll_decode_iteration(const LLDecodeArgs &a, cudaStream_t s) {
     using namespace ll;
-    const int nslots = pick_slots(a.T, a.d, a.f, a.E);
-    const size_t smem = smem_bytes(a.T, a.d, a.f, a.E, nslots);
+    int nslots = 3, slot_bytes = kSlotBytes;
+    pick_ring(a.T, a.d, a.f, a.E, &nslots, &slot_bytes);
+    const size_t smem = smem_bytes(a.T, a.d, a.f, a.E, nslots, slot_bytes);
     static size_t attr_smem[64] = {0};  // per device: dynamic shared memory the attribute allows
     static int grid_dev[64] = {0};
     const int dev = current_device();
@@ -805,6 +827,7 @@ int ll_decode_iteration(const LLDecodeArgs &a, cudaStream_t s) {
     p.nb = a.nb;
     p.nd = nd;
     p.nslots = nslots;
+    p.slot_bytes = slot_bytes;
     p.blocks = a.blocks;
     p.experts = static_cast<const unsigned char *>(a.experts);
     p.rec_bytes = a.rec_bytes;
