@@ -166,6 +166,14 @@ PGMOE_API int pgmoe_expert_forward_packed(const uint16_t *xb, int32_t n_max, int
                                           uint16_t *hb, float *y, pgmoe_stream_t stream);
 PGMOE_API int pgmoe_ep_unpermute_padded(const float *back, const pgmoe_routing *r, int32_t T, int32_t d, int32_t k,
                                         int32_t P, int32_t El, int32_t cap, float *yw, pgmoe_stream_t stream);
+/* Top-1: the combine weight applied and the result written as the dense
+ * layer's bf16 operand mixb [T][d] (linalg.py:45-51 for k = 1), consumed by
+ * pgmoe_dense_forward_packed (core.py:338) — one launch fewer per EP block. */
+PGMOE_API int pgmoe_ep_unpermute_padded_bf16(const float *back, const pgmoe_routing *r, int32_t T, int32_t d,
+                                             int32_t P, int32_t El, int32_t cap, uint16_t *mixb,
+                                             pgmoe_stream_t stream);
+PGMOE_API int pgmoe_dense_forward_packed(const uint16_t *mixb, int32_t T, int32_t d, const void *dense_w, float *y,
+                                         pgmoe_stream_t stream);
 
 /* Reads routing status after a sync: returns the device-detected error (or
  * PGMOE_OK) and optionally the serial-fallback counter.  (Flips against the

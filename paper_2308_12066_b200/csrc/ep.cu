@@ -212,6 +212,27 @@ __global__ void ep_unpermute_padded_kernel(const float *__restrict__ back, const
     }
 }
 
+// Top-1 combine straight into the dense layer's bf16 operand: mixb[t] =
+// bf16(w * y) — the same product and rounding the fused single-GPU down
+// epilogue writes (so EP == one GPU bitwise), one launch fewer per block.
+__global__ void ep_unpermute_padded_bf16_kernel(const float *__restrict__ back, const int *__restrict__ perm,
+                                                const float *__restrict__ w_perm, const int *__restrict__ off, int n,
+                                                int d, int P, int El, int slot, uint16_t *__restrict__ mixb) {
+    const int vec = d / 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * vec;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / vec), c = (int)(i - (long long)r * vec);
+        const int p = owner_of(off, El, P, r);
+        const size_t row = (size_t)p * slot + (r - __ldg(off + p * El));
+        const float w = __ldg(w_perm + r);
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(back) + row * vec + c);
+        uint2 o;
+        o.x = pack_bf16x2(w * v.x, w * v.y);
+        o.y = pack_bf16x2(w * v.z, w * v.w);
+        reinterpret_cast<uint2 *>(mixb)[(size_t)__ldg(perm + r) * vec + c] = o;
+    }
+}
+
 static int grid_for(long long work) { return (int)std::min<long long>(kNumSMs * 8, std::max(1LL, (work + 255) / 256)); }
 
 }  // namespace pgmoe
@@ -249,6 +270,19 @@ extern "C" int pgmoe_ep_unpermute_padded(const float *back, const pgmoe_routing 
     if (n == 0) return PGMOE_OK;
     ep_unpermute_padded_kernel<<<grid_for((long long)n * d / 4), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
         back, r->perm, r->w_perm, r->off, n, d, P, El, cap + ep_header_rows(El, d), yw);
+    PG_CUDA(cudaGetLastError());
+    count_launch();
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_ep_unpermute_padded_bf16(const float *back, const pgmoe_routing *r, int32_t T, int32_t d,
+                                              int32_t P, int32_t El, int32_t cap, uint16_t *mixb,
+                                              pgmoe_stream_t stream) {
+    PG_REQUIRE(d % 4 == 0, PGMOE_E_SHAPE, "ep_unpermute needs d %% 4 == 0");
+    if (T == 0) return PGMOE_OK;
+    ep_unpermute_padded_bf16_kernel<<<grid_for((long long)T * d / 4), 256, 0,
+                                      reinterpret_cast<cudaStream_t>(stream)>>>(
+        back, r->perm, r->w_perm, r->off, T, d, P, El, cap + ep_header_rows(El, d), mixb);
     PG_CUDA(cudaGetLastError());
     count_launch();
     return PGMOE_OK;

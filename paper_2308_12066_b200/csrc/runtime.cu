@@ -819,6 +819,16 @@ extern "C" int pgmoe_dense_forward(const float *yw, int32_t T, int32_t d, int32_
     return dense_simt(yw, T, d, k, dense_w, wdtype, y, s);
 }
 
+extern "C" int pgmoe_dense_forward_packed(const uint16_t *mixb, int32_t T, int32_t d, const void *dense_w,
+                                          float *y, pgmoe_stream_t stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (T == 0) return PGMOE_OK;
+    PG_REQUIRE(d % 128 == 0, PGMOE_E_CONFIG, "tcgen05 dense needs d multiple of 128");
+    void *ws = nullptr;
+    PG_TRY(shared_tc_ws(2, &ws));
+    return dense_tc2(nullptr, mixb, T, d, 1, dense_w, y, nullptr, ws, kSharedWsBytes, s, nullptr, nullptr);
+}
+
 extern "C" int pgmoe_model_create(const pgmoe_config *cfg, int32_t wdtype, int32_t placement,
                                   int32_t max_tokens, pgmoe_model **out) {
     PG_TRY(validate_config(cfg));

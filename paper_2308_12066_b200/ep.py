@@ -175,6 +175,7 @@ class EPDecoder:
             self.y_recv = torch.zeros((srows, d), dtype=torch.float32, device=dev)
             self.back = torch.zeros((srows, d), dtype=torch.float32, device=dev)
             self.yw = torch.zeros((self.cap, d), dtype=torch.float32, device=dev)
+            self.mixb = torch.zeros((max_tokens, d), **bf)
 
     def block(self, b: int, x: torch.Tensor, r_in: DeviceRouting, stream=None):
         if self.packed:
@@ -207,9 +208,15 @@ class EPDecoder:
             ev[1].record(torch.cuda.current_stream() if stream is None else stream)
             self.ffn_events.append((ev[0], ev[1], self.lr.act_n[El:El + 1].clone()))
         ex.fixed(self.y_recv, self.back)                 # fp32 results back to their senders
+        y = torch.empty_like(x)
+        if k == 1:  # combine straight into the dense layer's bf16 operand (as the fused single-GPU epilogue)
+            _lib.check(L.pgmoe_ep_unpermute_padded_bf16(_ptr(self.back), ctypes.byref(r_in.c), T, d, P, El, cap,
+                                                        _ptr(self.mixb), s))
+            _lib.check(L.pgmoe_dense_forward_packed(_ptr(self.mixb), T, d, _ptr(self.model.matrix("non_moe", b)),
+                                                    _ptr(y), s))
+            return y
         _lib.check(L.pgmoe_ep_unpermute_padded(_ptr(self.back), ctypes.byref(r_in.c), T, d, k, P, El, cap,
                                                _ptr(self.yw), s))
-        y = torch.empty_like(x)
         from .core import _KERNEL
         _lib.check(L.pgmoe_dense_forward(_ptr(self.yw), T, d, k, _ptr(self.model.matrix("non_moe", b)),
                                          self.model.wdt, _ptr(y), _KERNEL[self.kernel], s))

@@ -525,7 +525,8 @@ def test_model_tcgen05_equals_teacher_forced_oracle_large_dims(placement):
 
 # ------------------------------------------------------ expert parallel ----
 
-def test_ep_decoder_single_rank_nccl_equals_single_gpu():
+@pytest.mark.parametrize("k", [1, 2])
+def test_ep_decoder_single_rank_nccl_equals_single_gpu(k):
     """EP plumbing on one rank (NCCL world of 1): dispatch/combine over NCCL,
     receiver routing and un-permute must reproduce the single-GPU decoder
     bit-for-bit."""
@@ -539,7 +540,7 @@ def test_ep_decoder_single_rank_nccl_equals_single_gpu():
     s.close()
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     try:
-        cfg = p.ModelConfig(d_model=256, d_ff=512, num_blocks=4, num_experts=16, top_k=2, activation_level=1)
+        cfg = p.ModelConfig(d_model=256, d_ff=512, num_blocks=4, num_experts=16, top_k=k, activation_level=1)
         x = p.token_inputs(cfg, 24)
         ep = EPDecoder(cfg, dtype="bf16", max_tokens=24)
         y_ep, ids_ep = ep.decoder_iteration(x, trace=True)
