@@ -213,6 +213,7 @@ struct pgmoe_model {
     cudaStream_t io_stream = nullptr;
     float *io_x = nullptr, *io_y = nullptr, *io_w = nullptr;
     int32_t *io_ids = nullptr;
+    int32_t *io_status = nullptr;  // pinned mirror of every routing buffer's status [R][4]
     std::mutex mu;
 };
 
@@ -1015,6 +1016,7 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     cudaFree(m->io_y);
     cudaFree(m->io_ids);
     cudaFree(m->io_w);
+    if (m->io_status) cudaFreeHost(m->io_status);
     if (m->cap) cudaStreamDestroy(m->cap);
     if (m->copy) cudaStreamDestroy(m->copy);
     cudaFree(m->dev_pool);
@@ -1390,6 +1392,7 @@ extern "C" int pgmoe_decoder_iteration_host(pgmoe_model *m, const float *x_in, i
             PG_CUDA(cudaMalloc(&m->io_y, cap_x));
             PG_CUDA(cudaMalloc(&m->io_ids, cap_t));
             PG_CUDA(cudaMalloc(&m->io_w, cap_t));
+            PG_CUDA(cudaHostAlloc(&m->io_status, m->routing.size() * 4 * sizeof(int32_t), cudaHostAllocDefault));
         }
     }
     cudaStream_t s = m->io_stream;
@@ -1402,6 +1405,11 @@ extern "C" int pgmoe_decoder_iteration_host(pgmoe_model *m, const float *x_in, i
             PG_CUDA(cudaMemcpyAsync(ids_trace, m->io_ids, tb, cudaMemcpyDeviceToHost, s));
             PG_CUDA(cudaMemcpyAsync(w_trace, m->io_w, tb, cudaMemcpyDeviceToHost, s));
         }
+        // routing statuses ride along (one synchronisation per call instead
+        // of a blocking copy per routing buffer afterwards)
+        for (size_t i = 0; i < m->routing.size(); ++i)
+            PG_CUDA(cudaMemcpyAsync(m->io_status + 4 * i, m->routing[i].r.status, 4 * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, s));
     }
     if (cudaStreamSynchronize(s) != cudaSuccess && st == PGMOE_OK) {
         set_error("decoder iteration failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -1409,7 +1417,12 @@ extern "C" int pgmoe_decoder_iteration_host(pgmoe_model *m, const float *x_in, i
     }
     if (st == PGMOE_OK) {
         std::lock_guard<std::mutex> g(m->mu);
-        st = check_all_routing(m);
+        bool clean = true;
+        for (size_t i = 0; i < m->routing.size(); ++i) {
+            clean &= m->io_status[4 * i] == 0;
+            m->stats.route_fallbacks = std::max<int64_t>(m->stats.route_fallbacks, m->io_status[4 * i + 1]);
+        }
+        if (!clean) st = check_all_routing(m);  // error path: message, reset
     }
     return st;
 }
