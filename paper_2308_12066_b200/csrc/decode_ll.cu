@@ -173,10 +173,20 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1
 // serial path (a handful of disabled stamps measured +4 us per block).
 #ifdef PGMOE_LL_PROBE
 __device__ __forceinline__ void dprobe(const Params &p, int b, int k) {
-    if (p.probe && b < 5) p.probe[(size_t)blockIdx.x * kProbeSlots + 1 + 8 * b + k] = gtimer();
+    if (p.probe && b < 4) p.probe[(size_t)blockIdx.x * kProbeSlots + 1 + 8 * b + k] = gtimer();
 }
+// block 2's cycle accumulators (thread ct 0 of the compute group): slot 33 + 4 * phase + {wait for
+// the slice, stage, gemv, epilogue}; 45 + phase: pieces
+#define PCLK(v) long long v = clock64()
+#define PACC(b, ph, k, t0)                                                                               \
+    do {                                                                                                 \
+        if (p.probe && (b) == 2 && ct == 0) p.probe[(size_t)blockIdx.x * kProbeSlots + 33 + 4 * (ph) + (k)] += \
+            (unsigned long long)(clock64() - (t0));                                                      \
+    } while (0)
 #else
 __device__ __forceinline__ void dprobe(const Params &, int, int) {}
+#define PCLK(v)
+#define PACC(b, ph, k, t0)
 #endif
 __device__ __forceinline__ void csync() { named_sync(1, kCThreads); }
 __device__ __forceinline__ void rsync() { named_sync(2, kRThreads); }
@@ -648,7 +658,9 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
             bool first = true;
             for (;;) {
                 const int slot = pc % kSlots;
+                PCLK(tw);
                 mbar_wait(&full[slot], (pc / kSlots) & 1);
+                PACC(b, ph, 0, tw);
                 const Piece &pd = desc[slot];
                 const int nrows = pd.nrows, ng = pd.ng, e = pd.e, row0 = pd.row0, end = pd.end;
                 if (nrows > 0) {
@@ -657,6 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                     // slot is released
                     const int my_t = (ct & 7) < ng ? pd.tok[ct & 7] : 0;
                     const float my_w = pd.w[ct & 7];
+                    PCLK(ts);
                     if (e != staged) {
                         if (ph == 0)
                             stage(act, d, ng, pd.tok, p.llx + (size_t)(b & 1) * T * d, d,
@@ -667,8 +680,12 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                         if (first && ct == 0) dprobe(p, b, ph == 0 ? 1 : 3);
                         first = false;
                     }
+                    PACC(b, ph, 1, ts);
+                    PCLK(tg);
                     piece_gemv(slots + (size_t)slot * kSlotB, K * 2 + 16, nrows, act, K * 2 + 16, ng, K, red, ct,
                                out, orow, otok);
+                    PACC(b, ph, 2, tg);
+                    PCLK(te);
                     if (orow >= 0 && orow < nrows && otok < ng) {
                         const int t = my_t;
                         if (ph == 0)
@@ -677,6 +694,10 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                         else  // top-1 combine: mix = w * y (linalg.py:45-51)
                             st_ll(p.llmix + (size_t)t * d + row0 + orow, ll_word(__float_as_uint(my_w * out), fl));
                     }
+                    PACC(b, ph, 3, te);
+#ifdef PGMOE_LL_PROBE
+                    if (p.probe && b == 2 && ct == 0) p.probe[(size_t)blockIdx.x * kProbeSlots + 45 + ph] += 1;
+#endif
                 } else {
                     csync();
                 }

@@ -54,7 +54,7 @@ def main():
            "exit": [round(float((rows[:, 41][rows[:, 41] > 0].min() - t0) / 1e3), 2),
                     round(float((rows[:, 41].max() - t0) / 1e3), 2)],
            "blocks": []}
-    for blk in range(5):
+    for blk in range(4):
         ent = {"block": blk}
         for k, nm in enumerate(EVENTS):
             v = rows[:, 1 + 8 * blk + k]
@@ -63,14 +63,17 @@ def main():
                 r = (v - t0) / 1e3
                 ent[nm] = [round(float(r.min()), 2), round(float(np.median(r)), 2), round(float(r.max()), 2)]
         out["blocks"].append(ent)
-    fine = {}
-    for k, nm in enumerate(["up_w_landed", "red_partials", "sel_inputs", "sel_logits", "up_issued", "sel_start"]):
-        v = rows[:, 42 + k]
-        v = v[v > 0]
-        if v.size:
-            r = (v - t0) / 1e3
-            fine[nm] = [round(float(r.min()), 2), round(float(np.median(r)), 2), round(float(r.max()), 2)]
-    out["block2_fine"] = fine
+    # block 2, compute group of each CTA: cycles waiting for the weight slice, staging, in the
+    # GEMV, in the epilogue; pieces (medians / maxima over CTAs that had pieces)
+    acc = {}
+    for ph, nm in enumerate(["up", "dn"]):
+        n = rows[:, 45 + ph]
+        sel = n > 0
+        acc[nm] = {"pieces_med": float(np.median(n[sel])) if sel.any() else 0}
+        for k, q in enumerate(["wait", "stage", "gemv", "epi"]):
+            v = rows[sel, 33 + 4 * ph + k]
+            acc[nm][q] = [int(np.median(v)), int(v.max())] if v.size else None
+    out["block2_cycles"] = acc
     print(json.dumps(out))
 
 
