@@ -161,6 +161,11 @@ PGMOE_API int pgmoe_ep_local_routing_padded(const uint16_t *recv, int32_t P, int
                                             const pgmoe_routing *out, pgmoe_stream_t stream);
 PGMOE_API int pgmoe_ep_pack_recv(const uint16_t *recv, const pgmoe_routing *local, int32_t El, int32_t n_max,
                                  int32_t d, uint16_t *xb, pgmoe_stream_t stream);
+/* pgmoe_ep_local_routing_padded + pgmoe_ep_pack_recv in one launch: the local
+ * routing (out) and the received rows packed in local-expert order (xb,
+ * P*cap rows max).  Same outputs as the two calls. */
+PGMOE_API int pgmoe_ep_recv_route_pack(const uint16_t *recv, int32_t P, int32_t El, int32_t cap, int32_t d,
+                                       const pgmoe_routing *out, uint16_t *xb, pgmoe_stream_t stream);
 PGMOE_API int pgmoe_expert_forward_packed(const uint16_t *xb, int32_t n_max, int32_t d, int32_t f,
                                           const void *experts, size_t expert_stride, const pgmoe_routing *r,
                                           uint16_t *hb, float *y, pgmoe_stream_t stream);

@@ -72,7 +72,8 @@ EXPORTS = (
     "pgmoe_unpermute_combine", "pgmoe_ep_local_routing", "pgmoe_model_config", "pgmoe_weight_file_config",
     "pgmoe_model_load_pgmoe1", "pgmoe_model_save_pgmoe1", "pgmoe_model_set_strategy", "pgmoe_model_set_cache",
     "pgmoe_cache_replay", "pgmoe_debug_set_probe", "pgmoe_model_set_fused_route",
-    "pgmoe_ep_pack_send", "pgmoe_ep_local_routing_padded", "pgmoe_ep_pack_recv", "pgmoe_expert_forward_packed",
+    "pgmoe_ep_pack_send", "pgmoe_ep_local_routing_padded", "pgmoe_ep_pack_recv", "pgmoe_ep_recv_route_pack",
+    "pgmoe_expert_forward_packed",
     "pgmoe_ep_unpermute_padded", "pgmoe_ep_unpermute_padded_bf16", "pgmoe_dense_forward_packed", "pgmoe_ep_slot_rows", "pgmoe_route_from_decisions", "pgmoe_decoder_iteration_ex",
     "pgmoe_model_check_routing", "pgmoe_gate_forward_f64", "pgmoe_debug_green_context",
     "pgmoe_model_set_decode", "pgmoe_model_decode_iterations",
@@ -147,6 +148,7 @@ def load():
         "pgmoe_ep_local_routing_padded": (i32, [vp, i32, i32, i32, i32, P(Routing), vp]),
         "pgmoe_ep_slot_rows": (i32, [i32, i32, i32]),
         "pgmoe_ep_pack_recv": (i32, [vp, P(Routing), i32, i32, i32, vp, vp]),
+        "pgmoe_ep_recv_route_pack": (i32, [vp, i32, i32, i32, i32, P(Routing), vp, vp]),
         "pgmoe_expert_forward_packed": (i32, [vp, i32, i32, i32, vp, sz, P(Routing), vp, vp, vp]),
         "pgmoe_ep_unpermute_padded": (i32, [vp, P(Routing), i32, i32, i32, i32, i32, i32, vp, vp]),
         "pgmoe_ep_unpermute_padded_bf16": (i32, [vp, P(Routing), i32, i32, i32, i32, i32, vp, vp]),

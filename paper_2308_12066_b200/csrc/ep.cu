@@ -134,6 +134,95 @@ __global__ void __launch_bounds__(256) ep_local_routing_kernel(const int *__rest
     }
 }
 
+// Received row of local routing position pos: expert e = the last with
+// off[e] <= pos (a non-empty range), then the sources in order (counts cnt[p][e],
+// rows of e inside source p's slot at src_off[p][e]).
+__device__ __forceinline__ int ep_row_of(int pos, const int *off, const int *cnt, const int *src_off, int P, int El,
+                                         int slot) {
+    int lo = 0, hi = El - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= pos) lo = mid;
+        else hi = mid - 1;
+    }
+    int j = pos - off[lo];
+    for (int p = 0; p < P; ++p) {
+        const int c = cnt[p * El + lo];
+        if (j < c) return p * slot + src_off[p * El + lo] + j;
+        j -= c;
+    }
+    return 0;  // unreachable for pos < total
+}
+
+// The receiver side of the fixed-size exchange in one launch: every CTA builds
+// the local routing tables from the counts headers in shared memory (E =
+// P*El ints); CTA 0 publishes them (the pgmoe_routing a single GPU would build
+// for the concatenated batch, as ep_local_routing_kernel) and all CTAs pack the
+// received bf16 rows into local-expert order (xb, the FFN's operand).
+__global__ void __launch_bounds__(256) ep_recv_route_pack_kernel(const uint16_t *__restrict__ recv,
+                                                                 const int *__restrict__ cnt_g, int cnt_stride, int P,
+                                                                 int El, int slot, int d, int n_max, pgmoe_routing r,
+                                                                 uint16_t *__restrict__ xb) {
+    extern __shared__ int sm[];
+    int *cnt = sm;                   // [P][El] counts
+    int *src_off = cnt + P * El;     // [P][El] -> offsets of expert e inside source p's rows
+    int *hist = src_off + P * El;    // [El]    -> exclusive scan: off
+    int *actf = hist + El;           // [El]    -> exclusive scan: position in act
+    int *wt = actf + El;             // [8]
+    const int tid = threadIdx.x;
+    const bool pub = blockIdx.x == 0;
+    for (int i = tid; i < P * El; i += blockDim.x) {
+        const int v = __ldg(cnt_g + (size_t)(i / El) * cnt_stride + i % El);
+        cnt[i] = v;
+        src_off[i] = v;
+    }
+    __syncthreads();
+    for (int e = tid; e < El; e += blockDim.x) {
+        int h = 0;
+        for (int p = 0; p < P; ++p) h += cnt[p * El + e];
+        hist[e] = h;
+        actf[e] = h > 0;
+        if (pub) r.hist[e] = h;
+    }
+    __syncthreads();
+    for (int p = 0; p < P; ++p) block_exclusive_scan(src_off + p * El, El, wt);
+    const int total = block_exclusive_scan(hist, El, wt);
+    const int nact = block_exclusive_scan(actf, El, wt);
+    if (pub) {
+        for (int e = tid; e < El; e += blockDim.x) {
+            r.off[e] = hist[e];
+            if ((e + 1 < El ? hist[e + 1] : total) > hist[e]) r.act[actf[e]] = e;
+        }
+        if (tid == 0) {
+            r.off[El] = total;
+            *r.n_act = nact;
+        }
+        for (int pos = tid; pos < total; pos += blockDim.x) {
+            const int row = ep_row_of(pos, hist, cnt, src_off, P, El, slot);
+            r.perm[pos] = row;
+            r.w_perm[pos] = 1.0f;
+            if (r.ids || r.w) {
+                int lo = 0, hi = El - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (hist[mid] <= pos) lo = mid;
+                    else hi = mid - 1;
+                }
+                if (r.ids) r.ids[row] = lo;
+                if (r.w) r.w[row] = 1.0f;
+            }
+        }
+    }
+    const int vec = d / 8, n = min(n_max, total);
+    for (long long i = blockIdx.x * (long long)blockDim.x + tid; i < (long long)n * vec;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int pos = (int)(i / vec), c = (int)(i - (long long)pos * vec);
+        const int row = ep_row_of(pos, hist, cnt, src_off, P, El, slot);
+        reinterpret_cast<uint4 *>(xb)[(size_t)pos * vec + c] =
+            __ldg(reinterpret_cast<const uint4 *>(recv) + (size_t)row * vec + c);
+    }
+}
+
 // ---- fixed-size (padded) exchange: no host round trip for split sizes ----
 // Rank p owns experts [p*El, (p+1)*El), so K1's expert-grouped permutation
 // sends a contiguous run of routing positions to each peer: positions
@@ -301,6 +390,22 @@ extern "C" int pgmoe_ep_local_routing_padded(const uint16_t *recv, int32_t P, in
     PG_REQUIRE(d % 2 == 0, PGMOE_E_SHAPE, "ep header needs an even d");
     ep_local_routing_kernel<<<1, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(cnt, slot * d / 2, P, El, slot,
                                                                                       *out);
+    PG_CUDA(cudaGetLastError());
+    count_launch();
+    return PGMOE_OK;
+}
+
+extern "C" int pgmoe_ep_recv_route_pack(const uint16_t *recv, int32_t P, int32_t El, int32_t cap, int32_t d,
+                                        const pgmoe_routing *out, uint16_t *xb, pgmoe_stream_t stream) {
+    PG_REQUIRE(P >= 1 && El >= 1 && cap >= 1 && d >= 1, PGMOE_E_CONFIG, "bad EP shape P=%d El=%d cap=%d", P, El, cap);
+    PG_REQUIRE(d % 8 == 0, PGMOE_E_SHAPE, "ep_recv_route_pack needs d %% 8 == 0");
+    const size_t smem = (size_t)(2 * P * El + 2 * El + 8) * 4;
+    PG_REQUIRE(smem <= 48 * 1024, PGMOE_E_CONFIG, "EP routing table too large");
+    const int slot = cap + ep_header_rows(El, d);
+    const int *cnt = reinterpret_cast<const int *>(recv + (size_t)cap * d);  // source p's header: slot * d / 2 ints apart
+    const int n_max = P * cap;
+    ep_recv_route_pack_kernel<<<grid_for((long long)n_max * d / 8), 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+        recv, cnt, slot * d / 2, P, El, slot, d, n_max, *out, xb);
     PG_CUDA(cudaGetLastError());
     count_launch();
     return PGMOE_OK;

@@ -192,8 +192,9 @@ class EPDecoder:
         s = _stream(stream)
         _lib.check(L.pgmoe_ep_pack_send(_ptr(x), ctypes.byref(r_in.c), T, d, k, P, El, cap, _ptr(self.send), s))
         ex.fixed(self.send, self.recv)                   # bf16 rows + counts header, one slot per peer
-        _lib.check(L.pgmoe_ep_local_routing_padded(_ptr(self.recv), P, El, cap, d, ctypes.byref(self.lr.c), s))
-        _lib.check(L.pgmoe_ep_pack_recv(_ptr(self.recv), ctypes.byref(self.lr.c), El, P * cap, d, _ptr(self.xb), s))
+        # receiver routing + rows packed in local-expert order, one launch
+        _lib.check(L.pgmoe_ep_recv_route_pack(_ptr(self.recv), P, El, cap, d, ctypes.byref(self.lr.c),
+                                              _ptr(self.xb), s))
         base, stride = ctypes.c_void_p(), ctypes.c_size_t()
         eb, nl = ctypes.c_int32(), ctypes.c_int32()
         _lib.check(L.pgmoe_model_expert_records(self.model._h, b, ctypes.byref(base), ctypes.byref(stride),

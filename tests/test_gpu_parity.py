@@ -724,3 +724,48 @@ def test_activation_levels_wiring_and_migration(level, placement):
         assert torch.equal(ids2, ids) and torch.equal(y2, y)
         off.close()
     res.close()
+
+
+@pytest.mark.parametrize("Pn,El", [(1, 128), (3, 16), (8, 16)])
+def test_ep_recv_route_pack_equals_two_launches(Pn, El):
+    """pgmoe_ep_recv_route_pack (receiver routing + packing in one launch) ==
+    pgmoe_ep_local_routing_padded then pgmoe_ep_pack_recv, bit for bit, on a
+    received slot buffer with random in-band counts (empty experts and empty
+    sources included)."""
+    import ctypes
+    p = P()
+    from paper_2308_12066_b200 import _lib
+    L = _lib.load()
+    d, cap = 256, 40
+    slot = int(L.pgmoe_ep_slot_rows(cap, El, d))
+    g = torch.Generator().manual_seed(7 + Pn)
+    recv = torch.randn((Pn * slot, d), generator=g).to(torch.bfloat16)
+    for q in range(Pn):
+        cnt = torch.zeros(El, dtype=torch.int32)
+        n = 0 if q == 1 else int(torch.randint(0, cap + 1, (1,), generator=g))
+        for _ in range(n):
+            cnt[int(torch.randint(0, El // 2 if El > 2 else El, (1,), generator=g)) * 2 % El] += 1
+        hdr = recv[q * slot + cap:(q + 1) * slot].contiguous().view(torch.int32).view(-1)
+        hdr[:El] = cnt
+        recv[q * slot + cap:(q + 1) * slot] = hdr.view(torch.bfloat16).view(-1, d)
+    recv = recv.cuda()
+    outs = []
+    for fused in (False, True):
+        lr = p.DeviceRouting(Pn * slot, El, 1)
+        xb = torch.zeros((Pn * cap, d), dtype=torch.bfloat16, device="cuda")
+        if fused:
+            _lib.check(L.pgmoe_ep_recv_route_pack(recv.data_ptr(), Pn, El, cap, d, ctypes.byref(lr.c),
+                                                  xb.data_ptr(), None))
+        else:
+            _lib.check(L.pgmoe_ep_local_routing_padded(recv.data_ptr(), Pn, El, cap, d, ctypes.byref(lr.c), None))
+            _lib.check(L.pgmoe_ep_pack_recv(recv.data_ptr(), ctypes.byref(lr.c), El, Pn * cap, d, xb.data_ptr(),
+                                            None))
+        torch.cuda.synchronize()
+        outs.append((lr, xb))
+    (a, xa), (b, xb2) = outs
+    total = int(a.off[El].item())
+    assert total > 0
+    for name in ("hist", "off", "act_n", "ids", "w"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+    assert torch.equal(a.perm[:total], b.perm[:total]) and torch.equal(a.w_perm[:total], b.w_perm[:total])
+    assert torch.equal(xa[:total], xb2[:total])
