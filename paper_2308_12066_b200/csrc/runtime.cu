@@ -214,6 +214,7 @@ struct pgmoe_model {
     float *io_x = nullptr, *io_y = nullptr, *io_w = nullptr;
     int32_t *io_ids = nullptr;
     int32_t *io_status = nullptr;  // pinned mirror of every routing buffer's status [R][4]
+    int32_t *status_dev = nullptr; // the routing buffers' status words [R][4] (routing[i].r.status)
     std::mutex mu;
 };
 
@@ -922,6 +923,12 @@ extern "C" int pgmoe_model_create_ex(const pgmoe_config *cfg, int32_t wdtype, in
         if ((st = alloc_routing(m->routing[i], max_tokens, c.num_experts, (int)k)) != PGMOE_OK) return fail(st);
         cudaEventCreateWithFlags(&m->routed[i], cudaEventDisableTiming);
     }
+    // every routing buffer's status words side by side: the host-buffer entry
+    // point fetches them with one copy
+    if (cudaMalloc(&m->status_dev, (size_t)R * 4 * sizeof(int32_t)) != cudaSuccess ||
+        cudaMemset(m->status_dev, 0, (size_t)R * 4 * sizeof(int32_t)) != cudaSuccess)
+        return fail(PGMOE_E_OOM);
+    for (int i = 0; i < R; ++i) m->routing[i].r.status = m->status_dev + 4 * i;
     size_t rws = pgmoe_route_workspace_bytes(max_tokens, c.num_experts);
     for (int t = 1; t <= max_tokens; ++t)  // the routing role fused into the block kernel (resident)
         rws = std::max(rws, kFusedRouteHead + fused_route_ws_bytes(t, d, c.num_experts, device_sm_count()));
@@ -1017,6 +1024,7 @@ extern "C" int pgmoe_model_destroy(pgmoe_model *m) {
     cudaFree(m->io_ids);
     cudaFree(m->io_w);
     if (m->io_status) cudaFreeHost(m->io_status);
+    if (m->status_dev) cudaFree(m->status_dev);
     if (m->cap) cudaStreamDestroy(m->cap);
     if (m->copy) cudaStreamDestroy(m->copy);
     cudaFree(m->dev_pool);
@@ -1407,9 +1415,8 @@ extern "C" int pgmoe_decoder_iteration_host(pgmoe_model *m, const float *x_in, i
         }
         // routing statuses ride along (one synchronisation per call instead
         // of a blocking copy per routing buffer afterwards)
-        for (size_t i = 0; i < m->routing.size(); ++i)
-            PG_CUDA(cudaMemcpyAsync(m->io_status + 4 * i, m->routing[i].r.status, 4 * sizeof(int32_t),
-                                    cudaMemcpyDeviceToHost, s));
+        PG_CUDA(cudaMemcpyAsync(m->io_status, m->status_dev, m->routing.size() * 4 * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, s));
     }
     if (cudaStreamSynchronize(s) != cudaSuccess && st == PGMOE_OK) {
         set_error("decoder iteration failed: %s", cudaGetErrorString(cudaGetLastError()));
