@@ -196,7 +196,8 @@ __device__ __forceinline__ void rsync() { named_sync(2, kRThreads); }
 // Returns through `out` (thread ct < mt*128 owns output (ct / 8, ct % 8) of
 // its m-tile); rows past nrows repeat the last row (results discarded).
 __device__ __forceinline__ void piece_gemv(const unsigned char *A, int apitch, int nrows, const unsigned char *B,
-                                           int bpitch, int brows, int K, float *red, int ct, float &out, int &orow, int &otok) {
+                                           int bpitch, int brows, int K, float *red, int ct, float &out, int &orow, int &otok,
+                                           uint64_t *release = nullptr) {
     const int w = ct >> 5, lane = ct & 31, g = lane >> 2, t4 = lane & 3;
     const int mt = nrows > 16 ? 2 : 1, S = kCWarps / mt;
     const int m = w / S, s = w - m * S;
@@ -216,6 +217,10 @@ __device__ __forceinline__ void piece_gemv(const unsigned char *A, int apitch, i
         const uint32_t b0 = *reinterpret_cast<const uint32_t *>(bp + o);
         const uint32_t b1 = *reinterpret_cast<const uint32_t *>(bp + o + 16);
         mma_bf16(c, a0, a1, a2, a3, b0, b1);
+    }
+    if (release) {  // this warp is done reading the slot: the producer may refill it now
+        __syncwarp();
+        if (lane == 0) mbar_arrive(release);
     }
     // red[w][row 0..15][tok 0..7]
     float *rw = red + w * 128;
@@ -348,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
     if (tid == 0) {
         for (int i = 0; i < kSlots; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            mbar_init(&empty[i], kCWarps);  // each compute warp releases a slot after its last read
         }
         mbar_init(dfull, 1);
         mbar_init(dempty, 1);
@@ -683,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                     PACC(b, ph, 1, ts);
                     PCLK(tg);
                     piece_gemv(slots + (size_t)slot * kSlotB, K * 2 + 16, nrows, act, K * 2 + 16, ng, K, red, ct,
-                               out, orow, otok);
+                               out, orow, otok, &empty[slot]);
                     PACC(b, ph, 2, tg);
                     PCLK(te);
                     if (orow >= 0 && orow < nrows && otok < ng) {
@@ -699,9 +704,9 @@ __global__ void __launch_bounds__(kThreads, 1) ll_decode_kernel(const __grid_con
                     if (p.probe && b == 2 && ct == 0) p.probe[(size_t)blockIdx.x * kProbeSlots + 45 + ph] += 1;
 #endif
                 } else {
-                    csync();
+                    __syncwarp();
+                    if ((ct & 31) == 0) mbar_arrive(&empty[slot]);  // one arrival per compute warp
                 }
-                if (ct == 0) mbar_arrive(&empty[slot]);  // piece_gemv's trailing barrier: everyone is done reading
                 ++pc;
                 if (end) break;
             }
