@@ -202,18 +202,22 @@ __device__ __forceinline__ void piece_gemv(const unsigned char *A, int apitch, i
     const int mt = nrows > 16 ? 2 : 1, S = kCWarps / mt;
     const int m = w / S, s = w - m * S;
     const int KS = K / 16, k0 = KS * s / S, k1 = KS * (s + 1) / S;
-    const int r0 = min(m * 16 + g, nrows - 1), r1 = min(m * 16 + g + 8, nrows - 1);
-    const unsigned char *a0p = A + (size_t)r0 * apitch + t4 * 4;
-    const unsigned char *a1p = A + (size_t)r1 * apitch + t4 * 4;
+    // A fragments with one ldmatrix.x4 per k-step: lanes 0-15 address rows
+    // 0-15 of the m-tile at k, lanes 16-31 the same rows at k + 8
+    const int lr = min(m * 16 + (lane & 15), nrows - 1);
+    const uint32_t abase = (uint32_t)__cvta_generic_to_shared(A + (size_t)lr * apitch + (lane >> 4) * 16);
     const unsigned char *bp = B + (size_t)min(g, brows - 1) * bpitch + t4 * 4;  // staged rows only
     float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
     for (int ks = k0; ks < k1; ++ks) {
         const int o = ks * 32;
-        const uint32_t a0 = *reinterpret_cast<const uint32_t *>(a0p + o);
-        const uint32_t a1 = *reinterpret_cast<const uint32_t *>(a1p + o);
-        const uint32_t a2 = *reinterpret_cast<const uint32_t *>(a0p + o + 16);
-        const uint32_t a3 = *reinterpret_cast<const uint32_t *>(a1p + o + 16);
+        uint32_t a0, a1, a2, a3;
+        // not volatile (the k-steps' loads may be issued ahead of the mmas); the
+        // memory clobber keeps it behind the slot's barrier wait
+        asm("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+            : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+            : "r"(abase + o)
+            : "memory");
         const uint32_t b0 = *reinterpret_cast<const uint32_t *>(bp + o);
         const uint32_t b1 = *reinterpret_cast<const uint32_t *>(bp + o + 16);
         mma_bf16(c, a0, a1, a2, a3, b0, b1);
