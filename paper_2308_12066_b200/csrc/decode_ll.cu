@@ -255,7 +255,7 @@ __device__ __forceinline__ void piece_gemv(const unsigned char *A, int apitch, i
 __device__ __forceinline__ void stage(unsigned char *act, int K, int ng, const int *tok,
                                       const unsigned long long *ll, size_t ll_stride, const float *plain,
                                       size_t plain_stride, uint32_t flag, int ct) {
-    constexpr int U = 8;
+    constexpr int U = 4;
     const int apitch = K * 2 + 16;
     const int npair = K / 2, n_all = ng * npair;
     for (int i0 = ct; i0 < n_all; i0 += U * kCThreads) {
