@@ -1,5 +1,6 @@
 #!/bin/bash
 # K1 cluster size sweep (PGMOE_ROUTE_S) with tools/route_bench.py on the _build_B library.
+# (historical: the PGMOE_ROUTE_S override was removed from route.cu after this sweep — no effect)
 cd "$GRAFT_REPO_ROOT"
 OUT=gpurun_out/r2routeS; rm -rf $OUT; mkdir -p $OUT
 for S in 0 2 4 8 16; do
