@@ -733,29 +733,39 @@ __global__ void __launch_bounds__(kLogitThreads) route_cluster_kernel(const Rout
     if (nown > 0) {
         double gam, bscale;
         bound_constants<GT, float>(d, &gam, &bscale);
-        __syncthreads();  // every thread is past its partial loop: r0 is free
+        // the owned tokens' slice sums |x| over the cluster, once per token (rank order)
+        __shared__ double s_sx[kSelectWarps];
+        if (tid < nown) {
+            double xv[kClusterMaxS];
+#pragma unroll
+            for (int z = 0; z < kClusterMaxS; ++z) xv[z] = z < S ? cl.map_shared_rank(sxs, z)[own0 + tid] : 0.0;
+            double sx = 0.0;
+#pragma unroll
+            for (int z = 0; z < kClusterMaxS; ++z)
+                if (z < S) sx += xv[z];
+            s_sx[tid] = sx;
+        }
+        __syncthreads();  // every thread is past its partial loop: r0 is free; s_sx written
         double *lgs = reinterpret_cast<double *>(smem_raw + L.r0);
         for (int q = tid; q < nown * E; q += kLogitThreads) {
             const int tl = q / E, j = q - tl * E;
-            // one round of DSMEM loads: the S partials, column maxima and
-            // slice sums |x| (the latter redundantly per thread)
-            double pv[kClusterMaxS], xv[kClusterMaxS];
+            // one round of DSMEM loads: the S partials and column maxima
+            double pv[kClusterMaxS];
             float cv[kClusterMaxS];
 #pragma unroll
             for (int z = 0; z < kClusterMaxS; ++z) {
                 pv[z] = z < S ? cl.map_shared_rank(part, z)[(own0 + tl) * E + j] : 0.0;
                 cv[z] = z < S ? cl.map_shared_rank(scm, z)[j] : 0.f;
-                xv[z] = z < S ? cl.map_shared_rank(sxs, z)[own0 + tl] : 0.0;
             }
-            double sum = 0.0, sx = 0.0;
+            double sum = 0.0;
             float cm = 0.f;
 #pragma unroll
             for (int z = 0; z < kClusterMaxS; ++z)  // fixed order: deterministic
                 if (z < S) {
                     sum += pv[z];
                     cm = fmaxf(cm, cv[z]);
-                    sx += xv[z];
                 }
+            const double sx = s_sx[tl];
             lgs[tl * 2 * E + j] = sum;
             lgs[tl * 2 * E + E + j] = bscale * (sx * (1.0 + 2.0 * gam)) * (double)cm + 1e-300;
         }
