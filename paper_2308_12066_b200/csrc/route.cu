@@ -823,7 +823,10 @@ __global__ void __launch_bounds__(kLogitThreads) route_cluster_kernel(const Rout
         select_tokens<GT, float>(p, t0 + own0, nown, smem_raw + L.r0);
         if (p.T > TOK) __threadfence();  // ids / weights visible GPU-wide before rank 0's ticket
     }
-    cl.sync();  // the tile's ids / weights written; nobody reads remote shared memory any more
+    // every token of the tile owned by rank 0 (a one-token tile): the pushes
+    // are complete and nobody reads remote shared memory any more, so the
+    // other ranks are done and rank 0 needs no second barrier
+    if (!(kPush && ntok <= c)) cl.sync();  // the tile's ids / weights written by their owners
     if (rank != 0) return;
     if (tid == 0) probe(p.probe, cta, 4);  // tile selected
     // 6. permutation: one tile -> straight away; several -> the last tile
