@@ -59,7 +59,8 @@ struct RouteParams {
 };
 
 template <typename GT, typename XT>
-__device__ void select_tokens(const RouteParams &p, int tok0, int ntok, unsigned char *base);
+__device__ void select_tokens(const RouteParams &p, int tok0, int ntok, unsigned char *base, int *m_ids = nullptr,
+                              float *m_w = nullptr);
 
 // fp32/bf16 operands: products exact, d - 1 roundings on either side;
 // fp64 operands: one more (the product), gamma_{d+1}
@@ -128,7 +129,8 @@ __device__ void select_tile(const RouteParams &p, int tile, int tok0, int ntok, 
 // token, from shared memory: token w's fp64 logits at base + w * 2E and
 // their error bounds right after them (E doubles each).
 template <typename GT, typename XT>
-__device__ void select_tokens(const RouteParams &p, int tok0, int ntok, unsigned char *base) {
+__device__ void select_tokens(const RouteParams &p, int tok0, int ntok, unsigned char *base, int *m_ids,
+                              float *m_w) {
     const int d = p.d, E = p.E, k = p.k;
     const GT *G = static_cast<const GT *>(p.G);
     const XT *X = static_cast<const XT *>(p.x);
@@ -195,6 +197,10 @@ __device__ void select_tokens(const RouteParams &p, int tok0, int ntok, unsigned
             for (int s = lane; s < k; s += 32) {
                 p.out.ids[(size_t)tok * k + s] = 0;
                 p.out.w[(size_t)tok * k + s] = 0.f;
+                if (m_ids) {
+                    m_ids[(size_t)tok * k + s] = 0;
+                    m_w[(size_t)tok * k + s] = 0.f;
+                }
             }
         } else {
             if (!certified) {
@@ -235,6 +241,10 @@ __device__ void select_tokens(const RouteParams &p, int tok0, int ntok, unsigned
                     if (!(pr > 0.0)) atomicCAS(p.out.status, 0, (int)PGMOE_E_GATE_UNDERFLOW);
                     p.out.ids[(size_t)tok * k + s] = sel[s];
                     p.out.w[(size_t)tok * k + s] = __double2float_rn(pr);
+                    if (m_ids) {  // shared-memory copy (the caller permutes from it)
+                        m_ids[(size_t)tok * k + s] = sel[s];
+                        m_w[(size_t)tok * k + s] = __double2float_rn(pr);
+                    }
                 }
             }
         }
@@ -245,11 +255,11 @@ __device__ void select_tokens(const RouteParams &p, int tok0, int ntok, unsigned
 // ids in registers (no shared-memory histogram, no block barriers): row r
 // goes to #{rows with a smaller expert} + #{earlier rows, same expert}, the
 // same stable order permute_all builds.
-__device__ void permute_warp(const RouteParams &p) {
+__device__ void permute_warp(const RouteParams &p, const int *s_ids = nullptr, const float *s_w = nullptr) {
     const int E = p.E, N = p.T * p.k, lane = threadIdx.x & 31;
     const bool v = lane < N;
-    const int e = v ? __ldcg(p.out.ids + lane) : 0x7fffffff;
-    const float w = v ? __ldcg(p.out.w + lane) : 0.f;
+    const int e = v ? (s_ids ? s_ids[lane] : __ldcg(p.out.ids + lane)) : 0x7fffffff;
+    const float w = v ? (s_w ? s_w[lane] : __ldcg(p.out.w + lane)) : 0.f;
     int ev[32];
 #pragma unroll
     for (int l = 0; l < 32; ++l) ev[l] = __shfl_sync(0xffffffffu, e, l);
@@ -737,6 +747,8 @@ __global__ void __launch_bounds__(kLogitThreads) route_cluster_kernel(const Rout
     //     round trip after it; measured -0.4 us at T=1, slower at T >= 8)
     constexpr bool kPush = TOK <= 2;
     const int c = (TOK + S - 1) / S;
+    __shared__ int s_sel_ids[TOK * 8];  // one-token tiles: the selection, for the permutation (k <= 8)
+    __shared__ float s_sel_w[TOK * 8];
     if constexpr (kPush) {
         __syncthreads();  // part / scm / sxs complete
         double *rp = reinterpret_cast<double *>(smem_raw + L.rp);
@@ -820,7 +832,10 @@ __global__ void __launch_bounds__(kLogitThreads) route_cluster_kernel(const Rout
         __syncthreads();
         if (tid == 0) probe(p.probe, cta, 3);  // cluster sums done
         // 5. certified selection + softmax (one warp per token)
-        select_tokens<GT, float>(p, t0 + own0, nown, smem_raw + L.r0);
+        if (kPush && ntok <= c)  // one-token tile: rank 0 permutes from its own copy
+            select_tokens<GT, float>(p, t0 + own0, nown, smem_raw + L.r0, s_sel_ids, s_sel_w);
+        else
+            select_tokens<GT, float>(p, t0 + own0, nown, smem_raw + L.r0);
         if (p.T > TOK) __threadfence();  // ids / weights visible GPU-wide before rank 0's ticket
     }
     // every token of the tile owned by rank 0 (a one-token tile): the pushes
@@ -840,7 +855,14 @@ __global__ void __launch_bounds__(kLogitThreads) route_cluster_kernel(const Rout
     }
     if (tid == 0) probe(p.probe, cta, 5);
     if (p.T * p.k <= 32) {
-        if (warp == 0) permute_warp(p);
+        if (warp == 0) {
+            if (kPush && ntok <= c && p.T <= TOK) {
+                __syncwarp();
+                permute_warp(p, s_sel_ids, s_sel_w);
+            } else {
+                permute_warp(p);
+            }
+        }
     } else {
         permute_all(p, smem_raw + L.r0);
     }
