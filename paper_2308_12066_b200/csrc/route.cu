@@ -298,6 +298,61 @@ __device__ void permute_warp(const RouteParams &p, const int *s_ids = nullptr, c
     }
 }
 
+// permute_warp with the histogram in shared memory (`scratch`: E ints; ids
+// and weights from `s_ids` / `s_w` or, when null, from the outputs): N
+// smem atomics, one warp scan over E / 32 expert blocks, and the rank of a
+// row among its expert's rows by __match_any_sync — no 32-way compare loop
+// per expert block.  Same outputs as permute_warp.
+__device__ void permute_warp_smem(const RouteParams &p, const int *s_ids, const float *s_w, int *scratch) {
+    const int E = p.E, N = p.T * p.k, lane = threadIdx.x & 31;
+    const bool v = lane < N;
+    const int e = v ? (s_ids ? s_ids[lane] : __ldcg(p.out.ids + lane)) : -1;
+    const float w = v ? (s_w ? s_w[lane] : __ldcg(p.out.w + lane)) : 0.f;
+    for (int ex = lane; ex < E; ex += 32) scratch[ex] = 0;
+    __syncwarp();
+    if (v) atomicAdd(&scratch[e], 1);
+    __syncwarp();
+    const int epl = (E + 31) / 32, b0 = min(E, lane * epl), b1 = min(E, b0 + epl);
+    int cnt = 0, na = 0;
+    for (int ex = b0; ex < b1; ++ex) {
+        const int h = scratch[ex];
+        cnt += h;
+        na += h > 0;
+    }
+    int ic = cnt, ia = na;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int c2 = __shfl_up_sync(0xffffffffu, ic, o), a2 = __shfl_up_sync(0xffffffffu, ia, o);
+        if (lane >= o) {
+            ic += c2;
+            ia += a2;
+        }
+    }
+    const int nact = __shfl_sync(0xffffffffu, ia, 31);
+    int run = ic - cnt, arun = ia - na;
+    __syncwarp();  // every lane has read its counts
+    for (int ex = b0; ex < b1; ++ex) {
+        const int h = scratch[ex];
+        p.out.hist[ex] = h;
+        p.out.off[ex] = run;
+        if (h > 0) p.out.act[arun++] = ex;
+        scratch[ex] = run;  // offset, for the rows below
+        run += h;
+    }
+    const unsigned same = __match_any_sync(0xffffffffu, e);
+    __syncwarp();
+    if (v) {
+        const int pos = scratch[e] + __popc(same & ((1u << lane) - 1u));
+        p.out.perm[pos] = lane;
+        if (p.out.inv) p.out.inv[lane] = pos;
+        p.out.w_perm[pos] = w;
+    }
+    if (lane == 0) {
+        p.out.off[E] = N;
+        *p.out.n_act = nact;
+    }
+}
+
 // Phase 3: histogram, exclusive scan, stable permutation, active list.
 __device__ void permute_all(const RouteParams &p, unsigned char *smem_raw) {
     const int E = p.E, k = p.k;
@@ -856,12 +911,10 @@ __global__ void __launch_bounds__(kLogitThreads) route_cluster_kernel(const Rout
     if (tid == 0) probe(p.probe, cta, 5);
     if (p.T * p.k <= 32) {
         if (warp == 0) {
-            if (kPush && ntok <= c && p.T <= TOK) {
-                __syncwarp();
-                permute_warp(p, s_sel_ids, s_sel_w);
-            } else {
-                permute_warp(p);
-            }
+            const bool own = kPush && ntok <= c && p.T <= TOK;  // rank 0 selected every row
+            __syncwarp();
+            permute_warp_smem(p, own ? s_sel_ids : nullptr, own ? s_sel_w : nullptr,
+                              reinterpret_cast<int *>(smem_raw + L.r0));
         }
     } else {
         permute_all(p, smem_raw + L.r0);
