@@ -1,3 +1,6 @@
+#!/bin/bash
+# Block launch with narrow N tiles (PGMOE_BN=16/32 on a _build_B carrying those instantiations).
+# (historical: measured no gain and removed; results in profiles/r2/l2_prefetch/narrow_n_tiles.txt)
 cd "$GRAFT_REPO_ROOT"
 export PGMOE_LIB_PATH=paper_2308_12066_b200/_build_B/libpgmoe.so
 mkdir -p gpurun_out/bnab

@@ -1,5 +1,6 @@
 #!/bin/bash
 # A/B: route-kernel shared-memory carveout (PGMOE_ROUTE_CARVEOUT=0 restores the driver's choice) on the default bench.
+# (historical: the PGMOE_ROUTE_CARVEOUT knob was measured identical and removed; results in profiles/r2/launch_gap/)
 cd "$GRAFT_REPO_ROOT"
 OUT=gpurun_out/r2carve${TAG}; rm -rf $OUT; mkdir -p $OUT
 for rep in 1 2; do for cv in 0 1; do

@@ -1,5 +1,6 @@
 #!/bin/bash
 # LL decoder ring / row-group / partition sweep on one build (PGMOE_LIB_PATH=_build_B): env combos x shapes.
+# (historical: PGMOE_LL_GROUP / PGMOE_LL_ALIGN existed only in the measured variant, see profiles/r2/ll_chunk/attempt.diff)
 cd "$GRAFT_REPO_ROOT"
 OUT=gpurun_out/r2lls${TAG}; rm -rf $OUT; mkdir -p $OUT
 L=paper_2308_12066_b200/_build_${V:-B}/libpgmoe.so
